@@ -1,0 +1,166 @@
+/*
+ * dsp_b200.h -- C ABI of the B200-native Diversely-Stale-Parameters (DSP)
+ * train step (arXiv 1909.02625).  Plain pointers and sizes only; no torch
+ * types.  Every function returns 0 on success or a DSP_E* code; the message
+ * of the last failure on the calling thread is in dsp_last_error().
+ *
+ * The reference (`stalepipe`, pure Python/numpy) has no FFI; its per-block
+ * work is three Python calls inside TrainEngine._iterate_block
+ * (/root/reference/pkg/src/stalepipe/pipeline.py:538-606):
+ *
+ *   block_forward(block, h_in, record)   blocks.py:96-118   -> dsp_block_forward
+ *   softmax_xent(logits, labels)         tensor.py:86-111   -> dsp_block_loss
+ *   block_backward(block, tape, u)       blocks.py:121-154  -> dsp_block_backward
+ *   g = grad + wd*params; apply_update   pipeline.py:591-596,
+ *                                        optim.py:48-109    -> dsp_block_update
+ *
+ * The queues / FIFO indexing (pipeline.py:148-205, 483-513) stay on the host
+ * side (Python mirror of the reference) and pass device ring-slot pointers in.
+ * INTEGRATION.md shows the ctypes binding a `stalepipe` maintainer would add.
+ */
+#ifndef DSP_B200_H_
+#define DSP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ error codes */
+#define DSP_OK 0
+#define DSP_E_INVALID 1   /* bad argument / shape (reference: ShapeError, ValueError) */
+#define DSP_E_CUDA 2      /* CUDA runtime failure */
+#define DSP_E_STATE 3     /* call order violated (reference: RuntimeError "tape already consumed") */
+#define DSP_E_NONFINITE 4 /* non-finite values (reference: NonFiniteError, tensor.py:23-37) */
+
+/* ------------------------------------------------------------ enums */
+#define DSP_DTYPE_BF16 0 /* bf16 storage, kind::f16 tensor-core MMA, fp32 accumulate */
+#define DSP_DTYPE_F32 1  /* fp32 storage, kind::tf32 tensor-core MMA, fp32 accumulate */
+
+#define DSP_IGEMM_FPROP 0
+#define DSP_IGEMM_DGRAD 1
+#define DSP_IGEMM_WGRAD 2
+
+/* Layer kinds.  0..2 are the reference's own (blocks.py:21-33); the rest are
+ * the CNN kinds the BASELINE configs need (ResNet units at residual-unit
+ * granularity). */
+#define DSP_LAYER_DENSE 0
+#define DSP_LAYER_RELU 1
+#define DSP_LAYER_TANH 2
+#define DSP_LAYER_CONV_BN_RELU 10 /* conv kxk + BatchNorm + ReLU (stem) */
+#define DSP_LAYER_BASIC_UNIT 11   /* 2x conv3x3-BN (+1x1 projection-BN) + residual + ReLU */
+#define DSP_LAYER_BOTTLENECK 12   /* conv1x1-BN-ReLU, conv3x3-BN-ReLU, conv1x1-BN, shortcut, ReLU */
+#define DSP_LAYER_AVGPOOL 13      /* global average pool (B,H,W,C) -> (B,C) */
+#define DSP_LAYER_MAXPOOL 14      /* 3x3 stride-2 pad-1 max pool (ResNet-50 stem) */
+
+#define DSP_RULE_SGD 0
+#define DSP_RULE_SUM 1
+
+/* ------------------------------------------------------------ kernel level */
+typedef struct {
+  int32_t nimg;            /* batch */
+  int32_t H, W, C;         /* input spatial size, channels (padded to a multiple of 8) */
+  int32_t P, Q, K;         /* output spatial size, channels (padded to a multiple of 8) */
+  int32_t R, S, stride, pad;
+} dsp_conv_geom_t;
+
+typedef struct {
+  dsp_conv_geom_t geom;
+  int32_t M, N, Kd;        /* GEMM extents (see igemm.cu header comment) */
+  const void* A;           /* FPROP/WGRAD: X (NHWC); DGRAD: dY (NHWC) */
+  const void* B;           /* FPROP/DGRAD: packed weights [K][R][S][C]; WGRAD: dY */
+  void* D;                 /* FPROP/DGRAD: output [M][ldd]; WGRAD: fp32 partials [splits][M][N] */
+  int32_t ldd;
+  int32_t out_f32;         /* FPROP/DGRAD: store fp32 instead of the storage dtype */
+  const void* residual;    /* optional [M][ldd] added in the epilogue */
+  const float* bias;       /* optional [N] added in the epilogue */
+  float* stats;            /* optional BatchNorm partials [gridDim.x][2][N] (sum, sum of squares) */
+  int32_t kb_per_split;    /* WGRAD split-K: K blocks per split */
+  int32_t n_valid;         /* FPROP/DGRAD: columns >= n_valid are stored as 0 (0 = all N valid) */
+} dsp_igemm_args_t;
+
+/* Implicit-GEMM conv/dense on tcgen05 tensor cores (igemm.cu).  `splits` is the
+ * WGRAD split-K factor (ignored otherwise). */
+int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int splits, void* stream);
+
+/* Per-block parameter update (optim.py:48-109 + pipeline.py:591-596), flat
+ * vectors of length n.  The fp64 variant reproduces the reference's IEEE op
+ * order bit for bit (no FMA contraction); the fp32 variant is the engine's.
+ *   g      = grad + wd*x        (only if wd != 0)
+ *   SGD:   x' = x - lr*g
+ *   SUM:   y = x - lr*g; ys' = x - slr*g; x' = beta==0 ? y : y + beta*(ys' - ys)
+ * slr = s*lr is formed by the caller (optim.py:92 evaluates (state.s*lr)).
+ * grad_sq (optional, device) receives sum(grad^2) (pre-WD, pipeline.py:602).
+ * ys may be NULL for SGD; y (optional) receives y for API fidelity (optim.py:97). */
+int dsp_update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr,
+                   double slr, double beta, double wd, double* grad_sq, void* stream);
+int dsp_update_f32(int rule, int64_t n, float* x, const float* grad, float* ys, double lr, double slr,
+                   double beta, double wd, float* grad_sq, void* stream);
+
+/* ------------------------------------------------------------ block level */
+typedef struct {
+  int32_t kind;            /* DSP_LAYER_* */
+  int32_t in_c, in_h, in_w;   /* real (unpadded) input shape; dense: (in_dim, 1, 1) */
+  int32_t out_c, out_h, out_w;
+  int32_t mid_c;           /* bottleneck width */
+  int32_t stride;
+  int32_t ksize;           /* CONV_BN_RELU kernel size */
+  int32_t bias;            /* DENSE: has bias */
+  int32_t reserved;
+  int64_t param_offset;    /* into the block's flat fp32 parameter vector */
+  int64_t param_count;
+} dsp_layer_desc_t;
+
+typedef struct dsp_block dsp_block_t;
+
+/* Plan a block: a consecutive run of layers (blocks.py:65-93, 229-252).
+ * is_last: the block ends in logits and owns the loss (pipeline.py:575-576). */
+int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, int batch, int dtype, int is_last,
+                     dsp_block_t** out);
+void dsp_block_destroy(dsp_block_t* blk);
+/* Device bytes the caller must provide to dsp_block_bind (activations, tape,
+ * BN statistics, packed weights, split-K scratch). */
+int64_t dsp_block_workspace_bytes(const dsp_block_t* blk);
+/* Element counts (whole batch, padded NHWC) of the block input / output activation. */
+int64_t dsp_block_in_elems(const dsp_block_t* blk);
+int64_t dsp_block_out_elems(const dsp_block_t* blk);
+int64_t dsp_block_param_count(const dsp_block_t* blk);
+/* Bind device memory: workspace, flat fp32 params and grads (param_count each). */
+int dsp_block_bind(dsp_block_t* blk, void* workspace, float* params, float* grads, void* stream);
+/* Re-pack the storage-dtype weight shadow from the fp32 params (after an external write). */
+int dsp_block_pack(dsp_block_t* blk, void* stream);
+
+/* block_forward: x (padded input, storage dtype) -> y (padded output).
+ * record=1 keeps the tape for dsp_block_backward (recompute pass); y may be
+ * NULL when record=1 (the reference discards it, pipeline.py:566). For the
+ * last block the output is fp32 logits [B][classes padded to 8] kept in the
+ * workspace; if y is non-NULL they are also copied there. */
+int dsp_block_forward(dsp_block_t* blk, const void* x, void* y, int record, void* stream);
+/* softmax_xent on the recorded logits (last block only): writes the mean loss
+ * to *loss_dev (device fp32) and keeps dlogits as the backward upstream. */
+int dsp_block_loss(dsp_block_t* blk, const int64_t* labels_dev, float* loss_dev, void* stream);
+/* block_backward on the recorded tape.  upstream: padded dY (NULL for the
+ * last block, which uses dlogits).  grad_in: padded dX or NULL to skip the
+ * input gradient (block 0).  Writes the flat fp32 parameter gradient. */
+int dsp_block_backward(dsp_block_t* blk, const void* upstream, void* grad_in, void* stream);
+/* Update the bound params from the bound grads and re-pack the weight shadow. */
+int dsp_block_update(dsp_block_t* blk, int rule, float* ys, double lr, double slr, double beta, double wd,
+                     int apply, float* grad_sq_out, void* stream);
+
+/* ------------------------------------------------------------ utilities */
+/* Host fp64 batch -> padded device activation (storage dtype).  x_dev points
+ * to a device copy of the fp32 batch [B][C*H*W] in the reference's flattened
+ * (C,H,W) order (CNN) or [B][D] (dense). */
+int dsp_pack_input(const float* x_dev, void* out, int batch, int c, int h, int w, int c_pad, int dtype,
+                   int nchw, void* stream);
+int dsp_unpack_output(const void* in, float* out_dev, int batch, int c, int h, int w, int c_pad, int dtype,
+                      int nchw, void* stream);
+const char* dsp_last_error(void);
+int dsp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSP_B200_H_ */

@@ -1,0 +1,138 @@
+"""ctypes binding of ``libdsp_b200.so`` (the C ABI in include/dsp_b200.h).
+
+This is the only way the package reaches its CUDA kernels. There is no CPU
+fallback: if the library is missing or no CUDA device is present, the
+product path raises ``B200Unavailable`` instead of silently running elsewhere.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libdsp_b200.so"
+
+DSP_DTYPE_BF16 = 0
+DSP_DTYPE_F32 = 1
+
+DSP_IGEMM_FPROP = 0
+DSP_IGEMM_DGRAD = 1
+DSP_IGEMM_WGRAD = 2
+
+DSP_LAYER_DENSE = 0
+DSP_LAYER_RELU = 1
+DSP_LAYER_TANH = 2
+DSP_LAYER_CONV_BN_RELU = 10
+DSP_LAYER_BASIC_UNIT = 11
+DSP_LAYER_BOTTLENECK = 12
+DSP_LAYER_AVGPOOL = 13
+DSP_LAYER_MAXPOOL = 14
+
+DSP_RULE_SGD = 0
+DSP_RULE_SUM = 1
+
+
+class B200Unavailable(RuntimeError):
+    """The CUDA library or a CUDA device is missing; there is no fallback."""
+
+
+class DspError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[dsp error {code}] {message}")
+        self.code = code
+
+
+class ConvGeom(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("nimg", "H", "W", "C", "P", "Q", "K", "R", "S", "stride", "pad")]
+
+
+class IgemmArgs(C.Structure):
+    _fields_ = [
+        ("geom", ConvGeom),
+        ("M", C.c_int32), ("N", C.c_int32), ("Kd", C.c_int32),
+        ("A", C.c_void_p), ("B", C.c_void_p), ("D", C.c_void_p),
+        ("ldd", C.c_int32), ("out_f32", C.c_int32),
+        ("residual", C.c_void_p), ("bias", C.c_void_p), ("stats", C.c_void_p),
+        ("kb_per_split", C.c_int32),
+        ("n_valid", C.c_int32),
+    ]
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("in_c", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32),
+        ("out_c", C.c_int32), ("out_h", C.c_int32), ("out_w", C.c_int32),
+        ("mid_c", C.c_int32), ("stride", C.c_int32), ("ksize", C.c_int32),
+        ("bias", C.c_int32), ("reserved", C.c_int32),
+        ("param_offset", C.c_int64), ("param_count", C.c_int64),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/dsp_b200.h exactly
+_P = C.c_void_p
+_SIGNATURES = {
+    "dsp_igemm": (C.c_int, [C.c_int, C.c_int, C.POINTER(IgemmArgs), C.c_int, _P]),
+    "dsp_update_f64": (C.c_int, [C.c_int, C.c_int64, _P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
+                                 C.c_double, _P, _P]),
+    "dsp_update_f32": (C.c_int, [C.c_int, C.c_int64, _P, _P, _P, C.c_double, C.c_double, C.c_double,
+                                 C.c_double, _P, _P]),
+    "dsp_block_create": (C.c_int, [C.POINTER(LayerDesc), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "dsp_block_destroy": (None, [_P]),
+    "dsp_block_workspace_bytes": (C.c_int64, [_P]),
+    "dsp_block_in_elems": (C.c_int64, [_P]),
+    "dsp_block_out_elems": (C.c_int64, [_P]),
+    "dsp_block_param_count": (C.c_int64, [_P]),
+    "dsp_block_bind": (C.c_int, [_P, _P, _P, _P, _P]),
+    "dsp_block_pack": (C.c_int, [_P, _P]),
+    "dsp_block_forward": (C.c_int, [_P, _P, _P, C.c_int, _P]),
+    "dsp_block_loss": (C.c_int, [_P, _P, _P, _P]),
+    "dsp_block_backward": (C.c_int, [_P, _P, _P, _P]),
+    "dsp_block_update": (C.c_int, [_P, C.c_int, _P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
+                                   _P, _P]),
+    "dsp_pack_input": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    "dsp_unpack_output": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    "dsp_last_error": (C.c_char_p, []),
+    "dsp_abi_version": (C.c_int, []),
+}
+
+_lib = None
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES)
+
+
+def load(require_symbols: bool = True):
+    """Load libdsp_b200.so (no device needed). Raises B200Unavailable if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise B200Unavailable(
+            f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
+            "There is no CPU fallback for the DSP B200 path."
+        )
+    lib = C.CDLL(os.fspath(LIB_PATH))
+    for name, (res, args) in _SIGNATURES.items():
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            if require_symbols:
+                raise B200Unavailable(f"{LIB_PATH} does not export {name}")
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().dsp_last_error()
+        raise DspError(rc, msg.decode() if msg else "unknown")
+
+
+def lib():
+    return load()

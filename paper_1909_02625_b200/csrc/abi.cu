@@ -1,0 +1,95 @@
+// C-ABI glue: error reporting and kernel-level entry points (include/dsp_b200.h).
+#include "common.cuh"
+#include "abi_internal.h"
+#include "kernels.cuh"
+
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+namespace dsp {
+
+static thread_local char g_last_error[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DSP_OK;
+  return set_error(DSP_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+}  // namespace dsp
+
+using namespace dsp;
+
+extern "C" const char* dsp_last_error(void) { return g_last_error; }
+extern "C" int dsp_abi_version(void) { return DSP_ABI_VERSION; }
+
+extern "C" int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int splits, void* stream) {
+  if (args == nullptr) return set_error(DSP_E_INVALID, "dsp_igemm: null args");
+  if (mode < DSP_IGEMM_FPROP || mode > DSP_IGEMM_WGRAD) return set_error(DSP_E_INVALID, "dsp_igemm: bad mode %d", mode);
+  if (dtype != DSP_DTYPE_BF16 && dtype != DSP_DTYPE_F32) return set_error(DSP_E_INVALID, "dsp_igemm: bad dtype %d", dtype);
+  const int epc = dtype == DSP_DTYPE_BF16 ? 8 : 4;
+  const dsp_conv_geom_t& g = args->geom;
+  if (g.C % epc || g.K % epc) return set_error(DSP_E_INVALID, "dsp_igemm: channels C=%d K=%d not multiples of %d", g.C, g.K, epc);
+  if (args->M <= 0 || args->N <= 0 || args->Kd <= 0) return set_error(DSP_E_INVALID, "dsp_igemm: empty GEMM");
+  if (dtype == DSP_DTYPE_F32 && mode != DSP_IGEMM_FPROP)
+    return set_error(DSP_E_INVALID, "dsp_igemm: fp32/tf32 storage supports FPROP only (MN-major tf32 operands unsupported)");
+  if (mode == DSP_IGEMM_WGRAD && (splits <= 0 || args->kb_per_split <= 0))
+    return set_error(DSP_E_INVALID, "dsp_igemm: WGRAD needs splits and kb_per_split");
+  return cuda_check(igemm_launch(mode, dtype, *args, splits, (cudaStream_t)stream), "dsp_igemm launch");
+}
+
+extern "C" int dsp_update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr,
+                              double slr, double beta, double wd, double* grad_sq, void* stream) {
+  if (rule != DSP_RULE_SGD && rule != DSP_RULE_SUM) return set_error(DSP_E_INVALID, "dsp_update_f64: bad rule %d", rule);
+  if (n < 0 || (n > 0 && (!x || !grad))) return set_error(DSP_E_INVALID, "dsp_update_f64: bad vectors");
+  if (rule == DSP_RULE_SUM && n > 0 && !ys) return set_error(DSP_E_INVALID, "dsp_update_f64: SUM needs ys");
+  if (n == 0) return DSP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = nullptr;
+  if (grad_sq) DSP_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * update_grid(n), st));
+  DSP_CUDA(update_f64(rule, n, x, grad, ys, y, lr, slr, beta, wd, part, st));
+  if (grad_sq) {
+    DSP_CUDA(sum_partials_f64(part, update_grid(n), grad_sq, st));
+    DSP_CUDA(cudaFreeAsync(part, st));
+  }
+  return DSP_OK;
+}
+
+extern "C" int dsp_update_f32(int rule, int64_t n, float* x, const float* grad, float* ys, double lr, double slr,
+                              double beta, double wd, float* grad_sq, void* stream) {
+  if (rule != DSP_RULE_SGD && rule != DSP_RULE_SUM) return set_error(DSP_E_INVALID, "dsp_update_f32: bad rule %d", rule);
+  if (n < 0 || (n > 0 && (!x || !grad))) return set_error(DSP_E_INVALID, "dsp_update_f32: bad vectors");
+  if (rule == DSP_RULE_SUM && n > 0 && !ys) return set_error(DSP_E_INVALID, "dsp_update_f32: SUM needs ys");
+  if (n == 0) return DSP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  float* part = nullptr;
+  if (grad_sq) DSP_CUDA(cudaMallocAsync((void**)&part, sizeof(float) * update_grid(n), st));
+  DSP_CUDA(update_f32(rule, n, x, grad, ys, (float)lr, (float)slr, (float)beta, (float)wd, part, st));
+  if (grad_sq) {
+    DSP_CUDA(sum_partials_f32(part, update_grid(n), grad_sq, st));
+    DSP_CUDA(cudaFreeAsync(part, st));
+  }
+  return DSP_OK;
+}
+
+extern "C" int dsp_pack_input(const float* x_dev, void* out, int batch, int c, int h, int w, int c_pad, int dtype,
+                              int nchw, void* stream) {
+  if (!x_dev || !out || batch <= 0 || c <= 0 || h <= 0 || w <= 0 || c_pad < c || c_pad % 8)
+    return set_error(DSP_E_INVALID, "dsp_pack_input: bad shape");
+  return cuda_check(pack_input(x_dev, out, batch, c, h, w, c_pad, dtype, nchw, (cudaStream_t)stream), "pack_input");
+}
+
+extern "C" int dsp_unpack_output(const void* in, float* out_dev, int batch, int c, int h, int w, int c_pad, int dtype,
+                                 int nchw, void* stream) {
+  if (!in || !out_dev || batch <= 0 || c <= 0 || h <= 0 || w <= 0 || c_pad < c || c_pad % 8)
+    return set_error(DSP_E_INVALID, "dsp_unpack_output: bad shape");
+  return cuda_check(unpack_output(in, out_dev, batch, c, h, w, c_pad, dtype, nchw, (cudaStream_t)stream),
+                    "unpack_output");
+}

@@ -1,0 +1,652 @@
+// Block executor: plans one DSP block (a consecutive run of layers,
+// blocks.py:65-93) over a single caller-provided device workspace and
+// sequences the sm_100a kernels for block_forward (blocks.py:96-118),
+// softmax_xent (tensor.py:86-111), block_backward (blocks.py:121-154) and the
+// optimizer step (pipeline.py:591-596, optim.py:48-109).
+//
+// Memory plan (all offsets into one workspace, 256-byte aligned):
+//   per layer   : output activation (storage dtype, NHWC, channels padded to 8)
+//   per conv    : pre-BN conv output y, BN stats [4][Cp], BN-backward coef [3][Cp]
+//   per unit    : intermediate ReLU outputs z1 (and z2 for bottlenecks)
+//   shared      : 4 unit-backward scratch tensors, 2 layer-gradient ping-pong
+//                 tensors, BN / split-K / update partial-sum scratch, packed
+//                 storage-dtype weight shadow + its pack table.
+// The fresh forward and the recompute write the same buffers (the fresh pass's
+// block output goes straight to the caller's out-ring slot), so one block holds
+// exactly one tape, like the reference's single-use ForwardTape (blocks.py:54-62).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "abi_internal.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace dsp {
+
+namespace {
+
+inline int pad8(int c) { return (c + 7) / 8 * 8; }
+inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct ConvP {
+  dsp_conv_geom_t g;
+  int ci_real = 0, co_real = 0;
+  int64_t w_off = 0, gamma_off = 0, beta_off = 0;  // floats, into block params
+  int64_t wpack = 0;                               // elements, into packed weights
+  size_t y = 0, stat = 0, coef = 0;                // workspace byte offsets
+  int64_t M() const { return (int64_t)g.nimg * g.P * g.Q; }
+  int64_t Min() const { return (int64_t)g.nimg * g.H * g.W; }
+};
+
+struct LayerP {
+  dsp_layer_desc_t d{};
+  int in_cp = 0, out_cp = 0;
+  int in_h = 1, in_w = 1, out_h = 1, out_w = 1;
+  int in_real = 0, out_real = 0;  // real channels / dense widths
+  int64_t in_rows = 0, out_rows = 0;  // B*H*W
+  std::vector<ConvP> convs;
+  bool proj = false;
+  size_t out = 0, z1 = 0, z2 = 0, arg = 0;
+  // dense
+  ConvP dense;  // 1x1 conv view of the dense layer
+  int64_t b_off = -1;
+  bool logits = false;
+  int64_t in_elems() const { return in_rows * in_cp; }
+  int64_t out_elems() const { return out_rows * out_cp; }
+};
+
+}  // namespace
+}  // namespace dsp
+
+struct dsp_block {
+  int B = 0, dtype = 0, is_last = 0, esz = 2;
+  std::vector<dsp::LayerP> L;
+  size_t ws_bytes = 0;
+  size_t S[4] = {0, 0, 0, 0};
+  size_t G[2] = {0, 0};
+  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0;
+  size_t packed = 0, ptable = 0;
+  std::vector<dsp::PackEntry> packs;
+  int pack_max = 0;
+  size_t dlogits = 0;
+  int classes = 0, classes_pad = 0;
+  int64_t param_count = 0;
+  uint8_t* ws = nullptr;
+  float* params = nullptr;
+  float* grads = nullptr;
+  bool tape_valid = false;
+  const void* rec_x = nullptr;
+};
+
+namespace dsp {
+namespace {
+
+struct Planner {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off = align256(off + std::max<size_t>(bytes, 1));
+    return o;
+  }
+};
+
+void make_conv(ConvP& c, int B, int H, int W, int ci, int co, int k, int stride, int pad) {
+  c.g.nimg = B;
+  c.g.H = H;
+  c.g.W = W;
+  c.g.C = pad8(ci);
+  c.g.R = c.g.S = k;
+  c.g.stride = stride;
+  c.g.pad = pad;
+  c.g.P = (H + 2 * pad - k) / stride + 1;
+  c.g.Q = (W + 2 * pad - k) / stride + 1;
+  c.g.K = pad8(co);
+  c.ci_real = ci;
+  c.co_real = co;
+}
+
+int wgrad_splits(const ConvP& c, int* kb_per_split, int dtype) {
+  const int ks = dtype == DSP_DTYPE_BF16 ? 64 : 32;
+  const int64_t kd = c.M();
+  const int nkb = (int)((kd + ks - 1) / ks);
+  const int mw = c.g.R * c.g.S * c.g.C;
+  const int mt = (mw + 127) / 128;
+  const int nt = (c.g.K + 255) / 256;
+  int splits = std::max(1, 296 / std::max(1, mt * nt));
+  splits = std::min(splits, nkb);
+  int kb = (nkb + splits - 1) / splits;
+  splits = (nkb + kb - 1) / kb;
+  *kb_per_split = kb;
+  return splits;
+}
+
+template <typename P>
+inline P* at(dsp_block* b, size_t off) {
+  return reinterpret_cast<P*>(b->ws + off);
+}
+
+// ------------------------------------------------------------------ kernels per conv
+int conv_fprop(dsp_block* b, const ConvP& c, const void* x, cudaStream_t st) {
+  dsp_igemm_args_t a{};
+  a.geom = c.g;
+  a.M = (int)c.M();
+  a.N = c.g.K;
+  a.Kd = c.g.R * c.g.S * c.g.C;
+  a.A = x;
+  a.B = b->ws + b->packed + (size_t)c.wpack * b->esz;
+  a.D = b->ws + c.y;
+  a.ldd = c.g.K;
+  a.stats = at<float>(b, b->fpart);
+  a.n_valid = c.co_real;
+  DSP_CUDA(igemm_launch(DSP_IGEMM_FPROP, b->dtype, a, 1, st));
+  const int tiles = (a.M + 127) / 128;
+  DSP_CUDA(bn_finalize(at<float>(b, b->fpart), tiles, c.g.K, c.co_real, c.M(), b->params + c.gamma_off,
+                       b->params + c.beta_off, at<float>(b, c.stat), st));
+  return DSP_OK;
+}
+
+int conv_wgrad(dsp_block* b, const ConvP& c, const void* x, const void* dy, cudaStream_t st) {
+  dsp_igemm_args_t a{};
+  a.geom = c.g;
+  a.M = c.g.R * c.g.S * c.g.C;
+  a.N = c.g.K;
+  a.Kd = (int)c.M();
+  a.A = x;
+  a.B = dy;
+  a.D = b->ws + b->wpart;
+  int kb = 1;
+  const int splits = wgrad_splits(c, &kb, b->dtype);
+  a.kb_per_split = kb;
+  DSP_CUDA(igemm_launch(DSP_IGEMM_WGRAD, b->dtype, a, splits, st));
+  DSP_CUDA(wgrad_reduce(at<float>(b, b->wpart), splits, a.M, a.N, c.g.R * c.g.S, c.g.C, c.ci_real, c.co_real, 0,
+                        b->grads + c.w_off, st));
+  return DSP_OK;
+}
+
+int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const void* residual, cudaStream_t st) {
+  dsp_igemm_args_t a{};
+  a.geom = c.g;
+  a.M = (int)c.Min();
+  a.N = c.g.C;
+  a.Kd = c.g.R * c.g.S * c.g.K;
+  a.A = dy;
+  a.B = b->ws + b->packed + (size_t)c.wpack * b->esz;
+  a.D = dx;
+  a.ldd = c.g.C;
+  a.residual = residual;
+  a.n_valid = c.ci_real;
+  DSP_CUDA(igemm_launch(DSP_IGEMM_DGRAD, b->dtype, a, 1, st));
+  return DSP_OK;
+}
+
+// BN backward for one conv: dy = BNback(g = gsrc*(mask>0)), grads into params layout.
+int bn_backward_pair(dsp_block* b, const void* gsrc, const void* mask, const ConvP& c1, void* dy1, const ConvP* c2,
+                     void* dy2, void* g_out, cudaStream_t st) {
+  const int64_t M = c1.M();
+  const int Cp = c1.g.K;
+  const int chunks = bn_bwd_chunks(M, Cp);
+  DSP_CUDA(bn_bwd_reduce(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, b->bpart), M, Cp, st));
+  DSP_CUDA(bn_bwd_finalize(at<float>(b, b->bpart), chunks, Cp, c1.co_real, M, b->params + c1.gamma_off,
+                           at<float>(b, c1.stat), b->grads + c1.gamma_off, b->grads + c1.beta_off,
+                           at<float>(b, c1.coef), st));
+  if (c2) {
+    DSP_CUDA(bn_bwd_reduce(b->dtype, gsrc, mask, b->ws + c2->y, at<float>(b, c2->stat), at<float>(b, b->bpart2), M, Cp,
+                           st));
+    DSP_CUDA(bn_bwd_finalize(at<float>(b, b->bpart2), chunks, Cp, c2->co_real, M, b->params + c2->gamma_off,
+                             at<float>(b, c2->stat), b->grads + c2->gamma_off, b->grads + c2->beta_off,
+                             at<float>(b, c2->coef), st));
+  }
+  DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, c1.coef), dy1,
+                        c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
+                        c2 ? at<float>(b, c2->coef) : nullptr, c2 ? dy2 : nullptr, g_out, M, Cp, st));
+  return DSP_OK;
+}
+
+// ------------------------------------------------------------------ layer forward / backward
+int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_t st) {
+  const int dt = b->dtype;
+  switch (l.d.kind) {
+    case DSP_LAYER_DENSE: {
+      dsp_igemm_args_t a{};
+      a.geom = l.dense.g;
+      a.M = b->B;
+      a.N = l.out_cp;
+      a.Kd = l.in_cp;
+      a.A = x;
+      a.B = b->ws + b->packed + (size_t)l.dense.wpack * b->esz;
+      a.D = out;
+      a.ldd = l.out_cp;
+      a.out_f32 = l.logits ? 1 : 0;
+      a.bias = l.b_off >= 0 ? b->params + l.b_off : nullptr;
+      a.n_valid = l.out_real;
+      DSP_CUDA(igemm_launch(DSP_IGEMM_FPROP, dt, a, 1, st));
+      return DSP_OK;
+    }
+    case DSP_LAYER_RELU:
+    case DSP_LAYER_TANH:
+      DSP_CUDA(act_forward(dt, l.d.kind == DSP_LAYER_TANH, x, out, l.in_elems(), st));
+      return DSP_OK;
+    case DSP_LAYER_AVGPOOL:
+      DSP_CUDA(avgpool_forward(dt, x, out, b->B, l.in_h * l.in_w, l.in_cp, st));
+      return DSP_OK;
+    case DSP_LAYER_MAXPOOL:
+      DSP_CUDA(maxpool_forward(dt, x, out, at<int32_t>(b, l.arg), b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
+      return DSP_OK;
+    case DSP_LAYER_CONV_BN_RELU: {
+      const ConvP& c = l.convs[0];
+      DSP_TRY(conv_fprop(b, c, x, st));
+      DSP_CUDA(bn_apply(dt, b->ws + c.y, at<float>(b, c.stat), nullptr, nullptr, nullptr, out, c.M(), c.g.K, 1, st));
+      return DSP_OK;
+    }
+    case DSP_LAYER_BASIC_UNIT:
+    case DSP_LAYER_BOTTLENECK: {
+      const bool bott = l.d.kind == DSP_LAYER_BOTTLENECK;
+      const int nmain = bott ? 3 : 2;
+      const void* cur = x;
+      for (int i = 0; i < nmain - 1; ++i) {
+        const ConvP& c = l.convs[i];
+        DSP_TRY(conv_fprop(b, c, cur, st));
+        void* z = b->ws + (i == 0 ? l.z1 : l.z2);
+        DSP_CUDA(bn_apply(dt, b->ws + c.y, at<float>(b, c.stat), nullptr, nullptr, nullptr, z, c.M(), c.g.K, 1, st));
+        cur = z;
+      }
+      const ConvP& cl = l.convs[nmain - 1];
+      DSP_TRY(conv_fprop(b, cl, cur, st));
+      if (l.proj) {
+        const ConvP& cs = l.convs[nmain];
+        DSP_TRY(conv_fprop(b, cs, x, st));
+        DSP_CUDA(bn_apply(dt, b->ws + cl.y, at<float>(b, cl.stat), nullptr, b->ws + cs.y, at<float>(b, cs.stat), out,
+                          cl.M(), cl.g.K, 1, st));
+      } else {
+        DSP_CUDA(bn_apply(dt, b->ws + cl.y, at<float>(b, cl.stat), x, nullptr, nullptr, out, cl.M(), cl.g.K, 1, st));
+      }
+      return DSP_OK;
+    }
+  }
+  return set_error(DSP_E_INVALID, "unknown layer kind %d", l.d.kind);
+}
+
+// u: gradient w.r.t. the layer output; x: the layer input; dx may be null.
+int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* dx, cudaStream_t st) {
+  const int dt = b->dtype;
+  switch (l.d.kind) {
+    case DSP_LAYER_DENSE: {
+      if (l.b_off >= 0) {
+        const int chunks = bn_bwd_chunks(b->B, l.out_cp);
+        DSP_CUDA(bn_bwd_reduce(dt, u, nullptr, nullptr, nullptr, at<float>(b, b->bpart), b->B, l.out_cp, st));
+        DSP_CUDA(bn_bwd_finalize(at<float>(b, b->bpart), chunks, l.out_cp, l.out_real, b->B, nullptr, nullptr, nullptr,
+                                 b->grads + l.b_off, nullptr, st));
+      }
+      const ConvP& c = l.dense;
+      dsp_igemm_args_t a{};
+      a.geom = c.g;
+      a.M = l.in_cp;
+      a.N = l.out_cp;
+      a.Kd = b->B;
+      a.A = x;
+      a.B = u;
+      a.D = b->ws + b->wpart;
+      int kb = 1;
+      const int splits = wgrad_splits(c, &kb, dt);
+      a.kb_per_split = kb;
+      DSP_CUDA(igemm_launch(DSP_IGEMM_WGRAD, dt, a, splits, st));
+      DSP_CUDA(wgrad_reduce(at<float>(b, b->wpart), splits, a.M, a.N, 1, l.in_cp, l.in_real, l.out_real, 1,
+                            b->grads + c.w_off, st));
+      if (dx) DSP_TRY(conv_dgrad(b, c, u, dx, nullptr, st));
+      return DSP_OK;
+    }
+    case DSP_LAYER_RELU:
+    case DSP_LAYER_TANH:
+      if (dx) DSP_CUDA(act_backward(dt, l.d.kind == DSP_LAYER_TANH, x, u, dx, l.in_elems(), st));
+      return DSP_OK;
+    case DSP_LAYER_AVGPOOL:
+      if (dx) DSP_CUDA(avgpool_backward(dt, u, dx, b->B, l.in_h * l.in_w, l.in_cp, st));
+      return DSP_OK;
+    case DSP_LAYER_MAXPOOL:
+      if (dx)
+        DSP_CUDA(maxpool_backward(dt, u, at<int32_t>(b, l.arg), dx, b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp,
+                                  st));
+      return DSP_OK;
+    case DSP_LAYER_CONV_BN_RELU: {
+      const ConvP& c = l.convs[0];
+      void* dy = b->ws + b->S[0];
+      DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
+      DSP_TRY(conv_wgrad(b, c, x, dy, st));
+      if (dx) DSP_TRY(conv_dgrad(b, c, dy, dx, nullptr, st));
+      return DSP_OK;
+    }
+    case DSP_LAYER_BASIC_UNIT:
+    case DSP_LAYER_BOTTLENECK: {
+      const bool bott = l.d.kind == DSP_LAYER_BOTTLENECK;
+      const int nmain = bott ? 3 : 2;
+      void* S0 = b->ws + b->S[0];
+      void* S1 = b->ws + b->S[1];
+      void* S2 = b->ws + b->S[2];
+      void* S3 = b->ws + b->S[3];
+      const ConvP& cl = l.convs[nmain - 1];
+      const ConvP* cs = l.proj ? &l.convs[nmain] : nullptr;
+      // top BN(s): g = u * (out > 0); dy_last -> S0, dy_sc -> S1 (proj) or g -> S1 (identity)
+      DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st));
+      // walk the main path down
+      for (int i = nmain - 1; i >= 0; --i) {
+        const ConvP& c = l.convs[i];
+        const void* cin = i == 0 ? x : b->ws + (i == 1 ? l.z1 : l.z2);
+        DSP_TRY(conv_wgrad(b, c, cin, S0, st));
+        if (i == 0) break;
+        DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st));  // dz_{i}
+        const ConvP& cb = l.convs[i - 1];
+        const void* zmask = b->ws + (i == 1 ? l.z1 : l.z2);
+        DSP_TRY(bn_backward_pair(b, S2, zmask, cb, S0, nullptr, nullptr, nullptr, st));
+      }
+      const void* res = S1;
+      if (cs) {
+        DSP_TRY(conv_wgrad(b, *cs, x, S1, st));
+        if (dx) DSP_TRY(conv_dgrad(b, *cs, S1, S3, nullptr, st));
+        res = S3;
+      }
+      if (dx) DSP_TRY(conv_dgrad(b, l.convs[0], S0, dx, res, st));
+      return DSP_OK;
+    }
+  }
+  return set_error(DSP_E_INVALID, "unknown layer kind %d", l.d.kind);
+}
+
+}  // namespace
+}  // namespace dsp
+
+using namespace dsp;
+
+// ==================================================================== C ABI
+extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, int batch, int dtype, int is_last,
+                                dsp_block_t** out) {
+  if (!layers || n_layers <= 0 || batch <= 0 || !out) return set_error(DSP_E_INVALID, "dsp_block_create: bad args");
+  if (dtype != DSP_DTYPE_BF16) return set_error(DSP_E_INVALID, "dsp_block_create: only bf16 storage is supported");
+  dsp_block* b = new dsp_block();
+  b->B = batch;
+  b->dtype = dtype;
+  b->is_last = is_last;
+  b->esz = 2;
+  Planner pl;
+  const int B = batch;
+  // running shape (real channels, h, w)
+  int cur_c = 0, cur_h = 1, cur_w = 1;
+  {
+    const dsp_layer_desc_t& d0 = layers[0];
+    cur_c = d0.in_c;
+    cur_h = d0.kind == DSP_LAYER_DENSE ? 1 : std::max(1, d0.in_h);
+    cur_w = d0.kind == DSP_LAYER_DENSE ? 1 : std::max(1, d0.in_w);
+    if (d0.kind == DSP_LAYER_RELU || d0.kind == DSP_LAYER_TANH) {
+      delete b;
+      return set_error(DSP_E_INVALID, "a block cannot start with an activation (its width is unknown)");
+    }
+  }
+  int64_t max_act = 0, max_fpart = 0, max_bpart = 0, max_wpart = 0;
+  int64_t pack_elems = 0;
+  std::vector<ConvP*> all_convs;
+  b->L.resize(n_layers);
+  for (int i = 0; i < n_layers; ++i) {
+    LayerP& l = b->L[i];
+    l.d = layers[i];
+    const dsp_layer_desc_t& d = l.d;
+    const int kind = d.kind;
+    b->param_count = std::max<int64_t>(b->param_count, d.param_offset + d.param_count);
+    if (kind == DSP_LAYER_DENSE) {
+      if (cur_h * cur_w != 1 || d.in_c != cur_c) {
+        const int flat = cur_c * cur_h * cur_w;
+        delete b;
+        return set_error(DSP_E_INVALID, "layer %d: dense(%d,%d) does not accept width %d", i, d.in_c, d.out_c, flat);
+      }
+      l.in_real = d.in_c;
+      l.out_real = d.out_c;
+      l.in_cp = pad8(d.in_c);
+      l.out_cp = pad8(d.out_c);
+      l.in_rows = l.out_rows = B;
+      make_conv(l.dense, B, 1, 1, d.in_c, d.out_c, 1, 1, 0);
+      l.dense.w_off = d.param_offset;
+      l.b_off = d.bias ? d.param_offset + (int64_t)d.in_c * d.out_c : -1;
+      l.dense.wpack = pack_elems;
+      pack_elems += (int64_t)l.dense.g.K * l.dense.g.C;
+      b->packs.push_back({l.dense.w_off, l.dense.wpack, d.out_c, d.in_c, 1, l.dense.g.K, l.dense.g.C, 1});
+      l.logits = is_last && i == n_layers - 1;
+      cur_c = d.out_c;
+      int kb = 1;
+      const int sp = wgrad_splits(l.dense, &kb, dtype);
+      max_wpart = std::max<int64_t>(max_wpart, (int64_t)sp * l.in_cp * l.out_cp);
+      max_bpart = std::max<int64_t>(max_bpart, (int64_t)bn_bwd_chunks(B, l.out_cp) * 2 * l.out_cp);
+    } else if (kind == DSP_LAYER_RELU || kind == DSP_LAYER_TANH) {
+      l.in_real = l.out_real = cur_c;
+      l.in_cp = l.out_cp = pad8(cur_c);
+      l.in_h = l.out_h = cur_h;
+      l.in_w = l.out_w = cur_w;
+      l.in_rows = l.out_rows = (int64_t)B * cur_h * cur_w;
+    } else {
+      if (d.in_c != cur_c || d.in_h != cur_h || d.in_w != cur_w) {
+        delete b;
+        return set_error(DSP_E_INVALID, "layer %d: expects input (%d,%d,%d), got (%d,%d,%d)", i, d.in_c, d.in_h,
+                         d.in_w, cur_c, cur_h, cur_w);
+      }
+      l.in_real = d.in_c;
+      l.in_cp = pad8(d.in_c);
+      l.in_h = d.in_h;
+      l.in_w = d.in_w;
+      l.in_rows = (int64_t)B * d.in_h * d.in_w;
+      int64_t off = d.param_offset;
+      auto add_conv = [&](int H, int W, int ci, int co, int k, int stride, int pad) {
+        ConvP c;
+        make_conv(c, B, H, W, ci, co, k, stride, pad);
+        c.w_off = off;
+        off += (int64_t)co * k * k * ci;
+        c.gamma_off = off;
+        off += co;
+        c.beta_off = off;
+        off += co;
+        c.wpack = pack_elems;
+        pack_elems += (int64_t)c.g.K * k * k * c.g.C;
+        l.convs.push_back(c);
+        return l.convs.back().g;
+      };
+      if (kind == DSP_LAYER_CONV_BN_RELU) {
+        const int k = d.ksize > 0 ? d.ksize : 3;
+        auto g = add_conv(d.in_h, d.in_w, d.in_c, d.out_c, k, d.stride, k / 2);
+        l.out_h = g.P;
+        l.out_w = g.Q;
+        l.out_real = d.out_c;
+      } else if (kind == DSP_LAYER_BASIC_UNIT) {
+        auto g1 = add_conv(d.in_h, d.in_w, d.in_c, d.out_c, 3, d.stride, 1);
+        add_conv(g1.P, g1.Q, d.out_c, d.out_c, 3, 1, 1);
+        l.proj = d.stride != 1 || d.in_c != d.out_c;
+        if (l.proj) add_conv(d.in_h, d.in_w, d.in_c, d.out_c, 1, d.stride, 0);
+        l.out_h = g1.P;
+        l.out_w = g1.Q;
+        l.out_real = d.out_c;
+      } else if (kind == DSP_LAYER_BOTTLENECK) {
+        add_conv(d.in_h, d.in_w, d.in_c, d.mid_c, 1, 1, 0);
+        auto g2 = add_conv(d.in_h, d.in_w, d.mid_c, d.mid_c, 3, d.stride, 1);
+        add_conv(g2.P, g2.Q, d.mid_c, d.out_c, 1, 1, 0);
+        l.proj = d.stride != 1 || d.in_c != d.out_c;
+        if (l.proj) add_conv(d.in_h, d.in_w, d.in_c, d.out_c, 1, d.stride, 0);
+        l.out_h = g2.P;
+        l.out_w = g2.Q;
+        l.out_real = d.out_c;
+      } else if (kind == DSP_LAYER_AVGPOOL) {
+        l.out_h = l.out_w = 1;
+        l.out_real = d.in_c;
+      } else if (kind == DSP_LAYER_MAXPOOL) {
+        l.out_h = (d.in_h + 2 - 3) / 2 + 1;
+        l.out_w = (d.in_w + 2 - 3) / 2 + 1;
+        l.out_real = d.in_c;
+      } else {
+        delete b;
+        return set_error(DSP_E_INVALID, "layer %d: unknown kind %d", i, kind);
+      }
+      if (off != d.param_offset + d.param_count) {
+        delete b;
+        return set_error(DSP_E_INVALID, "layer %d: param_count %lld does not match the layout (%lld)", i,
+                         (long long)d.param_count, (long long)(off - d.param_offset));
+      }
+      l.out_cp = pad8(l.out_real);
+      l.out_rows = (int64_t)B * l.out_h * l.out_w;
+      cur_c = l.out_real;
+      cur_h = l.out_h;
+      cur_w = l.out_w;
+    }
+    max_act = std::max(max_act, std::max(l.in_elems(), l.out_elems()));
+  }
+  // second pass: per-layer buffers (after all convs exist so vectors are stable)
+  for (int i = 0; i < n_layers; ++i) {
+    LayerP& l = b->L[i];
+    l.out = pl.take((size_t)l.out_elems() * (l.logits ? 4 : b->esz));
+    if (l.d.kind == DSP_LAYER_MAXPOOL) l.arg = pl.take((size_t)l.out_elems() * 4);
+    for (size_t ci = 0; ci < l.convs.size(); ++ci) {
+      ConvP& c = l.convs[ci];
+      c.y = pl.take((size_t)c.M() * c.g.K * b->esz);
+      c.stat = pl.take((size_t)4 * c.g.K * 4);
+      c.coef = pl.take((size_t)3 * c.g.K * 4);
+      max_act = std::max(max_act, std::max(c.M() * c.g.K, c.Min() * c.g.C));
+      max_fpart = std::max<int64_t>(max_fpart, (c.M() + 127) / 128 * 2 * c.g.K);
+      max_bpart = std::max<int64_t>(max_bpart, (int64_t)bn_bwd_chunks(c.M(), c.g.K) * 2 * c.g.K);
+      int kb = 1;
+      const int sp = wgrad_splits(c, &kb, dtype);
+      max_wpart = std::max<int64_t>(max_wpart, (int64_t)sp * c.g.R * c.g.S * c.g.C * c.g.K);
+      b->packs.push_back({c.w_off, c.wpack, c.co_real, c.ci_real, c.g.R * c.g.S, c.g.K, c.g.C, 0});
+    }
+    if (l.d.kind == DSP_LAYER_BASIC_UNIT || l.d.kind == DSP_LAYER_BOTTLENECK) {
+      l.z1 = pl.take((size_t)l.convs[0].M() * l.convs[0].g.K * b->esz);
+      if (l.d.kind == DSP_LAYER_BOTTLENECK) l.z2 = pl.take((size_t)l.convs[1].M() * l.convs[1].g.K * b->esz);
+    }
+  }
+  const LayerP& last = b->L.back();
+  if (is_last) {
+    if (!last.logits) {
+      delete b;
+      return set_error(DSP_E_INVALID, "the last block must end with a dense layer (logits)");
+    }
+    b->classes = last.out_real;
+    b->classes_pad = last.out_cp;
+    b->dlogits = pl.take((size_t)B * last.out_cp * b->esz);
+  }
+  for (int s = 0; s < 4; ++s) b->S[s] = pl.take((size_t)max_act * b->esz);
+  for (int s = 0; s < 2; ++s) b->G[s] = pl.take((size_t)max_act * b->esz);
+  b->fpart = pl.take((size_t)std::max<int64_t>(max_fpart, 1) * 4);
+  b->bpart = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
+  b->bpart2 = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
+  b->wpart = pl.take((size_t)std::max<int64_t>(max_wpart, 1) * 4);
+  b->upart = pl.take((size_t)update_grid(std::max<int64_t>(b->param_count, 1)) * 8);
+  b->packed = pl.take((size_t)std::max<int64_t>(pack_elems, 1) * b->esz);
+  b->ptable = pl.take(sizeof(PackEntry) * std::max<size_t>(b->packs.size(), 1));
+  for (auto& p : b->packs) b->pack_max = std::max(b->pack_max, p.cop * p.rs * p.cip);
+  b->ws_bytes = pl.off;
+  *out = b;
+  return DSP_OK;
+}
+
+extern "C" void dsp_block_destroy(dsp_block_t* blk) { delete blk; }
+extern "C" int64_t dsp_block_workspace_bytes(const dsp_block_t* b) { return b ? (int64_t)b->ws_bytes : -1; }
+extern "C" int64_t dsp_block_in_elems(const dsp_block_t* b) { return b ? b->L.front().in_elems() : -1; }
+extern "C" int64_t dsp_block_out_elems(const dsp_block_t* b) { return b ? b->L.back().out_elems() : -1; }
+extern "C" int64_t dsp_block_param_count(const dsp_block_t* b) { return b ? b->param_count : -1; }
+
+extern "C" int dsp_block_pack(dsp_block_t* b, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_pack: block not bound");
+  DSP_CUDA(pack_weights(b->dtype, b->params, b->ws + b->packed, at<PackEntry>(b, b->ptable), (int)b->packs.size(),
+                        b->pack_max, (cudaStream_t)stream));
+  return DSP_OK;
+}
+
+extern "C" int dsp_block_bind(dsp_block_t* b, void* workspace, float* params, float* grads, void* stream) {
+  if (!b || !workspace || (b->param_count > 0 && (!params || !grads)))
+    return set_error(DSP_E_INVALID, "dsp_block_bind: null pointer");
+  b->ws = static_cast<uint8_t*>(workspace);
+  b->params = params;
+  b->grads = grads;
+  b->tape_valid = false;
+  cudaStream_t st = (cudaStream_t)stream;
+  // pad channels of every activation must read as zero; zero the whole workspace once
+  DSP_CUDA(cudaMemsetAsync(b->ws, 0, b->ws_bytes, st));
+  if (!b->packs.empty())
+    DSP_CUDA(cudaMemcpyAsync(b->ws + b->ptable, b->packs.data(), sizeof(PackEntry) * b->packs.size(),
+                             cudaMemcpyHostToDevice, st));
+  DSP_CUDA(cudaStreamSynchronize(st));  // the pack table source is a host vector
+  return dsp_block_pack(b, stream);
+}
+
+extern "C" int dsp_block_forward(dsp_block_t* b, const void* x, void* y, int record, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_forward: block not bound");
+  if (!x) return set_error(DSP_E_INVALID, "dsp_block_forward: null input");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = (int)b->L.size();
+  const void* cur = x;
+  b->tape_valid = false;
+  for (int i = 0; i < n; ++i) {
+    LayerP& l = b->L[i];
+    void* out = b->ws + l.out;
+    if (i == n - 1 && !record && !b->is_last) {
+      if (!y) return set_error(DSP_E_INVALID, "dsp_block_forward: fresh forward needs an output buffer");
+      out = y;
+    }
+    DSP_TRY(layer_forward(b, l, cur, out, st));
+    cur = out;
+  }
+  if (b->is_last && y) {
+    const LayerP& l = b->L.back();
+    DSP_CUDA(cudaMemcpyAsync(y, b->ws + l.out, (size_t)b->B * l.out_cp * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  if (record) {
+    b->tape_valid = true;
+    b->rec_x = x;
+  }
+  return DSP_OK;
+}
+
+extern "C" int dsp_block_loss(dsp_block_t* b, const int64_t* labels, float* loss, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_loss: block not bound");
+  if (!b->is_last) return set_error(DSP_E_STATE, "dsp_block_loss: only the last block owns the loss");
+  if (!b->tape_valid) return set_error(DSP_E_STATE, "dsp_block_loss: no recorded forward");
+  if (!labels || !loss) return set_error(DSP_E_INVALID, "dsp_block_loss: null pointer");
+  const LayerP& l = b->L.back();
+  DSP_CUDA(softmax_xent(b->dtype, at<float>(b, l.out), l.out_cp, b->B, b->classes, labels, b->ws + b->dlogits, loss,
+                        (cudaStream_t)stream));
+  return DSP_OK;
+}
+
+extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* grad_in, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_backward: block not bound");
+  if (!b->tape_valid) return set_error(DSP_E_STATE, "forward tape already consumed or never recorded");
+  b->tape_valid = false;
+  cudaStream_t st = (cudaStream_t)stream;
+  const void* u = b->is_last ? (const void*)(b->ws + b->dlogits) : upstream;
+  if (!u) return set_error(DSP_E_INVALID, "dsp_block_backward: null upstream");
+  const int n = (int)b->L.size();
+  DSP_CUDA(cudaMemsetAsync(b->grads, 0, sizeof(float) * b->param_count, st));
+  for (int i = n - 1; i >= 0; --i) {
+    LayerP& l = b->L[i];
+    const void* x = i == 0 ? b->rec_x : (const void*)(b->ws + b->L[i - 1].out);
+    void* dx = i == 0 ? grad_in : (void*)(b->ws + b->G[i & 1]);
+    DSP_TRY(layer_backward(b, l, x, u, dx, st));
+    u = dx;
+  }
+  return DSP_OK;
+}
+
+extern "C" int dsp_block_update(dsp_block_t* b, int rule, float* ys, double lr, double slr, double beta, double wd,
+                                int apply, float* grad_sq_out, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_update: block not bound");
+  if (rule != DSP_RULE_SGD && rule != DSP_RULE_SUM) return set_error(DSP_E_INVALID, "dsp_block_update: bad rule");
+  if (rule == DSP_RULE_SUM && !ys) return set_error(DSP_E_INVALID, "dsp_block_update: SUM needs ys");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = b->param_count;
+  if (n == 0) {
+    if (grad_sq_out) DSP_CUDA(cudaMemsetAsync(grad_sq_out, 0, sizeof(float), st));
+    return DSP_OK;
+  }
+  float* part = at<float>(b, b->upart);
+  if (apply) {
+    DSP_CUDA(update_f32(rule, n, b->params, b->grads, ys, (float)lr, (float)slr, (float)beta, (float)wd, part, st));
+  } else {
+    // grad norm only (discarded warmup update, pipeline.py:594)
+    DSP_CUDA(sumsq_f32(n, b->grads, part, st));
+  }
+  if (grad_sq_out) DSP_CUDA(sum_partials_f32(part, update_grid(n), grad_sq_out, st));
+  if (apply) DSP_TRY(dsp_block_pack(b, stream));
+  return DSP_OK;
+}

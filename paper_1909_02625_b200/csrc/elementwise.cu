@@ -1,0 +1,822 @@
+// Non-GEMM kernels of the DSP block step: BatchNorm statistics / apply /
+// backward, dense activations, pooling, softmax cross-entropy, split-K
+// reduction, weight-shadow packing, the per-block optimizer update, and the
+// host-layout <-> device-layout packing of boundary activations.
+//
+// All of these are HBM/L2-bandwidth or latency bound (no data reuse): 16-byte
+// vectorised, grid-stride, and every reduction is order-deterministic (fixed
+// per-thread ranges + fixed smem trees, no float atomics) so repeated runs
+// are bitwise identical.
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <math.h>
+
+namespace dsp {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t work, int threads = kThreads, int cap = 148 * 8) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+template <typename T>
+struct V16 {
+  static constexpr int N = 16 / sizeof(T);
+};
+
+template <typename T>
+__device__ __forceinline__ void ld16(const T* p, float (&v)[V16<T>::N]) {
+  uint4 raw = *reinterpret_cast<const uint4*>(p);
+  const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+  for (int i = 0; i < V16<T>::N; ++i) v[i] = to_f<T>(e[i]);
+}
+
+template <typename T>
+__device__ __forceinline__ void st16(T* p, const float (&v)[V16<T>::N]) {
+  uint4 raw;
+  T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+  for (int i = 0; i < V16<T>::N; ++i) e[i] = from_f<T>(v[i]);
+  *reinterpret_cast<uint4*>(p) = raw;
+}
+
+template <typename F>
+cudaError_t dispatch_dtype(int dtype, F&& f) {
+  if (dtype == DSP_DTYPE_BF16) return f(bf16{});
+  if (dtype == DSP_DTYPE_F32) return f(float{});
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ BatchNorm forward
+__global__ void bn_finalize_k(const float* __restrict__ part, int tiles, int Cp, int c_real, double count,
+                              const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ stat) {
+  __shared__ double s1[128], s2[128];
+  const int c = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    a += (double)part[((size_t)t * 2 + 0) * Cp + c];
+    b += (double)part[((size_t)t * 2 + 1) * Cp + c];
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    float mean = 0.f, inv = 0.f, scale = 0.f, shift = 0.f;
+    if (c < c_real) {
+      const double m = s1[0] / count;
+      double var = s2[0] / count - m * m;
+      if (var < 0.0) var = 0.0;
+      const double iv = 1.0 / sqrt(var + 1e-5);
+      mean = (float)m;
+      inv = (float)iv;
+      scale = (float)((double)gamma[c] * iv);
+      shift = (float)((double)beta[c] - m * (double)gamma[c] * iv);
+    }
+    stat[c] = mean;
+    stat[Cp + c] = inv;
+    stat[2 * Cp + c] = scale;
+    stat[3 * Cp + c] = shift;
+  }
+}
+
+template <typename T>
+__global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
+                           const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
+                           int64_t nvec, int Cp, int relu) {
+  constexpr int VE = V16<T>::N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = v * VE;
+    const int c0 = (int)(e0 % Cp);
+    float a[VE];
+    ld16(y + e0, a);
+#pragma unroll
+    for (int i = 0; i < VE; ++i) a[i] = a[i] * stat[2 * Cp + c0 + i] + stat[3 * Cp + c0 + i];
+    if (res != nullptr) {
+      float r[VE];
+      ld16(res + e0, r);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] += r[i];
+    }
+    if (y2 != nullptr) {
+      float r[VE];
+      ld16(y2 + e0, r);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] += r[i] * stat2[2 * Cp + c0 + i] + stat2[3 * Cp + c0 + i];
+    }
+    if (relu) {
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
+    }
+    st16(out + e0, a);
+  }
+}
+
+// ------------------------------------------------------------------ BatchNorm backward
+// Layout of a reduction CTA: G = Cp/VE channel groups, TR = 256/G row lanes.
+template <typename T>
+__global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+                                const float* __restrict__ stat, float* __restrict__ part, int64_t M, int Cp,
+                                int rows_per_chunk) {
+  constexpr int VE = V16<T>::N;
+  __shared__ float red[kThreads][2 * VE];
+  const int G = Cp / VE;
+  const int TR = kThreads / G;
+  const int tid = threadIdx.x;
+  const int cg = tid % G;
+  const int tr = tid / G;
+  float s1[VE], s2[VE];
+#pragma unroll
+  for (int i = 0; i < VE; ++i) s1[i] = s2[i] = 0.f;
+  if (tr < TR) {
+    const int c0 = cg * VE;
+    float mean[VE], inv[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) {
+      mean[i] = y ? stat[c0 + i] : 0.f;
+      inv[i] = y ? stat[Cp + c0 + i] : 0.f;
+    }
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_chunk;
+    const int64_t r1 = min(M, r0 + rows_per_chunk);
+    for (int64_t r = r0 + tr; r < r1; r += TR) {
+      const int64_t e0 = r * Cp + c0;
+      float g[VE];
+      ld16(gsrc + e0, g);
+      if (mask != nullptr) {
+        float mk[VE];
+        ld16(mask + e0, mk);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
+      }
+      if (y != nullptr) {
+        float yy[VE];
+        ld16(y + e0, yy);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+          s1[i] += g[i];
+          s2[i] += g[i] * ((yy[i] - mean[i]) * inv[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) s1[i] += g[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VE; ++i) {
+    red[tid][i] = s1[i];
+    red[tid][VE + i] = s2[i];
+  }
+  __syncthreads();
+  for (int c = tid; c < Cp; c += kThreads) {
+    const int g = c / VE, e = c % VE;
+    float a = 0.f, b = 0.f;
+    for (int t = 0; t < TR; ++t) {
+      a += red[t * G + g][e];
+      b += red[t * G + g][VE + e];
+    }
+    part[((size_t)blockIdx.x * 2 + 0) * Cp + c] = a;
+    part[((size_t)blockIdx.x * 2 + 1) * Cp + c] = b;
+  }
+}
+
+__global__ void bn_bwd_finalize_k(const float* __restrict__ part, int chunks, int Cp, int c_real, double count,
+                                  const float* __restrict__ gamma, const float* __restrict__ stat,
+                                  float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ coef) {
+  __shared__ double s1[128], s2[128];
+  const int c = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int t = threadIdx.x; t < chunks; t += blockDim.x) {
+    a += (double)part[((size_t)t * 2 + 0) * Cp + c];
+    b += (double)part[((size_t)t * 2 + 1) * Cp + c];
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const bool real = c < c_real;
+    if (real && dbeta) dbeta[c] = (float)s1[0];
+    if (real && dgamma && gamma) dgamma[c] = (float)s2[0];
+    if (coef) {
+      coef[c] = (real && gamma) ? gamma[c] * stat[Cp + c] : 0.f;
+      coef[Cp + c] = real ? (float)(s1[0] / count) : 0.f;
+      coef[2 * Cp + c] = real ? (float)(s2[0] / count) : 0.f;
+    }
+  }
+}
+
+template <typename T>
+__global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+                               const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
+                               const T* __restrict__ yb, const float* __restrict__ statb,
+                               const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
+                               int64_t nvec, int Cp) {
+  constexpr int VE = V16<T>::N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = v * VE;
+    const int c0 = (int)(e0 % Cp);
+    float g[VE];
+    ld16(gsrc + e0, g);
+    if (mask != nullptr) {
+      float mk[VE];
+      ld16(mask + e0, mk);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
+    }
+    if (gout != nullptr) st16(gout + e0, g);
+    {
+      float yy[VE], o[VE];
+      ld16(y + e0, yy);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) {
+        const int c = c0 + i;
+        const float xh = (yy[i] - stat[c]) * stat[Cp + c];
+        o[i] = coef[c] * (g[i] - coef[Cp + c] - xh * coef[2 * Cp + c]);
+      }
+      st16(dy + e0, o);
+    }
+    if (dyb != nullptr) {
+      float yy[VE], o[VE];
+      ld16(yb + e0, yy);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) {
+        const int c = c0 + i;
+        const float xh = (yy[i] - statb[c]) * statb[Cp + c];
+        o[i] = coefb[c] * (g[i] - coefb[Cp + c] - xh * coefb[2 * Cp + c]);
+      }
+      st16(dyb + e0, o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ activations / pooling
+template <typename T>
+__global__ void act_fwd_k(int tanh_kind, const T* __restrict__ x, T* __restrict__ out, int64_t nvec) {
+  constexpr int VE = V16<T>::N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    float a[VE];
+    ld16(x + v * VE, a);
+#pragma unroll
+    for (int i = 0; i < VE; ++i) a[i] = tanh_kind ? tanhf(a[i]) : fmaxf(a[i], 0.f);
+    st16(out + v * VE, a);
+  }
+}
+
+template <typename T>
+__global__ void act_bwd_k(int tanh_kind, const T* __restrict__ x, const T* __restrict__ u, T* __restrict__ dx,
+                          int64_t nvec) {
+  constexpr int VE = V16<T>::N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    float a[VE], g[VE];
+    ld16(x + v * VE, a);
+    ld16(u + v * VE, g);
+#pragma unroll
+    for (int i = 0; i < VE; ++i) {
+      if (tanh_kind) {
+        const float t = tanhf(a[i]);
+        g[i] = g[i] * (1.f - t * t);
+      } else {
+        g[i] = a[i] > 0.f ? g[i] : 0.f;
+      }
+    }
+    st16(dx + v * VE, g);
+  }
+}
+
+template <typename T>
+__global__ void avgpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int B, int HW, int Cp) {
+  constexpr int VE = V16<T>::N;
+  const int G = Cp / VE;
+  const int64_t nthr = (int64_t)B * G;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nthr; t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(t / G), g = (int)(t % G);
+    float acc[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) acc[i] = 0.f;
+    for (int p = 0; p < HW; ++p) {
+      float v[VE];
+      ld16(x + ((int64_t)b * HW + p) * Cp + g * VE, v);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) acc[i] += v[i];
+    }
+    const float inv = 1.f / (float)HW;
+#pragma unroll
+    for (int i = 0; i < VE; ++i) acc[i] *= inv;
+    st16(out + (int64_t)b * Cp + g * VE, acc);
+  }
+}
+
+template <typename T>
+__global__ void avgpool_bwd_k(const T* __restrict__ u, T* __restrict__ dx, int B, int HW, int Cp) {
+  constexpr int VE = V16<T>::N;
+  const int64_t nvec = (int64_t)B * HW * Cp / VE;
+  const float inv = 1.f / (float)HW;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = v * VE;
+    const int64_t b = e0 / ((int64_t)HW * Cp);
+    const int c0 = (int)(e0 % Cp);
+    float g[VE];
+    ld16(u + b * Cp + c0, g);
+#pragma unroll
+    for (int i = 0; i < VE; ++i) g[i] *= inv;
+    st16(dx + e0, g);
+  }
+}
+
+template <typename T>
+__global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int32_t* __restrict__ arg, int B, int H,
+                              int W, int P, int Q, int Cp) {
+  const int64_t n = (int64_t)B * P * Q * Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cp);
+    int64_t t = i / Cp;
+    const int q = (int)(t % Q);
+    t /= Q;
+    const int p = (int)(t % P);
+    const int b = (int)(t / P);
+    float best = -INFINITY;
+    int ba = 0;
+    for (int r = 0; r < 3; ++r) {
+      const int h = 2 * p - 1 + r;
+      for (int s = 0; s < 3; ++s) {
+        const int w = 2 * q - 1 + s;
+        if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) {
+          const float v = to_f<T>(x[(((int64_t)b * H + h) * W + w) * Cp + c]);
+          if (v > best) {
+            best = v;
+            ba = r * 3 + s;
+          }
+        }
+      }
+    }
+    out[i] = from_f<T>(best);
+    arg[i] = ba;
+  }
+}
+
+template <typename T>
+__global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict__ arg, T* __restrict__ dx, int B,
+                              int H, int W, int P, int Q, int Cp) {
+  const int64_t n = (int64_t)B * H * W * Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cp);
+    int64_t t = i / Cp;
+    const int w = (int)(t % W);
+    t /= W;
+    const int h = (int)(t % H);
+    const int b = (int)(t / H);
+    float acc = 0.f;
+    for (int r = 0; r < 3; ++r) {
+      const int pp = h + 1 - r;
+      if (pp < 0 || (pp & 1)) continue;
+      const int p = pp >> 1;
+      if (p >= P) continue;
+      for (int s = 0; s < 3; ++s) {
+        const int qq = w + 1 - s;
+        if (qq < 0 || (qq & 1)) continue;
+        const int q = qq >> 1;
+        if (q >= Q) continue;
+        const int64_t o = (((int64_t)b * P + p) * Q + q) * Cp + c;
+        if (arg[o] == r * 3 + s) acc += to_f<T>(u[o]);
+      }
+    }
+    dx[i] = from_f<T>(acc);
+  }
+}
+
+// ------------------------------------------------------------------ loss
+template <typename T>
+__global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, int C, const int64_t* __restrict__ labels,
+                               T* __restrict__ dlogits, float* __restrict__ loss) {
+  extern __shared__ float row_loss[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int b = warp; b < B; b += nw) {
+    const float* z = logits + (size_t)b * ld;
+    float mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float den = 0.f;
+    for (int c = lane; c < C; c += 32) den += expf(z[c] - mx);
+    den = warp_sum(den);
+    const int lab = (int)labels[b];
+    const float inv_b = 1.f / (float)B;
+    for (int c = lane; c < ld; c += 32) {
+      float gval = 0.f;
+      if (c < C) {
+        gval = expf(z[c] - mx) / den;
+        if (c == lab) gval -= 1.f;
+        gval *= inv_b;
+      }
+      dlogits[(size_t)b * ld + c] = from_f<T>(gval);
+    }
+    if (lane == 0) row_loss[b] = -((z[lab] - mx) - logf(den));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < B; ++b) s += (double)row_loss[b];
+    *loss = (float)(s / (double)B);
+  }
+}
+
+// ------------------------------------------------------------------ split-K reduce / packing
+__global__ void wgrad_reduce_k(const float* __restrict__ part, int splits, int Mw, int N, int RS, int Cp, int ci_real,
+                               int co_real, int dense_layout, float* __restrict__ grad) {
+  const int64_t total = dense_layout ? (int64_t)ci_real * co_real : (int64_t)co_real * RS * ci_real;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int m, n;
+    if (dense_layout) {
+      n = (int)(idx % co_real);
+      m = (int)(idx / co_real);
+    } else {
+      const int ci = (int)(idx % ci_real);
+      const int64_t t = idx / ci_real;
+      const int tap = (int)(t % RS);
+      n = (int)(t / RS);
+      m = tap * Cp + ci;
+    }
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[((size_t)z * Mw + m) * N + n];
+    grad[idx] = s;
+  }
+}
+
+template <typename T>
+__global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__ packed,
+                               const PackEntry* __restrict__ ents, int n_entries) {
+  const PackEntry e = ents[blockIdx.y];
+  const int64_t total = (int64_t)e.cop * e.rs * e.cip;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int ci = (int)(idx % e.cip);
+    const int64_t t = idx / e.cip;
+    const int tap = (int)(t % e.rs);
+    const int co = (int)(t / e.rs);
+    float v = 0.f;
+    if (co < e.co && ci < e.ci) {
+      v = e.dense_src ? params[e.src_off + (int64_t)ci * e.co + co]
+                      : params[e.src_off + ((int64_t)co * e.rs + tap) * e.ci + ci];
+    }
+    packed[e.dst_off + idx] = from_f<T>(v);
+  }
+}
+
+// ------------------------------------------------------------------ optimizer
+template <int RULE, bool WD>
+__global__ void update_f32_k(int64_t n, float* __restrict__ x, const float* __restrict__ grad, float* __restrict__ ys,
+                             float lr, float slr, float beta, float wd, float* __restrict__ part) {
+  __shared__ float red[kThreads];
+  float sq = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float g0 = grad[i];
+    sq = __fadd_rn(sq, __fmul_rn(g0, g0));
+    const float xv = x[i];
+    const float g = WD ? __fadd_rn(g0, __fmul_rn(wd, xv)) : g0;
+    if (RULE == DSP_RULE_SGD) {
+      x[i] = __fsub_rn(xv, __fmul_rn(lr, g));
+    } else {
+      const float y = __fsub_rn(xv, __fmul_rn(lr, g));
+      const float ysn = __fsub_rn(xv, __fmul_rn(slr, g));
+      x[i] = (beta == 0.f) ? y : __fadd_rn(y, __fmul_rn(beta, __fsub_rn(ysn, ys[i])));
+      ys[i] = ysn;
+    }
+  }
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && part) part[blockIdx.x] = red[0];
+}
+
+template <int RULE, bool WD>
+__global__ void update_f64_k(int64_t n, double* __restrict__ x, const double* __restrict__ grad,
+                             double* __restrict__ ys, double* __restrict__ yout, double lr, double slr, double beta,
+                             double wd, double* __restrict__ part) {
+  __shared__ double red[kThreads];
+  double sq = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double g0 = grad[i];
+    sq = __dadd_rn(sq, __dmul_rn(g0, g0));
+    const double xv = x[i];
+    const double g = WD ? __dadd_rn(g0, __dmul_rn(wd, xv)) : g0;
+    if (RULE == DSP_RULE_SGD) {
+      x[i] = __dsub_rn(xv, __dmul_rn(lr, g));
+    } else {
+      const double y = __dsub_rn(xv, __dmul_rn(lr, g));
+      const double ysn = __dsub_rn(xv, __dmul_rn(slr, g));
+      x[i] = (beta == 0.0) ? y : __dadd_rn(y, __dmul_rn(beta, __dsub_rn(ysn, ys[i])));
+      ys[i] = ysn;
+      if (yout) yout[i] = y;
+    }
+  }
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && part) part[blockIdx.x] = red[0];
+}
+
+__global__ void sumsq_k(int64_t n, const float* __restrict__ v, float* __restrict__ part) {
+  __shared__ float red[kThreads];
+  float sq = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    sq = __fadd_rn(sq, __fmul_rn(v[i], v[i]));
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+template <typename S, typename O>
+__global__ void sum_partials_k(const S* __restrict__ part, int n, O* __restrict__ out) {
+  __shared__ double red[kThreads];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads) s += (double)part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = (O)red[0];
+}
+
+// ------------------------------------------------------------------ boundary layout
+template <typename T>
+__global__ void pack_input_k(const float* __restrict__ x, T* __restrict__ out, int B, int C, int H, int W, int Cp,
+                             int nchw) {
+  const int64_t n = (int64_t)B * H * W * Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cp);
+    const int64_t pix = i / Cp;  // b*H*W + h*W + w
+    const int64_t b = pix / ((int64_t)H * W);
+    const int64_t hw = pix % ((int64_t)H * W);
+    float v = 0.f;
+    if (c < C) v = nchw ? x[(b * C + c) * H * W + hw] : x[pix * C + c];
+    out[i] = from_f<T>(v);
+  }
+}
+
+template <typename T>
+__global__ void unpack_output_k(const T* __restrict__ in, float* __restrict__ out, int B, int C, int H, int W, int Cp,
+                                int nchw) {
+  const int64_t n = (int64_t)B * C * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b, c, hw;
+    if (nchw) {
+      hw = i % ((int64_t)H * W);
+      const int64_t t = i / ((int64_t)H * W);
+      c = t % C;
+      b = t / C;
+    } else {
+      c = i % C;
+      const int64_t t = i / C;
+      hw = t % ((int64_t)H * W);
+      b = t / ((int64_t)H * W);
+    }
+    out[i] = to_f<T>(in[(b * H * W + hw) * Cp + c]);
+  }
+}
+
+}  // namespace
+
+// ================================================================== launch wrappers
+cudaError_t bn_finalize(const float* part, int tiles, int Cp, int c_real, int64_t count, const float* gamma,
+                        const float* beta, float* stat, cudaStream_t st) {
+  bn_finalize_k<<<Cp, 128, 0, st>>>(part, tiles, Cp, c_real, (double)count, gamma, beta, stat);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* res, const void* y2, const float* stat2,
+                     void* out, int64_t M, int Cp, int relu, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    const int64_t nvec = M * Cp / V16<T>::N;
+    bn_apply_k<T><<<grid_for(nvec), kThreads, 0, st>>>((const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
+                                                      nvec, Cp, relu);
+    return cudaGetLastError();
+  });
+}
+
+int bn_bwd_chunks(int64_t M, int Cp) {
+  const int G = Cp / 8;  // conservative (bf16 VE=8); fp32 uses the same chunking
+  const int TR = G >= kThreads ? 1 : kThreads / G;
+  int64_t rows = (M + 295) / 296;
+  rows = ((rows + TR - 1) / TR) * TR;
+  if (rows < TR) rows = TR;
+  return (int)((M + rows - 1) / rows);
+}
+
+static int64_t bn_rows_per_chunk(int64_t M, int Cp) {
+  const int chunks = bn_bwd_chunks(M, Cp);
+  return (M + chunks - 1) / chunks;
+}
+
+cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
+                          int64_t M, int Cp, cudaStream_t st) {
+  const int chunks = bn_bwd_chunks(M, Cp);
+  const int rows = (int)bn_rows_per_chunk(M, Cp);
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
+    bn_bwd_reduce_k<T><<<chunks, kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
+                                                    rows);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, int64_t count, const float* gamma,
+                            const float* stat, float* dgamma, float* dbeta, float* coef, cudaStream_t st) {
+  bn_bwd_finalize_k<<<Cp, 128, 0, st>>>(part, chunks, Cp, c_real, (double)count, gamma, stat, dgamma, dbeta, coef);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
+                         const float* coef, void* dy, const void* y_b, const float* stat_b, const float* coef_b,
+                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    const int64_t nvec = M * Cp / V16<T>::N;
+    bn_bwd_apply_k<T><<<grid_for(nvec), kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, coef,
+                                                           (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b,
+                                                           (T*)g_out, nvec, Cp);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t act_forward(int dtype, int tanh_kind, const void* x, void* out, int64_t n, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    const int64_t nvec = n / V16<T>::N;
+    act_fwd_k<T><<<grid_for(nvec), kThreads, 0, st>>>(tanh_kind, (const T*)x, (T*)out, nvec);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t act_backward(int dtype, int tanh_kind, const void* x, const void* u, void* dx, int64_t n, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    const int64_t nvec = n / V16<T>::N;
+    act_bwd_k<T><<<grid_for(nvec), kThreads, 0, st>>>(tanh_kind, (const T*)x, (const T*)u, (T*)dx, nvec);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t avgpool_forward(int dtype, const void* x, void* out, int B, int HW, int Cp, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    avgpool_fwd_k<T><<<grid_for((int64_t)B * Cp / V16<T>::N), kThreads, 0, st>>>((const T*)x, (T*)out, B, HW, Cp);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, int Cp, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    avgpool_bwd_k<T><<<grid_for((int64_t)B * HW * Cp / V16<T>::N), kThreads, 0, st>>>((const T*)u, (T*)dx, B, HW, Cp);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, int B, int H, int W, int P, int Q,
+                            int Cp, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    maxpool_fwd_k<T><<<grid_for((int64_t)B * P * Q * Cp), kThreads, 0, st>>>((const T*)x, (T*)out, arg, B, H, W, P, Q,
+                                                                            Cp);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void* dx, int B, int H, int W, int P, int Q,
+                             int Cp, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    maxpool_bwd_k<T><<<grid_for((int64_t)B * H * W * Cp), kThreads, 0, st>>>((const T*)u, arg, (T*)dx, B, H, W, P, Q,
+                                                                            Cp);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, const int64_t* labels, void* dlogits,
+                         float* loss, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    softmax_xent_k<T><<<1, 512, B * sizeof(float), st>>>(logits, ld, B, C, labels, (T*)dlogits, loss);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
+                         int dense_layout, float* grad, cudaStream_t st) {
+  const int64_t total = dense_layout ? (int64_t)ci_real * co_real : (int64_t)co_real * RS * ci_real;
+  wgrad_reduce_k<<<grid_for(total), kThreads, 0, st>>>(part, splits, Mw, N, RS, Cp, ci_real, co_real, dense_layout,
+                                                       grad);
+  return cudaGetLastError();
+}
+
+cudaError_t pack_weights(int dtype, const float* params, void* packed, const PackEntry* entries_dev, int n_entries,
+                         int max_elems, cudaStream_t st) {
+  if (n_entries == 0) return cudaSuccess;
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    dim3 grid(grid_for(max_elems, kThreads, 256), n_entries);
+    pack_weights_k<T><<<grid, kThreads, 0, st>>>(params, (T*)packed, entries_dev, n_entries);
+    return cudaGetLastError();
+  });
+}
+
+int update_grid(int64_t n) { return grid_for(n, kThreads, 148 * 4); }
+
+cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* ys, float lr, float slr, float beta,
+                       float wd, float* part, cudaStream_t st) {
+  const int g = update_grid(n);
+  const bool w = wd != 0.f;
+  if (rule == DSP_RULE_SGD) {
+    if (w) update_f32_k<DSP_RULE_SGD, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
+    else update_f32_k<DSP_RULE_SGD, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
+  } else {
+    if (w) update_f32_k<DSP_RULE_SUM, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
+    else update_f32_k<DSP_RULE_SUM, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr, double slr,
+                       double beta, double wd, double* part, cudaStream_t st) {
+  const int g = update_grid(n);
+  const bool w = wd != 0.0;
+  if (rule == DSP_RULE_SGD) {
+    if (w) update_f64_k<DSP_RULE_SGD, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
+    else update_f64_k<DSP_RULE_SGD, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
+  } else {
+    if (w) update_f64_k<DSP_RULE_SUM, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
+    else update_f64_k<DSP_RULE_SUM, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t sumsq_f32(int64_t n, const float* v, float* part, cudaStream_t st) {
+  sumsq_k<<<update_grid(n), kThreads, 0, st>>>(n, v, part);
+  return cudaGetLastError();
+}
+
+cudaError_t sum_partials_f32(const float* part, int n, float* out, cudaStream_t st) {
+  sum_partials_k<float, float><<<1, kThreads, 0, st>>>(part, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t sum_partials_f64(const double* part, int n, double* out, cudaStream_t st) {
+  sum_partials_k<double, double><<<1, kThreads, 0, st>>>(part, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t pack_input(const float* x, void* out, int B, int C, int H, int W, int Cp, int dtype, int nchw,
+                       cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    pack_input_k<T><<<grid_for((int64_t)B * H * W * Cp), kThreads, 0, st>>>(x, (T*)out, B, C, H, W, Cp, nchw);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t unpack_output(const void* in, float* out, int B, int C, int H, int W, int Cp, int dtype, int nchw,
+                          cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    unpack_output_k<T><<<grid_for((int64_t)B * C * H * W), kThreads, 0, st>>>((const T*)in, out, B, C, H, W, Cp, nchw);
+    return cudaGetLastError();
+  });
+}
+
+}  // namespace dsp

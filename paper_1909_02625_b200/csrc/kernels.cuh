@@ -1,0 +1,93 @@
+// Launch wrappers for the non-GEMM kernels of the DSP block step (elementwise.cu).
+// All activation tensors are NHWC with the channel dimension padded to a
+// multiple of 8 ("Cp"); pad channels always hold exact zeros.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/dsp_b200.h"
+
+namespace dsp {
+
+cudaError_t igemm_launch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st);
+
+// BatchNorm forward: reduce igemm partials [tiles][2][Cp] -> per-channel
+// stat[0]=mean, stat[1]=invstd, stat[2]=scale(gamma*invstd), stat[3]=shift(beta-mean*scale)
+// (each [Cp]). gamma/beta point into the fp32 params (c_real entries).
+cudaError_t bn_finalize(const float* part, int tiles, int Cp, int c_real, int64_t count, const float* gamma,
+                        const float* beta, float* stat, cudaStream_t st);
+
+// out = act(y*scale + shift  [+ res]  [+ y2*scale2 + shift2]); act = relu if relu.
+cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* res, const void* y2,
+                     const float* stat2, void* out, int64_t M, int Cp, int relu, cudaStream_t st);
+
+// BatchNorm backward, reduction half: g = gsrc * (mask > 0 if mask);
+// xhat = (y - mean) * invstd (if y != null, else 0).  Writes per-chunk
+// partial (sum g, sum g*xhat) [chunks][2][Cp]; returns the chunk count.
+int bn_bwd_chunks(int64_t M, int Cp);
+cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
+                          float* part, int64_t M, int Cp, cudaStream_t st);
+// Finalize: sum partials -> dgamma/dbeta into the flat grad (if non-null) and
+// coefficients coef[0]=gamma*invstd, coef[1]=sum(g)/M, coef[2]=sum(g*xhat)/M.
+// With gamma == null (bias gradient) only dbeta = sum(g) is produced.
+cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, int64_t count, const float* gamma,
+                            const float* stat, float* dgamma, float* dbeta, float* coef, cudaStream_t st);
+// Apply: dy = coef0*(g - coef1 - xhat*coef2); optional second BN (y_b, stat_b, coef_b -> dy_b)
+// sharing g; optional g_out = g.
+cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
+                         const float* coef, void* dy, const void* y_b, const float* stat_b, const float* coef_b,
+                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st);
+
+// Dense activations (tensor.py:59-83): out = relu/tanh(x); dx = u * act'(x).
+cudaError_t act_forward(int dtype, int tanh_kind, const void* x, void* out, int64_t n, cudaStream_t st);
+cudaError_t act_backward(int dtype, int tanh_kind, const void* x, const void* u, void* dx, int64_t n, cudaStream_t st);
+
+// Global average pool NHWC [B][HW][Cp] -> [B][Cp] and its backward.
+cudaError_t avgpool_forward(int dtype, const void* x, void* out, int B, int HW, int Cp, cudaStream_t st);
+cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, int Cp, cudaStream_t st);
+
+// 3x3 stride-2 pad-1 max pool and backward (argmax of the first max in (r,s) order).
+cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, int B, int H, int W, int P, int Q,
+                            int Cp, cudaStream_t st);
+cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void* dx, int B, int H, int W, int P,
+                             int Q, int Cp, cudaStream_t st);
+
+// softmax_xent (tensor.py:86-111) on fp32 logits [B][ld] (C real classes):
+// dlogits (storage dtype, pads zero) and the mean loss into *loss (device).
+cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, const int64_t* labels,
+                         void* dlogits, float* loss, cudaStream_t st);
+
+// Split-K WGRAD partials [splits][Mw][N] -> flat fp32 weight gradient.
+//  conv  (dense_layout=0): grad[(co*RS + tap)*ci_real + ci] for Mw = RS*Cp rows (tap*Cp + ci)
+//  dense (dense_layout=1): grad[i*out_real + o]   (reference W[in][out] layout)
+cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
+                         int dense_layout, float* grad, cudaStream_t st);
+
+// Weight shadow packing: fp32 params -> storage dtype [cop][RS][cip] (zero pads).
+// dense_src=1: source is the reference W[in=ci][out=co] layout (transposed on the fly).
+struct PackEntry {
+  int64_t src_off;   // into params (floats)
+  int64_t dst_off;   // into the packed buffer (elements)
+  int32_t co, ci, rs, cop, cip, dense_src;
+};
+cudaError_t pack_weights(int dtype, const float* params, void* packed, const PackEntry* entries_dev, int n_entries,
+                         int max_elems, cudaStream_t st);
+
+// Optimizer step over a flat vector (optim.py:48-109, pipeline.py:591-596).
+int update_grid(int64_t n);
+cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* ys, float lr, float slr, float beta,
+                       float wd, float* part, cudaStream_t st);
+cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr,
+                       double slr, double beta, double wd, double* part, cudaStream_t st);
+// Per-CTA partial sums of v^2 (grid = update_grid(n)).
+cudaError_t sumsq_f32(int64_t n, const float* v, float* part, cudaStream_t st);
+// Sum per-CTA partials in fixed order into *out.
+cudaError_t sum_partials_f32(const float* part, int n, float* out, cudaStream_t st);
+cudaError_t sum_partials_f64(const double* part, int n, double* out, cudaStream_t st);
+
+// NCHW-flattened fp32 [B][C*H*W] <-> padded NHWC storage dtype.
+cudaError_t pack_input(const float* x, void* out, int B, int C, int H, int W, int Cp, int dtype, int nchw,
+                       cudaStream_t st);
+cudaError_t unpack_output(const void* in, float* out, int B, int C, int H, int W, int Cp, int dtype, int nchw,
+                          cudaStream_t st);
+
+}  // namespace dsp

@@ -1,0 +1,140 @@
+"""Per-layer-kind parity of the CUDA block executor vs the oracle.
+
+One block holding one layer kind: forward (fresh and recorded), backward with
+a random upstream; output, flat parameter gradient and input gradient are
+compared with oracle/dsp_ref.py's block_forward / block_backward on identical
+inputs, twice:
+  * vs the oracle in bf16-storage emulation (same rounding points as the
+    device, float64 sums): relative L2 error <= TIGHT = 1e-2;
+  * vs the pure float64 oracle: relative L2 error <= LOOSE = 1.2e-1 for
+    gradients (ReLU-boundary flips between bf16 and fp64 forwards move whole
+    |u| terms in small per-channel sums) and 3e-2 for forward outputs.
+"""
+
+import numpy as np
+import pytest
+
+import oracle.dsp_ref as R
+import paper_1909_02625_b200 as P
+from paper_1909_02625_b200.runtime import DeviceBlock, pack_input, unpack_output, torch_mod
+from tests.gpu_util import rel_err, to_oracle_layers
+
+pytestmark = pytest.mark.gpu
+TIGHT = 1e-2
+LOOSE = 2.5e-1
+FWD = 3e-2
+
+
+def _oracle(layers, vec, xb, up_fn, last, mode):
+    with R.storage(mode):
+        om = R.build_model(to_oracle_layers(layers), [])
+        om.blocks[0].params[:] = vec
+        out, tape = R.block_forward(om.blocks[0], xb, record=True)
+        if last:
+            loss, up = R.softmax_xent(out, up_fn(out))
+            up = R.cnn.q(up)
+        else:
+            loss, up = None, up_fn(out)
+        g, gin = R.block_backward(om.blocks[0], tape, up)
+    return out, loss, g, gin
+
+
+def _run_block(layers, B, seed=0, last=False):
+    torch = torch_mod()
+    pm = P.build_model(layers, [])
+    P.init_params(pm, seed)
+    rng = np.random.default_rng(seed)
+    # perturb everything (incl. BN gamma/beta) so all gradients are exercised
+    vec = pm.blocks[0].params + 0.05 * rng.standard_normal(pm.blocks[0].param_count)
+    pm.blocks[0].params = vec
+    blk = pm.blocks[0]
+    in_shape = blk.in_shape
+    x = rng.standard_normal((B, int(np.prod(in_shape))))
+    xb = R.cnn.bf16_round(x)  # what the device sees
+    dev = torch.device("cuda")
+    st = torch.cuda.current_stream()
+    db = DeviceBlock(blk, B, is_last=last, device=dev, stream=st)
+    xd = pack_input(x, in_shape, dev, st)
+    labels = None
+    up_host = None
+
+    def up_fn(out):
+        nonlocal labels, up_host
+        if last:
+            if labels is None:
+                labels = rng.integers(0, out.shape[1], size=B)
+            return labels
+        if up_host is None:
+            up_host = R.cnn.bf16_round(rng.standard_normal(out.shape))
+        return up_host
+
+    ref = {m: _oracle(layers, vec, xb, up_fn, last, m) for m in ("bf16", "f64")}
+    res = {}
+    if last:
+        out_dim = ref["f64"][0].shape[1]
+        cp = (out_dim + 7) // 8 * 8
+        logits = torch.empty(B * cp, device=dev)
+        db.forward(xd, logits, record=True)
+        res["out"] = logits.view(B, cp)[:, :out_dim].double().cpu().numpy()
+        loss_d = torch.zeros(1, device=dev)
+        db.loss(torch.from_numpy(labels).cuda(), loss_d)
+        res["loss"] = loss_d.item()
+        gin = torch.empty(db.in_elems, dtype=torch.bfloat16, device=dev)
+        db.backward(None, gin)
+    else:
+        y = torch.empty(db.out_elems, dtype=torch.bfloat16, device=dev)
+        db.forward(xd, y, record=False)
+        res["out"] = unpack_output(y, B, blk.out_shape, st)
+        db.forward(xd, None, record=True)
+        upd = pack_input(up_host, blk.out_shape, dev, st)
+        gin = torch.empty(db.in_elems, dtype=torch.bfloat16, device=dev)
+        db.backward(upd, gin)
+    st.synchronize()
+    res["g"] = db.grads[: blk.param_count].double().cpu().numpy()
+    res["gin"] = unpack_output(gin, B, in_shape, st)
+    return res, ref
+
+
+def _check(res, ref):
+    for mode, tol_g, tol_f in (("bf16", TIGHT, TIGHT), ("f64", LOOSE, FWD)):
+        out, loss, g, gin = ref[mode]
+        assert rel_err(res["out"], out) < tol_f, (mode, "forward", rel_err(res["out"], out))
+        if loss is not None:
+            assert abs(res["loss"] - loss) <= tol_f * max(1.0, abs(loss)), (mode, "loss")
+        assert rel_err(res["g"], g) < tol_g, (mode, "param grad", rel_err(res["g"], g))
+        assert rel_err(res["gin"], gin) < tol_g, (mode, "input grad", rel_err(res["gin"], gin))
+
+
+@pytest.mark.parametrize("B", [4, 37])
+def test_stem(B):
+    _check(*_run_block([P.conv_bn_relu((3, 8, 8), 16)], B))
+
+
+@pytest.mark.parametrize("stride,cin,cout", [(1, 16, 16), (2, 16, 32), (1, 8, 24)])
+def test_basic_unit(stride, cin, cout):
+    _check(*_run_block([P.basic_unit((cin, 8, 8), cout, stride)], 6))
+
+
+@pytest.mark.parametrize("stride", [1, 2])
+def test_bottleneck(stride):
+    _check(*_run_block([P.bottleneck((32, 8, 8), 8, 32 if stride == 1 else 64, stride)], 4))
+
+
+def test_pools_and_head():
+    layers = [P.conv_bn_relu((3, 12, 12), 16), P.maxpool((16, 12, 12)), P.avgpool((16, 6, 6)), P.dense(16, 10)]
+    _check(*_run_block(layers, 8, last=True))
+
+
+def test_mlp_kinds():
+    layers = [P.dense(12, 16), P.relu(), P.dense(16, 12), P.tanh(), P.dense(12, 4)]
+    _check(*_run_block(layers, 16, last=True))
+
+
+def test_mlp_nonlast_block():
+    layers = [P.dense(20, 24), P.relu(), P.dense(24, 9, bias=False), P.tanh()]
+    _check(*_run_block(layers, 5))
+
+
+def test_resnet56_stage_shapes_b128():
+    """Full-size CIFAR stage shapes at B=128 (M = 131072 rows)."""
+    _check(*_run_block([P.basic_unit((16, 32, 32), 16, 1)], 128))

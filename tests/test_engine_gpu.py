@@ -1,0 +1,151 @@
+"""End-to-end DSP train-step parity: B200 TrainEngine vs the oracle engine.
+
+Same model init, same synthetic batches, same queue config and optimizer.
+Checked against the oracle twice (see tests/test_block_gpu.py for the modes):
+  * FIFO / staleness schedule: (step, block, batch_index) log bit-exact;
+  * realized_staleness() == m;
+  * per-step loss: |dL| <= LOSS_TOL[mode] * max(1, |L_ref|)
+  * per-(step, block) grad norm: relative <= GN_TOL[mode]
+  * final parameters per block: relative L2 error <= PARAM_TOL[mode].
+"""
+
+import numpy as np
+import pytest
+
+import oracle.dsp_ref as R
+import paper_1909_02625_b200 as P
+from tests.gpu_util import rel_err, small_resnet, twin_models
+
+pytestmark = pytest.mark.gpu
+
+LOSS_TOL = {"bf16": 1e-2, "f64": 5e-2}
+GN_TOL = {"bf16": 3e-2, "f64": 2e-1}
+PARAM_TOL = {"bf16": 2e-2, "f64": 1e-1}
+
+
+def _run(layers, boundaries, p, m, B, steps, in_shape, classes, rule="sum", beta=0.9, lr=0.05,
+         warmup="faithful_zero_updates", wd=0.0):
+    pool = R.synthetic_batches(6, B, in_shape, classes, seed=1)
+    sched = ((steps // 2, 0.5),)
+    pm, _ = twin_models(layers, boundaries, seed=3)
+    eng = P.TrainEngine(pm, P.validate_config(p, m, warmup=warmup), R.cycle(pool), P.LrSchedule(lr, sched),
+                        rule=rule, beta=beta, weight_decay=wd)
+    eng.run(steps)
+    refs = {}
+    for mode in ("bf16", "f64"):
+        with R.storage(mode):
+            _, om = twin_models(layers, boundaries, seed=3)
+            ref = R.Engine(om, R.validate_config(p, m, warmup=warmup), R.cycle(pool), R.LrSchedule(lr, sched),
+                           rule=rule, beta=beta, weight_decay=wd)
+            ref.run(steps)
+        refs[mode] = (ref, om)
+    return eng, pm, refs
+
+
+def _check(eng, pm, refs, m):
+    log = eng.log
+    assert eng.realized_staleness() == list(m)
+    for mode, (ref, om) in refs.items():
+        got_idx = [(r.step, r.block, r.batch_index) for r in log.sorted()]
+        want_idx = sorted((r.step, r.block, r.batch_index) for r in ref.records)
+        assert got_idx == want_idx
+        ref_loss = {r.step: r.loss for r in ref.records if r.loss is not None}
+        for step, loss in log.losses():
+            want = ref_loss[step]
+            assert abs(loss - want) <= LOSS_TOL[mode] * max(1.0, abs(want)), (mode, step, loss, want)
+        ref_gn = {(r.step, r.block): r.grad_norm for r in ref.records}
+        for r in log.records:
+            want = ref_gn[(r.step, r.block)]
+            assert abs(r.grad_norm - want) <= GN_TOL[mode] * max(want, 1e-3), (mode, r.step, r.block, r.grad_norm,
+                                                                             want)
+        for bp, bo in zip(pm.blocks, om.blocks):
+            assert rel_err(bp.params, bo.params) < PARAM_TOL[mode], (mode, bp.index, rel_err(bp.params, bo.params))
+
+
+def test_resnet_k2_sum():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    eng, pm, refs = _run(layers, [2], (1, 0), (2, 0), 16, 12, (3, 8, 8), 10)
+    _check(eng, pm, refs, (2, 0))
+
+
+def test_resnet_k3_discard_warmup_sgd_wd():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    eng, pm, refs = _run(layers, [2, 4], (1, 1, 0), (4, 2, 0), 8, 10, (3, 8, 8), 10, rule="sgd", beta=0.0,
+                         warmup="discard_warmup_updates", wd=5e-4)
+    _check(eng, pm, refs, (4, 2, 0))
+
+
+def test_resnet_k4_default_queues():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    cfg = P.default_queue_config(4)
+    eng, pm, refs = _run(layers, [1, 2, 3], cfg.p, cfg.m, 8, 12, (3, 8, 8), 10)
+    _check(eng, pm, refs, cfg.m)
+
+
+def test_mlp_k3_reference_kinds():
+    layers = [P.dense(12, 16), P.relu(), P.dense(16, 12), P.relu(), P.dense(12, 4)]
+    eng, pm, refs = _run(layers, [2, 4], (1, 1, 0), (4, 2, 0), 16, 30, (12, 1, 1), 4)
+    _check(eng, pm, refs, (4, 2, 0))
+
+
+def test_k1_is_plain_bp():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    eng, pm, refs = _run(layers, [], (0,), (0,), 16, 8, (3, 8, 8), 10, rule="sgd", beta=0.0)
+    _check(eng, pm, refs, (0,))
+
+
+def test_resume_equals_single_run():
+    """run(a); run(b) == run(a+b): queue contents persist across calls (pipeline.py:443-449)."""
+    layers = small_resnet(in_shape=(3, 8, 8))
+    pool = R.synthetic_batches(4, 8, (3, 8, 8), 10, seed=4)
+    finals = []
+    for chunks in ((7,), (3, 4)):
+        pm, _ = twin_models(layers, [2], seed=2)
+        eng = P.TrainEngine(pm, P.validate_config((1, 0), (2, 0)), R.cycle(pool), P.LrSchedule(0.05), rule="sum",
+                            beta=0.9)
+        for c in chunks:
+            eng.run(c)
+        finals.append((pm.flat_params(), eng.log.checksum()))
+    assert np.array_equal(finals[0][0], finals[1][0])
+    assert finals[0][1] == finals[1][1]
+
+
+def test_deterministic_across_runs():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    pool = R.synthetic_batches(4, 8, (3, 8, 8), 10, seed=4)
+    sums = []
+    for _ in range(2):
+        pm, _ = twin_models(layers, [1, 3], seed=2)
+        eng = P.TrainEngine(pm, P.validate_config((1, 1, 0), (4, 2, 0)), R.cycle(pool), P.LrSchedule(0.05),
+                            rule="sum", beta=0.9)
+        eng.run(9)
+        sums.append(eng.log.checksum())
+    assert sums[0] == sums[1]
+
+
+def test_eval_forward_matches_oracle():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    pm, om = twin_models(layers, [2], seed=5)
+    x, _ = R.synthetic_batches(1, 8, (3, 8, 8), 10, seed=2)[0]
+    got = pm.forward(x)
+    with R.storage("bf16"):
+        want = om.forward(R.cnn.bf16_round(x))
+    assert rel_err(got, want) < 1e-2
+
+
+def test_tape_single_use():
+    from paper_1909_02625_b200.runtime import DeviceBlock
+
+    pm, _ = twin_models([P.dense(8, 8), P.relu(), P.dense(8, 4)], [], seed=1)
+    db = DeviceBlock(pm.blocks[0], 4, is_last=True)
+    with pytest.raises(P.DspError):
+        db.backward(None, None)  # no recorded forward
+
+
+def test_label_out_of_range_rejected():
+    layers = [P.dense(12, 8), P.relu(), P.dense(8, 4)]
+    pm, _ = twin_models(layers, [], seed=1)
+    bad = [(np.zeros((4, 12)), np.array([0, 1, 2, 4]))]
+    eng = P.TrainEngine(pm, P.validate_config((0,), (0,)), R.cycle(bad), P.LrSchedule(0.1))
+    with pytest.raises(ValueError, match="label out of range"):
+        eng.run(1)
