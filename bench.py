@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py -- DSP training throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): ResNet-56, synthetic CIFAR-10-shaped
+batches of 128, DSP with K blocks (K=4 for N<=4 GPUs, K=8 for N=8), queue
+config p_k=1, m_k=2(K-1-k), SUM momentum beta=0.9 s=1, lr 0.1,
+weight decay 5e-4, bf16 storage / fp32 accumulate on tcgen05 tensor cores.
+One "step" = one DSP iteration of every block (fresh forward, recompute,
+backward, update) = one batch through the pipeline.
+
+  python bench.py [--gpus N --steps K --warmup W]       # this repo's B200 engine
+  python bench.py --impl reference [...]                  # the CPU oracle (reference algorithm)
+
+Prints ONE JSON line on rank 0. See DESIGN.md §5 for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "training samples/sec (device-timed) at K=1/2/4/8 B200 vs BP; conv tensor-pipe % of peak"
+UNIT = "samples/s"
+L2_BYTES = 126 * 1024 * 1024
+DEPTH = 56
+CLASSES = 10
+IN_SHAPE = (3, 32, 32)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--k", type=int, default=0, help="DSP blocks (default 4, or 8 when --gpus 8)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def blocks_for(args) -> int:
+    if args.k:
+        return args.k
+    return 8 if args.gpus >= 8 else 4
+
+
+def workload(args):
+    import paper_1909_02625_b200 as P
+
+    K = blocks_for(args)
+    layers = P.resnet_cifar_layers(DEPTH, CLASSES)
+    bounds = P.flop_balanced_boundaries(layers, K) if K > 1 else []
+    cfg = P.default_queue_config(K)
+    return layers, bounds, cfg
+
+
+def config_dict(args, K, world):
+    return {"workload": f"ResNet-{DEPTH} DSP K={K}, synthetic CIFAR-10-shaped 32x32x3, batch {args.batch}",
+            "model": f"resnet{DEPTH}-cifar", "global_batch": args.batch, "k_blocks": K,
+            "queues": "p_k=1, m_k=2(K-1-k)", "optimizer": "SUM momentum beta=0.9 s=1, lr 0.1, wd 5e-4",
+            "parallelism": f"dsp-pipeline k{K} over {world} gpu(s)",
+            "l2": "L2 flushed (256 MiB write) between timed steps; step working set > L2"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=1)
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, val in zip(names, r[4:8]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle (reference algorithm)
+def cpu_oracle_steps(args, steps: int, warmup: int, batch: int):
+    """Time the float64 CPU restatement of the reference DSP step (oracle/)."""
+    import oracle.dsp_ref as R
+
+    layers, bounds, cfg = workload(args)
+    olayers = [R.LayerSpec(s.kind, s.in_dim, s.out_dim, s.bias, tuple(s.in_shape), s.out_c, s.mid_c, s.stride,
+                           s.ksize) for s in layers]
+    om = R.build_model(olayers, bounds)
+    R.init_params(om, 0)
+    pool = R.synthetic_batches(4, batch, IN_SHAPE, CLASSES, seed=0)
+    eng = R.Engine(om, R.validate_config(cfg.p, cfg.m), R.cycle(pool), R.LrSchedule(0.1), rule="sum", beta=0.9,
+                   weight_decay=5e-4)
+    eng.run(warmup)
+    t0 = time.perf_counter()
+    r0 = os.times()
+    eng.run(steps)
+    dt = time.perf_counter() - t0
+    r1 = os.times()
+    cpu_s = (r1.user - r0.user) + (r1.system - r0.system)
+    return batch * steps / dt, dt, cpu_s
+
+
+def threads_used() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    K = blocks_for(args)
+    sub = min(args.batch, 32)
+    steps = max(1, args.steps)
+    warm = max(1, min(args.warmup, 3))
+    # bound the run to a few minutes: ~2.7 s per K=4 step at batch 32 on 8 cores
+    budget_s = 150.0
+    est = 0.085 * sub
+    if (steps + warm) * est > budget_s:
+        steps = max(1, int(budget_s / est) - warm)
+    v, dt, cpu_s = cpu_oracle_steps(args, steps, warm, sub)
+    cores = threads_used()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, K, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"oracle/dsp_ref.py float64 DSP step (reference algorithm, CPU restatement), "
+                                       f"ResNet-{DEPTH} K={K}, {steps} timed steps of a {sub}-sample sub-batch "
+                                       f"after {warm} warmup; cpu/wall={cpu_s / dt:.2f}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ B200 arm
+def kernel_roofline(torch, peaks, batch):
+    """Time the dominant kernel alone (CUDA events, launching stream) on rotating
+    buffers larger than L2; achieved = algorithmic bytes / average duration."""
+    import ctypes as C
+
+    from paper_1909_02625_b200 import _lib as L
+
+    lib = L.load()
+    st = torch.cuda.current_stream()
+    # stage-1 3x3 16->16 conv of ResNet-56 at B=128: the most frequent shape of the step
+    nimg, H, W, Cc, K = batch, 32, 32, 16, 16
+    M = nimg * H * W
+    nbuf = max(2, int(2 * L2_BYTES // (M * Cc * 2)) + 1)
+    xs = [torch.randn(M * Cc, device="cuda").bfloat16() for _ in range(nbuf)]
+    ys = [torch.empty(M * K, device="cuda", dtype=torch.bfloat16) for _ in range(nbuf)]
+    w = torch.randn(K * 9 * Cc, device="cuda").bfloat16()
+    tiles = (M + 127) // 128
+    stats = torch.empty(tiles * 2 * K, device="cuda")
+    g = L.ConvGeom(nimg, H, W, Cc, H, W, K, 3, 3, 1, 1)
+
+    def launch(i):
+        a = L.IgemmArgs()
+        a.geom = g
+        a.M, a.N, a.Kd = M, K, 9 * Cc
+        a.A, a.B, a.D = xs[i].data_ptr(), w.data_ptr(), ys[i].data_ptr()
+        a.ldd = K
+        a.stats = stats.data_ptr()
+        L.check(lib.dsp_igemm(L.DSP_IGEMM_FPROP, L.DSP_DTYPE_BF16, C.byref(a), 1, C.c_void_p(st.cuda_stream)))
+
+    for i in range(nbuf):
+        launch(i)
+    torch.cuda.synchronize()
+    reps = 4 * nbuf
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(reps):
+        launch(i % nbuf)
+    e1.record(st)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / 1000.0 / reps
+    algo = M * Cc * 2 + M * K * 2 + K * 9 * Cc * 2 + tiles * 2 * K * 4
+    achieved = algo / t / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "igemm_kernel<bf16,FPROP,16> (ResNet-56 stage-1 conv3x3 16->16 + BN stats, B=128)",
+            "algorithmic_bytes_per_launch": algo, "launch_us": t * 1e6,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_02625_b200 as P
+    from paper_1909_02625_b200 import _lib as L
+    from paper_1909_02625_b200.data import cycle, synthetic_batches, to_device_batches
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = L.load()
+    K = blocks_for(args)
+    layers, bounds, cfg = workload(args)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+
+    host_pool = synthetic_batches(16, args.batch, IN_SHAPE, CLASSES, seed=0)
+    model = P.build_model(layers, bounds)
+    P.init_params(model, 0)
+    stream = torch.cuda.current_stream(dev)
+    dev_pool = to_device_batches(host_pool, IN_SHAPE, dev, stream)
+    eng = P.TrainEngine(model, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(0.1), rule="sum",
+                        beta=0.9, s=1.0, weight_decay=5e-4, device=dev)
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        eng.run(1)
+    torch.cuda.synchronize()
+    barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = lib.dsp_launch_count()
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # evict L2 between timed steps (outside the timed window)
+            starts[i].record(stream)
+            eng.run(1)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = lib.dsp_launch_count() - launches0
+    barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = args.batch * args.steps / (total_ms / 1000.0)
+    loss_ok = True
+    log = eng.log
+    if (K - 1) in eng.local:
+        losses = [lv for _, lv in log.losses()]
+        loss_ok = all(np.isfinite(losses))
+
+    # ---- end to end through the public API: host batches (pinned H2D each step) + D2H loss read
+    e2e = None
+    if not args.no_e2e:
+        model2 = P.build_model(layers, bounds)
+        P.init_params(model2, 0)
+        eng2 = P.TrainEngine(model2, cfg, cycle(host_pool), P.LrSchedule(0.1), rule="sum", beta=0.9, s=1.0,
+                             weight_decay=5e-4, device=dev)
+        for _ in range(3):
+            eng2.run(1)
+            eng2.last_loss()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            eng2.run(1)
+            eng2.last_loss()  # device->host read of the step's result
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+        h2d = args.batch * int(np.prod(IN_SHAPE)) * 4 + args.batch * 8 if 0 in eng2.local else 0
+        d2h = 4 if (K - 1) in eng2.local else 0
+        e2e = {"value": args.batch * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "timing": "host wall clock incl. pinned H2D + per-step loss D2H"}
+        del eng2, model2
+
+    roof = kernel_roofline(torch, peaks, args.batch) if rank == 0 else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            v, dt, cpu_s = cpu_oracle_steps(args, 3, 1, 32)
+            cpu = {"value": v, "unit": UNIT, "cores": threads_used(), "kind": "port",
+                   "sample": f"oracle/dsp_ref.py float64 DSP step (CPU restatement of the reference), ResNet-{DEPTH} "
+                             f"K={K}, 3 timed steps of a 32-sample sub-batch after 1 warmup ({dt:.1f} s)"}
+        except Exception as exc:  # the baseline must never sink the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc!r}"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": config_dict(args, K, world), "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+                "step_ms_median": statistics.median(step_ms), "loss_finite": bool(loss_ok)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -159,6 +159,8 @@ int dsp_unpack_output(const void* in, float* out_dev, int batch, int c, int h, i
                       int nchw, void* stream);
 const char* dsp_last_error(void);
 int dsp_abi_version(void);
+/* Number of kernels this library has launched in the process (bench evidence). */
+int64_t dsp_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -122,12 +122,12 @@ def conv_bwd(dy, cols, x_shape, w, stride, pad):
     dyf = dy.transpose(0, 2, 3, 1).reshape(-1, co)
     dw = (dyf.T @ cols).reshape(w.shape)
     dcols = (dyf @ w.reshape(co, -1)).reshape(B, dy.shape[2], dy.shape[3], k, k, C)
-    dxp = np.zeros((B, C, H + 2 * pad, W + 2 * pad))
+    dxp = np.zeros((B, H + 2 * pad, W + 2 * pad, C))  # NHWC scatter: contiguous inner dim
     P, Q = dy.shape[2], dy.shape[3]
     for r in range(k):
         for s_ in range(k):
-            dxp[:, :, r:r + stride * P:stride, s_:s_ + stride * Q:stride] += dcols[:, :, :, r, s_, :].transpose(0, 3, 1, 2)
-    dx = dxp[:, :, pad:pad + H, pad:pad + W]
+            dxp[:, r:r + stride * P:stride, s_:s_ + stride * Q:stride, :] += dcols[:, :, :, r, s_, :]
+    dx = dxp[:, pad:pad + H, pad:pad + W, :].transpose(0, 3, 1, 2)
     return dx, dw
 
 

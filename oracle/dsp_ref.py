@@ -544,7 +544,8 @@ def validate_config(p, m, warmup="faithful_zero_updates", overlap_recompute=True
     if warmup not in WARMUP_POLICIES:
         raise ConfigError("warmup", 0, f"warmup must be one of {WARMUP_POLICIES}, got {warmup!r}")
     if p[-1] != 0:
-        raise ConfigError("p_last_zero", K - 1, f"p[{K - 1}] = {p[-1]} must be 0")
+        raise ConfigError("p_last_zero", K - 1,
+                          f"p[{K - 1}] = {p[-1]} must be 0 (the last block sends no activations upward)")
     for k in range(K - 1):
         if p[k] <= 0:
             raise ConfigError("p_positive", k, f"p[{k}] = {p[k]} must be > 0")

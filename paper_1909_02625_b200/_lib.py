@@ -95,6 +95,7 @@ _SIGNATURES = {
     "dsp_unpack_output": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "dsp_last_error": (C.c_char_p, []),
     "dsp_abi_version": (C.c_int, []),
+    "dsp_launch_count": (C.c_int64, []),
 }
 
 _lib = None

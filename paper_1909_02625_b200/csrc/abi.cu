@@ -3,6 +3,7 @@
 #include "abi_internal.h"
 #include "kernels.cuh"
 
+#include <atomic>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -10,6 +11,9 @@
 namespace dsp {
 
 static thread_local char g_last_error[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
@@ -29,6 +33,7 @@ using namespace dsp;
 
 extern "C" const char* dsp_last_error(void) { return g_last_error; }
 extern "C" int dsp_abi_version(void) { return DSP_ABI_VERSION; }
+extern "C" int64_t dsp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int splits, void* stream) {
   if (args == nullptr) return set_error(DSP_E_INVALID, "dsp_igemm: null args");

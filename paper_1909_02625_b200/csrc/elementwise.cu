@@ -614,7 +614,7 @@ __global__ void unpack_output_k(const T* __restrict__ in, float* __restrict__ ou
 cudaError_t bn_finalize(const float* part, int tiles, int Cp, int c_real, int64_t count, const float* gamma,
                         const float* beta, float* stat, cudaStream_t st) {
   bn_finalize_k<<<Cp, 128, 0, st>>>(part, tiles, Cp, c_real, (double)count, gamma, beta, stat);
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* res, const void* y2, const float* stat2,
@@ -624,7 +624,7 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
     const int64_t nvec = M * Cp / V16<T>::N;
     bn_apply_k<T><<<grid_for(nvec), kThreads, 0, st>>>((const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
                                                       nvec, Cp, relu);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -651,14 +651,14 @@ cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const v
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     bn_bwd_reduce_k<T><<<chunks, kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
                                                     rows);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
 cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, int64_t count, const float* gamma,
                             const float* stat, float* dgamma, float* dbeta, float* coef, cudaStream_t st) {
   bn_bwd_finalize_k<<<Cp, 128, 0, st>>>(part, chunks, Cp, c_real, (double)count, gamma, stat, dgamma, dbeta, coef);
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
@@ -670,7 +670,7 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
     bn_bwd_apply_k<T><<<grid_for(nvec), kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, coef,
                                                            (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b,
                                                            (T*)g_out, nvec, Cp);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -679,7 +679,7 @@ cudaError_t act_forward(int dtype, int tanh_kind, const void* x, void* out, int6
     using T = decltype(t);
     const int64_t nvec = n / V16<T>::N;
     act_fwd_k<T><<<grid_for(nvec), kThreads, 0, st>>>(tanh_kind, (const T*)x, (T*)out, nvec);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -688,7 +688,7 @@ cudaError_t act_backward(int dtype, int tanh_kind, const void* x, const void* u,
     using T = decltype(t);
     const int64_t nvec = n / V16<T>::N;
     act_bwd_k<T><<<grid_for(nvec), kThreads, 0, st>>>(tanh_kind, (const T*)x, (const T*)u, (T*)dx, nvec);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -696,7 +696,7 @@ cudaError_t avgpool_forward(int dtype, const void* x, void* out, int B, int HW, 
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     avgpool_fwd_k<T><<<grid_for((int64_t)B * Cp / V16<T>::N), kThreads, 0, st>>>((const T*)x, (T*)out, B, HW, Cp);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -704,7 +704,7 @@ cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, 
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     avgpool_bwd_k<T><<<grid_for((int64_t)B * HW * Cp / V16<T>::N), kThreads, 0, st>>>((const T*)u, (T*)dx, B, HW, Cp);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -714,7 +714,7 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, i
     using T = decltype(t);
     maxpool_fwd_k<T><<<grid_for((int64_t)B * P * Q * Cp), kThreads, 0, st>>>((const T*)x, (T*)out, arg, B, H, W, P, Q,
                                                                             Cp);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -724,7 +724,7 @@ cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void*
     using T = decltype(t);
     maxpool_bwd_k<T><<<grid_for((int64_t)B * H * W * Cp), kThreads, 0, st>>>((const T*)u, arg, (T*)dx, B, H, W, P, Q,
                                                                             Cp);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -733,7 +733,7 @@ cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, c
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     softmax_xent_k<T><<<1, 512, B * sizeof(float), st>>>(logits, ld, B, C, labels, (T*)dlogits, loss);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -742,7 +742,7 @@ cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, i
   const int64_t total = dense_layout ? (int64_t)ci_real * co_real : (int64_t)co_real * RS * ci_real;
   wgrad_reduce_k<<<grid_for(total), kThreads, 0, st>>>(part, splits, Mw, N, RS, Cp, ci_real, co_real, dense_layout,
                                                        grad);
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t pack_weights(int dtype, const float* params, void* packed, const PackEntry* entries_dev, int n_entries,
@@ -752,7 +752,7 @@ cudaError_t pack_weights(int dtype, const float* params, void* packed, const Pac
     using T = decltype(t);
     dim3 grid(grid_for(max_elems, kThreads, 256), n_entries);
     pack_weights_k<T><<<grid, kThreads, 0, st>>>(params, (T*)packed, entries_dev, n_entries);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -769,7 +769,7 @@ cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* 
     if (w) update_f32_k<DSP_RULE_SUM, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
     else update_f32_k<DSP_RULE_SUM, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
   }
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr, double slr,
@@ -783,22 +783,22 @@ cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, doubl
     if (w) update_f64_k<DSP_RULE_SUM, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
     else update_f64_k<DSP_RULE_SUM, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
   }
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t sumsq_f32(int64_t n, const float* v, float* part, cudaStream_t st) {
   sumsq_k<<<update_grid(n), kThreads, 0, st>>>(n, v, part);
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t sum_partials_f32(const float* part, int n, float* out, cudaStream_t st) {
   sum_partials_k<float, float><<<1, kThreads, 0, st>>>(part, n, out);
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t sum_partials_f64(const double* part, int n, double* out, cudaStream_t st) {
   sum_partials_k<double, double><<<1, kThreads, 0, st>>>(part, n, out);
-  return cudaGetLastError();
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t pack_input(const float* x, void* out, int B, int C, int H, int W, int Cp, int dtype, int nchw,
@@ -806,7 +806,7 @@ cudaError_t pack_input(const float* x, void* out, int B, int C, int H, int W, in
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     pack_input_k<T><<<grid_for((int64_t)B * H * W * Cp), kThreads, 0, st>>>(x, (T*)out, B, C, H, W, Cp, nchw);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 
@@ -815,7 +815,7 @@ cudaError_t unpack_output(const void* in, float* out, int B, int C, int H, int W
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     unpack_output_k<T><<<grid_for((int64_t)B * C * H * W), kThreads, 0, st>>>((const T*)in, out, B, C, H, W, Cp, nchw);
-    return cudaGetLastError();
+    return note_launch(), cudaGetLastError();
   });
 }
 

@@ -27,6 +27,7 @@
 //   K-major:  row = M/N index, 16 B = EPC consecutive K elements.
 //   MN-major: row = K index,   16 B = EPC consecutive M/N elements.
 #include "common.cuh"
+#include "kernels.cuh"
 #include "../../include/dsp_b200.h"
 
 #include <stdio.h>
@@ -392,6 +393,7 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   }
   dim3 grid((a.M + IG_BM - 1) / IG_BM, (a.N + BN - 1) / BN, MODE == DSP_IGEMM_WGRAD ? splits : 1);
   igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, smem, st>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -8,6 +8,9 @@
 
 namespace dsp {
 
+// Counts every kernel launch issued by this library (dsp_launch_count()).
+void note_launch();
+
 cudaError_t igemm_launch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st);
 
 // BatchNorm forward: reduce igemm partials [tiles][2][Cp] -> per-channel

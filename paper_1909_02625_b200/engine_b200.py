@@ -68,7 +68,11 @@ class B200Runtime:
     def in_elems(self, k: int) -> int:
         return act_elems(self.B, self.model.blocks[k].in_shape)
 
-    def make_input(self, x: np.ndarray, labels: np.ndarray):
+    def make_input(self, x, labels):
+        from .data import DeviceBatch
+
+        if isinstance(x, DeviceBatch):  # already packed in HBM
+            return x.act, x.labels
         if x.shape[0] != self.B:
             raise ValueError(f"batch of {x.shape[0]} rows, engine sized for {self.B}")
         lab = np.asarray(labels, dtype=np.int64)
@@ -161,6 +165,9 @@ class B200Runtime:
 
     def synchronize(self) -> None:
         self.stream.synchronize()
+
+    def read_scalar(self, h) -> float:
+        return float(self._chunks[h[0]][h[1]].item())
 
     def read_scalars(self, pairs):
         self.stream.synchronize()

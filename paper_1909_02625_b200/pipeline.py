@@ -261,7 +261,8 @@ class TrainEngine:
         self._data = data_stream
         self._first_batch = next(data_stream)  # peeked to size the warmup packets (pipeline.py:479)
         self._pending_first = True
-        self.batch_size = int(np.asarray(self._first_batch[0]).shape[0])
+        x0 = self._first_batch[0]
+        self.batch_size = int(x0.shape[0] if hasattr(x0, "shape") else np.asarray(x0).shape[0])
 
         K = config.k
         self._transport = _transport
@@ -338,7 +339,7 @@ class TrainEngine:
 
         if k == 0:
             x, labels = self._next_batch()
-            act, lab = rt.make_input(np.asarray(x), np.asarray(labels))
+            act, lab = rt.make_input(x, labels)
             fresh = ActivationPacket(n, act, lab)
         else:
             fresh = self.out_queues[k - 1].get()
@@ -441,6 +442,16 @@ class TrainEngine:
 
     def synchronize(self) -> None:
         self.rt.synchronize()
+
+    def last_loss(self) -> float | None:
+        """Loss of the most recent last-block step on this rank (a 4-byte device->host read)."""
+        K = self.config.k
+        if (K - 1) not in self.local or not self._block_logs[K - 1]:
+            return None
+        for rec, lh, _ in reversed(self._pending):
+            if rec.block == K - 1:
+                return self.rt.read_scalar(lh)
+        return self._block_logs[K - 1][-1].loss
 
     def _materialize(self) -> None:
         if not self._pending:
