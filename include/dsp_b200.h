@@ -76,10 +76,23 @@ typedef struct {
   int32_t out_f32;         /* FPROP/DGRAD: store fp32 instead of the storage dtype */
   const void* residual;    /* optional [M][ldd] added in the epilogue */
   const float* bias;       /* optional [N] added in the epilogue */
-  float* stats;            /* optional BatchNorm partials [gridDim.x][2][N] (sum, sum of squares) */
+  float* stats;            /* optional BatchNorm partials, one row per CTA: [DSP_IGEMM_MAX_CTAS][2][N]
+                              (sum, sum of squares of the stored values) */
   int32_t kb_per_split;    /* WGRAD split-K: K blocks per split */
   int32_t n_valid;         /* FPROP/DGRAD: columns >= n_valid are stored as 0 (0 = all N valid) */
+  /* FPROP fused BatchNorm finalize (optional, needs stats): the last CTA to
+   * finish reduces the per-CTA partials in fixed order and writes
+   * stat_out[4][N] = mean, invstd, gamma*invstd, beta - mean*gamma*invstd
+   * (columns >= n_valid get zeros).  sem: a device int that is 0 on entry
+   * (the kernel leaves it 0 again). */
+  float* stat_out;
+  const float* gamma;
+  const float* beta;
+  int32_t* sem;
+  int64_t* trace;          /* optional profiling: clock64() stamps of CTA 0's pipeline events (>= 192 slots) */
 } dsp_igemm_args_t;
+
+#define DSP_IGEMM_MAX_CTAS 296
 
 /* Implicit-GEMM conv/dense on tcgen05 tensor cores (igemm.cu).  `splits` is the
  * WGRAD split-K factor (ignored otherwise). */

@@ -56,7 +56,12 @@ class IgemmArgs(C.Structure):
         ("residual", C.c_void_p), ("bias", C.c_void_p), ("stats", C.c_void_p),
         ("kb_per_split", C.c_int32),
         ("n_valid", C.c_int32),
+        ("stat_out", C.c_void_p), ("gamma", C.c_void_p), ("beta", C.c_void_p), ("sem", C.c_void_p),
+        ("trace", C.c_void_p),
     ]
+
+
+IGEMM_MAX_CTAS = 296
 
 
 class LayerDesc(C.Structure):

@@ -64,7 +64,7 @@ struct dsp_block {
   size_t ws_bytes = 0;
   size_t S[4] = {0, 0, 0, 0};
   size_t G[2] = {0, 0};
-  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0;
+  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0, sem = 0;
   size_t packed = 0, ptable = 0;
   std::vector<dsp::PackEntry> packs;
   int pack_max = 0;
@@ -138,10 +138,12 @@ int conv_fprop(dsp_block* b, const ConvP& c, const void* x, cudaStream_t st) {
   a.ldd = c.g.K;
   a.stats = at<float>(b, b->fpart);
   a.n_valid = c.co_real;
+  // BatchNorm statistics: per-CTA partials in the epilogue, finalized by the last CTA
+  a.stat_out = at<float>(b, c.stat);
+  a.gamma = b->params + c.gamma_off;
+  a.beta = b->params + c.beta_off;
+  a.sem = at<int32_t>(b, b->sem);
   DSP_CUDA(igemm_launch(DSP_IGEMM_FPROP, b->dtype, a, 1, st));
-  const int tiles = (a.M + 127) / 128;
-  DSP_CUDA(bn_finalize(at<float>(b, b->fpart), tiles, c.g.K, c.co_real, c.M(), b->params + c.gamma_off,
-                       b->params + c.beta_off, at<float>(b, c.stat), st));
   return DSP_OK;
 }
 
@@ -503,7 +505,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       c.stat = pl.take((size_t)4 * c.g.K * 4);
       c.coef = pl.take((size_t)3 * c.g.K * 4);
       max_act = std::max(max_act, std::max(c.M() * c.g.K, c.Min() * c.g.C));
-      max_fpart = std::max<int64_t>(max_fpart, (c.M() + 127) / 128 * 2 * c.g.K);
+      max_fpart = std::max<int64_t>(max_fpart, (int64_t)DSP_IGEMM_MAX_CTAS * 2 * c.g.K);
       max_bpart = std::max<int64_t>(max_bpart, (int64_t)bn_bwd_chunks(c.M(), c.g.K) * 2 * c.g.K);
       int kb = 1;
       const int sp = wgrad_splits(c, &kb, dtype);
@@ -528,6 +530,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
   for (int s = 0; s < 4; ++s) b->S[s] = pl.take((size_t)max_act * b->esz);
   for (int s = 0; s < 2; ++s) b->G[s] = pl.take((size_t)max_act * b->esz);
   b->fpart = pl.take((size_t)std::max<int64_t>(max_fpart, 1) * 4);
+  b->sem = pl.take(256);  // zeroed at bind; fused-finalize kernels leave it zero
   b->bpart = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
   b->bpart2 = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
   b->wpart = pl.take((size_t)std::max<int64_t>(max_wpart, 1) * 4);

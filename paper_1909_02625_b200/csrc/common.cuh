@@ -31,31 +31,40 @@ __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Blocking phase wait. The suspend-time hint lets the hardware park the warp
+// until the phase flips instead of re-issuing try_wait, which would otherwise
+// compete with the producers' cp.async for the MIO pipe.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t"
       ".reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t"
       "}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 
 // ---------------------------------------------------------------- cp.async
 // 16-byte global->shared copy; src_bytes == 0 zero-fills the destination
 // (used for conv padding, ragged tiles and stride-2 dgrad holes).
+// .ca: allocate in L1, so the k*k taps of an implicit-GEMM gather re-hit L1.
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Arrive (count 1, no pending-count increment) on an mbarrier once every cp.async
+// previously issued by this thread has landed in shared memory.
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -153,6 +162,35 @@ __host__ __device__ __forceinline__ uint32_t umma_idesc(uint32_t fmt, uint32_t a
   d |= ((M >> 4) & 31u) << 24;
   return d;
 }
+
+// ---------------------------------------------------------------- fast division
+// n / d for 0 <= n < 2^31 as umulhi(n, mul) >> shr (Granlund-Montgomery, as
+// CUTLASS FastDivmod): the implicit-GEMM gathers decode pixel / tap indices per
+// 16-byte chunk, and runtime 32-bit division would dominate the producer warps.
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __device__ __forceinline__ void init(uint32_t div) {
+    d = div;
+    if (div <= 1) {
+      mul = 0;
+      shr = 0;
+    } else {
+      uint32_t l = 0;  // ceil(log2(div))
+      while ((1u << l) < div) ++l;
+      const uint32_t p = 31 + l;  // 2^p / div < 2^32 since div > 2^(l-1)
+      mul = (uint32_t)((((uint64_t)1 << p) + div - 1) / div);
+      shr = p - 32;
+    }
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return d <= 1 ? n : (int)(__umulhi((uint32_t)n, mul) >> shr);
+  }
+  __device__ __forceinline__ int divmod(int n, int& rem) const {
+    const int q = div(n);
+    rem = n - q * (int)d;
+    return q;
+  }
+};
 
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ float warp_sum(float v) {

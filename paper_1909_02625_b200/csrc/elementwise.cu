@@ -444,23 +444,26 @@ __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, 
 // ------------------------------------------------------------------ split-K reduce / packing
 __global__ void wgrad_reduce_k(const float* __restrict__ part, int splits, int Mw, int N, int RS, int Cp, int ci_real,
                                int co_real, int dense_layout, float* __restrict__ grad) {
-  const int64_t total = dense_layout ? (int64_t)ci_real * co_real : (int64_t)co_real * RS * ci_real;
+  // threads walk the partials in their natural (m, n) order so every split is
+  // read coalesced; the (tiny) weight-gradient writes are scattered instead
+  const int64_t total = (int64_t)Mw * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int m, n;
+    const int n = (int)(idx % N);
+    const int m = (int)(idx / N);
+    if (n >= co_real) continue;
+    int64_t dst;
     if (dense_layout) {
-      n = (int)(idx % co_real);
-      m = (int)(idx / co_real);
+      if (m >= ci_real) continue;
+      dst = (int64_t)m * co_real + n;
     } else {
-      const int ci = (int)(idx % ci_real);
-      const int64_t t = idx / ci_real;
-      const int tap = (int)(t % RS);
-      n = (int)(t / RS);
-      m = tap * Cp + ci;
+      const int ci = m % Cp, tap = m / Cp;
+      if (ci >= ci_real || tap >= RS) continue;
+      dst = ((int64_t)n * RS + tap) * ci_real + ci;
     }
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += part[((size_t)z * Mw + m) * N + n];
-    grad[idx] = s;
+    grad[dst] = s;
   }
 }
 
@@ -739,7 +742,7 @@ cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, c
 
 cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
                          int dense_layout, float* grad, cudaStream_t st) {
-  const int64_t total = dense_layout ? (int64_t)ci_real * co_real : (int64_t)co_real * RS * ci_real;
+  const int64_t total = (int64_t)Mw * N;
   wgrad_reduce_k<<<grid_for(total), kThreads, 0, st>>>(part, splits, Mw, N, RS, Cp, ci_real, co_real, dense_layout,
                                                        grad);
   return note_launch(), cudaGetLastError();

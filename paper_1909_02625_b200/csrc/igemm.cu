@@ -11,32 +11,36 @@
 // 147-151; tensor.py:40-56) generalised from dense to conv layers (a dense
 // layer is the 1x1 conv on a 1x1 image).
 //
-// Structure (per CTA, 128 threads, one 128 x BN output tile):
-//   * all 4 warps gather the A/B operand tiles with 16-byte cp.async (zero-fill
-//     implements padding, ragged edges and stride-2 dgrad holes) straight into
-//     the UMMA canonical SWIZZLE_NONE layout, STAGES-deep ring;
-//   * one thread issues tcgen05.mma (kind::f16 for bf16 / kind::tf32 for fp32)
-//     with the accumulator in TMEM, and tcgen05.commit releases each ring slot;
-//   * the epilogue reads TMEM with tcgen05.ld (32 lanes per warp) and fuses
-//     bias / residual add / dtype conversion / BatchNorm partial statistics
-//     (FPROP, DGRAD) or writes split-K fp32 partials (WGRAD).
+// Persistent, warp-specialised CTA (288 threads), one or two CTAs per SM:
+//   warps 0-3  producers: gather A/B operand tiles with 16-byte cp.async
+//              (zero-fill = conv padding, ragged edges, stride-2 dgrad holes)
+//              straight into the UMMA canonical SWIZZLE_NONE layout, through a
+//              STAGES-deep smem ring that runs continuously across output tiles;
+//   warp 4     allocates TMEM; lane 0 issues tcgen05.mma (kind::f16 / kind::tf32)
+//              into a double-buffered TMEM accumulator and tcgen05.commit's the
+//              ring slots / accumulators back;
+//   warps 5-8  epilogue: tcgen05.ld 32 lanes each, fuse bias / residual add /
+//              dtype conversion / BatchNorm statistics (FPROP, with the per-channel
+//              finalize done by the last CTA to finish) or write split-K fp32
+//              partials (WGRAD), while the MMA works on the next tile.
 //
 // Shared-memory operand layout (both K-major and MN-major, 16-byte "chunks"):
 //   core matrix = 128 contiguous bytes (8 rows x 16 B), core (mn_grp, k_grp)
-//   at k_grp * LBO + mn_grp * 128, LBO = E * 16 (E = rows of the tile).
+//   at k_grp * LBO + mn_grp * 128.
 //   K-major:  row = M/N index, 16 B = EPC consecutive K elements.
 //   MN-major: row = K index,   16 B = EPC consecutive M/N elements.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "../../include/dsp_b200.h"
 
-#include <stdio.h>
+#include <algorithm>
 
 namespace dsp {
 
 constexpr int IG_BM = 128;
-constexpr int IG_STAGES = 4;
-constexpr int IG_THREADS = 128;
+constexpr int IG_THREADS = 288;
+constexpr int IG_MMA_WARP = 4;
+constexpr int IG_EPI_WARP0 = 5;
 
 template <typename T>
 struct MmaTraits;
@@ -53,346 +57,547 @@ struct MmaTraits<float> {
   __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t i, uint32_t acc) { umma_tf32(d, a, b, i, acc); }
 };
 
+template <int BN>
+struct IgCfg {
+  static constexpr int STAGES = BN <= 32 ? 5 : (BN <= 128 ? 4 : 3);
+  static constexpr int SMEM = STAGES * (IG_BM * 128 + BN * 128);
+  static constexpr int NACC = BN <= 128 ? 4 : 2;  // TMEM accumulators: MMA runs NACC-1 tiles ahead
+  static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
+  static constexpr int CTAS_PER_SM = (SMEM <= 100 * 1024 && TMEM_COLS <= 256) ? 2 : 1;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Column sums of a 32-row x 16-column register tile (one row per lane) with 16
+// shuffles: halve the column set at each butterfly step. Lane l ends holding the
+// full sum of column (l >> 1) & 15.
+__device__ __forceinline__ float colsum16(const float (&v)[16], int lane) {
+  float w8[8], w4[4], w2[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    const float send = up ? v[i] : v[i + 8];
+    const float keep = up ? v[i + 8] : v[i];
+    w8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    const float send = up ? w8[i] : w8[i + 4];
+    const float keep = up ? w8[i + 4] : w8[i];
+    w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    const float send = up ? w4[i] : w4[i + 2];
+    const float keep = up ? w4[i + 2] : w4[i];
+    w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const bool up = lane & 2;
+  float w1 = (up ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, up ? w2[0] : w2[1], 2);
+  w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
+  return w1;
+}
+
 template <typename T, int MODE, int BN>
-__global__ void __launch_bounds__(IG_THREADS) igemm_kernel(const dsp_igemm_args_t a) {
-  constexpr int EPC = 16 / (int)sizeof(T);   // elements per 16-byte chunk
-  constexpr int KS = 8 * EPC;                // K extent of one ring stage (128 B per row)
+__global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kernel(const dsp_igemm_args_t a) {
+  using Cfg = IgCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr int NACC = Cfg::NACC;
+  constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+  constexpr int KS = 8 * EPC;               // K extent of one ring stage (128 B per row)
   constexpr int A_BYTES = IG_BM * 128;
   constexpr int B_BYTES = BN * 128;
-  constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   constexpr bool A_MN = (MODE == DSP_IGEMM_WGRAD);
   constexpr bool B_MN = (MODE != DSP_IGEMM_FPROP);
+  constexpr int AG = IG_BM / EPC;  // MN groups in the A tile (MN-major)
+  constexpr int BG = BN / EPC;     // MN groups in the B tile (MN-major)
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mma_bar[IG_STAGES];
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[NACC], tempty_bar[NACC];
   __shared__ uint32_t tmem_base_s;
+  __shared__ int last_cta_s;
   __shared__ float red[4][BN][2];
+  __shared__ double fin[256][2];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
   const dsp_conv_geom_t g = a.geom;
   const int M = a.M, N = a.N, Kd = a.Kd;
-  const int m0 = blockIdx.x * IG_BM;
-  const int n0 = blockIdx.y * BN;
-
   const T* __restrict__ Asrc = reinterpret_cast<const T*>(a.A);
   const T* __restrict__ Bsrc = reinterpret_cast<const T*>(a.B);
 
   const int nkb_total = (Kd + KS - 1) / KS;
-  int kb_begin = 0, kb_end = nkb_total;
-  if (MODE == DSP_IGEMM_WGRAD) {
-    kb_begin = blockIdx.z * a.kb_per_split;
-    kb_end = min(nkb_total, kb_begin + a.kb_per_split);
-  }
-  const int nk = kb_end - kb_begin;
+  const int mt = (M + IG_BM - 1) / IG_BM;
+  const int nt = (N + BN - 1) / BN;
+  const int kbps = MODE == DSP_IGEMM_WGRAD ? a.kb_per_split : nkb_total;
+  const int ns = MODE == DSP_IGEMM_WGRAD ? (nkb_total + kbps - 1) / kbps : 1;
+  const int units = mt * nt * ns;
+  const bool want_stats = (MODE == DSP_IGEMM_FPROP) && a.stats != nullptr;
+
+  // Work assignment. FPROP/DGRAD: CTA c owns n-tile c % nt (so per-column BN
+  // statistics can accumulate in registers) and m-tiles c/nt, c/nt + G/nt, ...
+  // (the launcher makes gridDim.x a multiple of nt). WGRAD: round-robin units.
+  auto get_unit = [&](int j, int& m0, int& n0, int& z, int& kb0, int& kb1) -> bool {
+    if (MODE == DSP_IGEMM_WGRAD) {
+      const int u = blockIdx.x + j * gridDim.x;
+      if (u >= units) return false;
+      m0 = (u % mt) * IG_BM;
+      n0 = ((u / mt) % nt) * BN;
+      z = u / (mt * nt);
+      kb0 = z * kbps;
+      kb1 = min(nkb_total, kb0 + kbps);
+      return true;
+    }
+    const int mtile = blockIdx.x / nt + j * (gridDim.x / nt);
+    if (mtile >= mt) return false;
+    m0 = mtile * IG_BM;
+    n0 = (blockIdx.x % nt) * BN;
+    z = 0;
+    kb0 = 0;
+    kb1 = nkb_total;
+    return true;
+  };
+  (void)units;
 
   if (tid == 0) {
-    for (int s = 0; s < IG_STAGES; ++s) mbar_init(&mma_bar[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 128);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < NACC; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(&tmem_base_s, TMEM_COLS);
+  if (warp == IG_MMA_WARP) tmem_alloc(&tmem_base_s, Cfg::TMEM_COLS);
+  if (want_stats && warp >= IG_EPI_WARP0) {
+    for (int c = lane; c < BN; c += 32) red[warp & 3][c][0] = red[warp & 3][c][1] = 0.f;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_d = tmem_base_s;
-
+  int64_t* const trace = (a.trace != nullptr && blockIdx.x == 0) ? a.trace : nullptr;
+#define IG_TRACE(slot, cond)                                   \
+  do {                                                          \
+    if (trace != nullptr && (cond) && (slot) < 192) trace[(slot)] = clock64(); \
+  } while (0)
+  IG_TRACE(176, tid == 0);
   const uint32_t sA0 = smem_u32(smem);
-  const uint32_t sB0 = sA0 + IG_STAGES * A_BYTES;
+  const uint32_t sB0 = sA0 + STAGES * A_BYTES;
 
-  // ---------------- per-tile precompute for the A gather ----------------
-  // K-major A (FPROP / DGRAD): thread owns chunk column j and rows (tid>>3)+16*i.
-  const int aj = tid & 7;
-  int a_h[8], a_w[8];
-  long long a_img[8];
-  // MN-major A (WGRAD): thread owns MN group ag and k-rows.
-  constexpr int AG = IG_BM / EPC;  // MN groups in the A tile
-  const int ag = tid % AG;
-  int wg_r = 0, wg_s = 0, wg_c = 0;
-  bool wg_ok = false;
-  if (MODE == DSP_IGEMM_FPROP || MODE == DSP_IGEMM_DGRAD) {
-    const int PQ = (MODE == DSP_IGEMM_FPROP) ? g.P * g.Q : g.H * g.W;
-    const int QQ = (MODE == DSP_IGEMM_FPROP) ? g.Q : g.W;
+  if (warp < 4) {
+    // =============================== producers ===============================
+    const int aj = tid & 7;
+    const int ag = tid % AG;
+    // every runtime divisor of the gathers as a multiply-shift (FastDiv)
+    FastDiv fd_pix, fd_row, fd_ch, fd_s, fd_k;
+    fd_pix.init(MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q);
+    fd_row.init(MODE == DSP_IGEMM_DGRAD ? g.W : g.Q);
+    fd_ch.init(MODE == DSP_IGEMM_DGRAD ? g.K : g.C);
+    fd_s.init(g.S);
+    fd_k.init(g.K);
+    const int sh = g.stride == 2 ? 1 : 0;  // stride is 1 or 2
+    const int img_stride = MODE == DSP_IGEMM_DGRAD ? g.P * g.Q * g.K : g.H * g.W * g.C;
+    int gcount = 0;
+    int m0, n0, z, kb0, kb1;
+    for (int j = 0; get_unit(j, m0, n0, z, kb0, kb1); ++j) {
+      // per-tile A-row precompute
+      int a_h[8], a_w[8], a_img[8];
+      int wg_r = 0, wg_s = 0, wg_c = 0;
+      bool wg_ok = false;
+      if (MODE != DSP_IGEMM_WGRAD) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = m0 + (tid >> 3) + 16 * i;
-      if (m < M) {
-        const int img = m / PQ;
-        const int rem = m - img * PQ;
-        const int y = rem / QQ;
-        const int x = rem - y * QQ;
-        if (MODE == DSP_IGEMM_FPROP) {
-          a_h[i] = y * g.stride - g.pad;
-          a_w[i] = x * g.stride - g.pad;
-          a_img[i] = (long long)img * g.H * g.W * g.C;
-        } else {
-          a_h[i] = y + g.pad;
-          a_w[i] = x + g.pad;
-          a_img[i] = (long long)img * g.P * g.Q * g.K;
-        }
-      } else {
-        a_h[i] = -(1 << 28);  // forces the bounds check to fail
-        a_w[i] = -(1 << 28);
-        a_img[i] = 0;
-      }
-    }
-  } else {
-    const int m = m0 + ag * EPC;
-    if (m < M) {
-      const int tap = m / g.C;
-      wg_c = m - tap * g.C;
-      wg_r = tap / g.S;
-      wg_s = tap - wg_r * g.S;
-      wg_ok = true;
-    }
-  }
-
-  auto load_stage = [&](int kb, uint32_t sA, uint32_t sB) {
-    // ---------------- A operand ----------------
-    if (MODE == DSP_IGEMM_FPROP || MODE == DSP_IGEMM_DGRAD) {
-      const int k0 = kb * KS + aj * EPC;
-      const bool kok = k0 < Kd;
-      const int cdim = (MODE == DSP_IGEMM_FPROP) ? g.C : g.K;
-      const int tap = kok ? k0 / cdim : 0;
-      const int c0 = k0 - tap * cdim;
-      const int r = tap / g.S;
-      const int s = tap - r * g.S;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int row = (tid >> 3) + 16 * i;
-        const T* src = Asrc;
-        bool ok = kok;
-        if (MODE == DSP_IGEMM_FPROP) {
-          const int ih = a_h[i] + r, iw = a_w[i] + s;
-          ok = ok && (unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W;
-          if (ok) src = Asrc + a_img[i] + ((long long)ih * g.W + iw) * g.C + c0;
-        } else {
-          int hh = a_h[i] - r, ww = a_w[i] - s;
-          if (g.stride != 1) {
-            ok = ok && hh >= 0 && ww >= 0 && (hh % g.stride) == 0 && (ww % g.stride) == 0;
-            hh /= g.stride;
-            ww /= g.stride;
-          }
-          ok = ok && (unsigned)hh < (unsigned)g.P && (unsigned)ww < (unsigned)g.Q;
-          if (ok) src = Asrc + a_img[i] + ((long long)hh * g.Q + ww) * g.K + c0;
-        }
-        cp_async_16(sA + aj * (IG_BM * 16) + row * 16, src, ok ? 16u : 0u);
-      }
-    } else {
-      // WGRAD: A[m=(r,s,ci)][k=pixel] from X, MN-major
-      const int PQ = g.P * g.Q;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int kr = tid / AG + (IG_THREADS / AG) * i;
-        const int p = kb * KS + kr;
-        const T* src = Asrc;
-        bool ok = wg_ok && p < Kd;
-        if (ok) {
-          const int img = p / PQ;
-          const int rem = p - img * PQ;
-          const int oh = rem / g.Q;
-          const int ow = rem - oh * g.Q;
-          const int ih = oh * g.stride - g.pad + wg_r;
-          const int iw = ow * g.stride - g.pad + wg_s;
-          ok = (unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W;
-          if (ok) src = Asrc + (((long long)img * g.H + ih) * g.W + iw) * g.C + wg_c;
-        }
-        cp_async_16(sA + (kr >> 3) * (AG * 128) + ag * 128 + (kr & 7) * 16, src, ok ? 16u : 0u);
-      }
-    }
-    // ---------------- B operand ----------------
-    constexpr int BCH = 8 * BN;  // chunks per stage
-    if (MODE == DSP_IGEMM_FPROP) {
-      // K-major weights Wb[n][Kd]
-#pragma unroll
-      for (int c = tid; c < BCH; c += IG_THREADS) {
-        const int n = c >> 3, j = c & 7;
-        const int k0 = kb * KS + j * EPC;
-        const bool ok = (n0 + n) < N && k0 < Kd;
-        const T* src = ok ? Bsrc + (long long)(n0 + n) * Kd + k0 : Bsrc;
-        cp_async_16(sB + j * (BN * 16) + n * 16, src, ok ? 16u : 0u);
-      }
-    } else {
-      constexpr int BG = BN / EPC;  // MN groups in the B tile
-#pragma unroll
-      for (int c = tid; c < BCH; c += IG_THREADS) {
-        const int gg = c % BG, kr = c / BG;
-        const int k = kb * KS + kr;
-        const int n = n0 + gg * EPC;
-        bool ok = n < N && k < Kd;
-        const T* src = Bsrc;
-        if (ok) {
-          if (MODE == DSP_IGEMM_DGRAD) {
-            // B[n=ci][k=(r,s,co)] = Wb[co][r][s][ci]
-            const int tap = k / g.K;
-            const int co = k - tap * g.K;
-            src = Bsrc + ((long long)co * g.R * g.S + tap) * g.C + n;
+        for (int i = 0; i < 8; ++i) {
+          const int m = m0 + (tid >> 3) + 16 * i;
+          if (m < M) {
+            int rem, x;
+            const int img = fd_pix.divmod(m, rem);
+            const int y = fd_row.divmod(rem, x);
+            if (MODE == DSP_IGEMM_FPROP) {
+              a_h[i] = (y << sh) - g.pad;
+              a_w[i] = (x << sh) - g.pad;
+            } else {
+              a_h[i] = y + g.pad;
+              a_w[i] = x + g.pad;
+            }
+            a_img[i] = img * img_stride;
           } else {
-            // WGRAD: B[n=co][k=pixel] = dY[pixel][co]
-            src = Bsrc + (long long)k * g.K + n;
+            a_h[i] = -(1 << 28);
+            a_w[i] = -(1 << 28);
+            a_img[i] = 0;
           }
         }
-        cp_async_16(sB + (kr >> 3) * (BG * 128) + gg * 128 + (kr & 7) * 16, src, ok ? 16u : 0u);
-      }
-    }
-  };
-
-  const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, A_MN ? 1u : 0u, B_MN ? 1u : 0u, IG_BM, BN);
-
-  // ---------------- main pipelined K loop ----------------
-  for (int it = 0; it < nk + IG_STAGES - 1; ++it) {
-    if (it < nk) {
-      const int s = it % IG_STAGES;
-      if (it >= IG_STAGES) mbar_wait(&mma_bar[s], ((it / IG_STAGES) - 1) & 1);
-      load_stage(kb_begin + it, sA0 + s * A_BYTES, sB0 + s * B_BYTES);
-    }
-    cp_async_commit();
-    const int kc = it - (IG_STAGES - 1);
-    if (kc >= 0) {
-      cp_async_wait<IG_STAGES - 1>();
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        tc_fence_after();
-        const int s = kc % IG_STAGES;
-        const uint32_t sa = sA0 + s * A_BYTES;
-        const uint32_t sb = sB0 + s * B_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < KS / MmaTraits<T>::MMA_K; ++kk) {
-          const uint64_t ad = umma_sdesc(sa + kk * 32 * IG_BM, A_MN ? (IG_BM / EPC) * 128 : IG_BM * 16, 128);
-          const uint64_t bd = umma_sdesc(sb + kk * 32 * BN, B_MN ? (BN / EPC) * 128 : BN * 16, 128);
-          MmaTraits<T>::mma(tmem_d, ad, bd, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+      } else {
+        const int m = m0 + ag * EPC;
+        if (m < M) {
+          int c, ss;
+          const int tap = fd_ch.divmod(m, c);
+          wg_c = c;
+          wg_r = fd_s.divmod(tap, ss);
+          wg_s = ss;
+          wg_ok = true;
         }
-        umma_commit(&mma_bar[s]);
       }
-    }
-  }
-  if (nk > 0) {
-    const int last = nk - 1;
-    mbar_wait(&mma_bar[last % IG_STAGES], (last / IG_STAGES) & 1);
-  }
-  tc_fence_after();
-
-  // ---------------- epilogue ----------------
-  const int row = warp * 32 + lane;
-  const int m = m0 + row;
-  const bool mok = m < M;
-  const uint32_t tl = tmem_d + ((uint32_t)(warp * 32) << 16);
-  const bool want_stats = (MODE != DSP_IGEMM_WGRAD) && a.stats != nullptr;
-
-#pragma unroll 1
-  for (int cc = 0; cc < BN / 16; ++cc) {
-    float v[16];
-    if (nk > 0) {
-      tmem_ld16(tl + cc * 16, v);
-    } else {
+      for (int kb = kb0; kb < kb1; ++kb, ++gcount) {
+        const int s = gcount % STAGES;
+        IG_TRACE(2 * gcount, tid == 0 && gcount < 32);
+        if (gcount >= STAGES) mbar_wait(&empty_bar[s], ((gcount / STAGES) - 1) & 1);
+        const uint32_t sA = sA0 + s * A_BYTES;
+        const uint32_t sB = sB0 + s * B_BYTES;
+        if (a.out_f32 & 2) {  // ablation: skip operand loads
+          cp_async_arrive_noinc(&full_bar[s]);
+          continue;
+        }
+        // ---------------- A operand ----------------
+        if (MODE != DSP_IGEMM_WGRAD) {
+          const int k0 = kb * KS + aj * EPC;
+          const bool kok = k0 < Kd;
+          int c0 = 0, s2 = 0, r = 0;
+          if (kok) {
+            const int tap = fd_ch.divmod(k0, c0);
+            r = fd_s.divmod(tap, s2);
+          }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
-    }
-    const int nb = n0 + cc * 16;
-    if (MODE == DSP_IGEMM_WGRAD) {
-      float* out = reinterpret_cast<float*>(a.D) + (size_t)blockIdx.z * M * N + (size_t)m * N;
-      if (mok) {
-        if (nb + 16 <= N && (N & 3) == 0) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(out + nb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int i = 0; i < 8; ++i) {
+            const int row = (tid >> 3) + 16 * i;
+            int off = 0;
+            bool ok = kok;
+            if (MODE == DSP_IGEMM_FPROP) {
+              const int ih = a_h[i] + r, iw = a_w[i] + s2;
+              ok = ok && (unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W;
+              off = a_img[i] + (ih * g.W + iw) * g.C + c0;
+            } else {
+              int hh = a_h[i] - r, ww = a_w[i] - s2;
+              if (sh) {
+                ok = ok && hh >= 0 && ww >= 0 && ((hh | ww) & 1) == 0;
+                hh >>= 1;
+                ww >>= 1;
+              }
+              ok = ok && (unsigned)hh < (unsigned)g.P && (unsigned)ww < (unsigned)g.Q;
+              off = a_img[i] + (hh * g.Q + ww) * g.K + c0;
+            }
+            cp_async_16(sA + aj * (IG_BM * 16) + row * 16, ok ? Asrc + off : Asrc, ok ? 16u : 0u);
+          }
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (nb + i < N) out[nb + i] = v[i];
+          for (int i = 0; i < 8; ++i) {
+            const int kr = tid / AG + (128 / AG) * i;
+            const int p = kb * KS + kr;
+            int off = 0;
+            bool ok = wg_ok && p < Kd;
+            if (ok) {
+              int rem, ow;
+              const int img = fd_pix.divmod(p, rem);
+              const int oh = fd_row.divmod(rem, ow);
+              const int ih = (oh << sh) - g.pad + wg_r;
+              const int iw = (ow << sh) - g.pad + wg_s;
+              ok = (unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W;
+              off = ((img * g.H + ih) * g.W + iw) * g.C + wg_c;
+            }
+            cp_async_16(sA + (kr >> 3) * (AG * 128) + ag * 128 + (kr & 7) * 16, ok ? Asrc + off : Asrc,
+                        ok ? 16u : 0u);
+          }
         }
-      }
-    } else {
-      const int nvalid = a.n_valid > 0 ? a.n_valid : N;
-      if (a.bias != nullptr) {
+        // ---------------- B operand ----------------
+        constexpr int BCH = 8 * BN;
+        if (MODE == DSP_IGEMM_FPROP) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (nb + i < nvalid) v[i] += a.bias[nb + i];
-      }
-      if (a.residual != nullptr && mok) {
-        const T* res = reinterpret_cast<const T*>(a.residual) + (size_t)m * a.ldd;
+          for (int c = tid; c < BCH; c += 128) {
+            const int n = c >> 3, jj = c & 7;
+            const int k0 = kb * KS + jj * EPC;
+            const bool ok = (n0 + n) < N && k0 < Kd;
+            cp_async_16(sB + jj * (BN * 16) + n * 16, ok ? Bsrc + (n0 + n) * Kd + k0 : Bsrc, ok ? 16u : 0u);
+          }
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (nb + i < N) v[i] += to_f<T>(res[nb + i]);
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (nb + i >= nvalid) v[i] = 0.f;
-      if (a.out_f32) {
-        float* out = reinterpret_cast<float*>(a.D) + (size_t)m * a.ldd;
-        if (mok) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (nb + i < N) out[nb + i] = v[i];
+          for (int c = tid; c < BCH; c += 128) {
+            const int gg = c % BG, kr = c / BG;
+            const int k = kb * KS + kr;
+            const int n = n0 + gg * EPC;
+            const bool ok = n < N && k < Kd;
+            int off = 0;
+            if (MODE == DSP_IGEMM_DGRAD) {
+              int co;
+              const int tap = fd_k.divmod(k, co);
+              off = (co * g.R * g.S + tap) * g.C + n;
+            } else {
+              off = k * g.K + n;
+            }
+            cp_async_16(sB + (kr >> 3) * (BG * 128) + gg * 128 + (kr & 7) * 16, ok ? Bsrc + off : Bsrc,
+                        ok ? 16u : 0u);
+          }
         }
-      } else {
-        T* out = reinterpret_cast<T*>(a.D) + (size_t)m * a.ldd;
-        // round to the storage type first so BN statistics describe the stored tensor
+        // arrive on full[s] when this thread's copies land; never block the producer
+        cp_async_arrive_noinc(&full_bar[s]);
+        IG_TRACE(2 * gcount + 1, tid == 0 && gcount < 32);
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == IG_MMA_WARP) {
+    // =============================== MMA issuer ===============================
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, A_MN ? 1u : 0u, B_MN ? 1u : 0u, IG_BM, BN);
+      const uint32_t lbo_a = A_MN ? (IG_BM / EPC) * 128 : IG_BM * 16;
+      const uint32_t lbo_b = B_MN ? (BN / EPC) * 128 : BN * 16;
+      int gcount = 0, i = 0;
+      int m0, n0, z, kb0, kb1;
+      for (; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
+        const int acc = i % NACC;
+        if (i >= NACC) mbar_wait(&tempty_bar[acc], ((i / NACC) - 1) & 1);
+        IG_TRACE(128 + i, i < 16);
+        tc_fence_after();
+        const uint32_t td = tmem_d + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++gcount) {
+          const int s = gcount % STAGES;
+          mbar_wait(&full_bar[s], (gcount / STAGES) & 1);
+          IG_TRACE(64 + 2 * gcount, gcount < 32);
+          tc_fence_after();
+          const uint32_t sa = sA0 + s * A_BYTES;
+          const uint32_t sb = sB0 + s * B_BYTES;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = to_f<T>(from_f<T>(v[i]));
-        if (mok) {
-          if (nb + 16 <= N && (a.ldd % EPC) == 0) {
+          for (int kk = 0; kk < KS / MmaTraits<T>::MMA_K; ++kk) {
+            const uint64_t ad = umma_sdesc(sa + kk * 32 * IG_BM, lbo_a, 128);
+            const uint64_t bd = umma_sdesc(sb + kk * 32 * BN, lbo_b, 128);
+            if (!(a.out_f32 & 4)) MmaTraits<T>::mma(td, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[s]);
+          IG_TRACE(65 + 2 * gcount, gcount < 32);
+        }
+        umma_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogue ===============================
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;
+    const int et = tid - IG_EPI_WARP0 * 32;  // 0..127
+    int i = 0;
+    int m0, n0, z, kb0, kb1;
+    for (; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
+      const int acc = i % NACC;
+      mbar_wait(&tfull_bar[acc], (i / NACC) & 1);
+      IG_TRACE(144 + 2 * i, et == 0 && i < 16);
+      tc_fence_after();
+      const int m = m0 + row;
+      const bool mok = m < M;
+      const uint32_t tl = tmem_d + acc * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 16; ++cc) {
+        float v[16];
+        tmem_ld16(tl + cc * 16, v);
+        const int nb = n0 + cc * 16;
+        if (MODE == DSP_IGEMM_WGRAD) {
+          float* out = reinterpret_cast<float*>(a.D) + (size_t)z * M * N + (size_t)m * N;
+          if (mok) {
+            if (nb + 16 <= N && (N & 3) == 0) {
 #pragma unroll
-            for (int q = 0; q < 16 / EPC; ++q) {
-              T tmp[EPC];
+              for (int qq = 0; qq < 4; ++qq)
+                *reinterpret_cast<float4*>(out + nb + 4 * qq) =
+                    make_float4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
+            } else {
 #pragma unroll
-              for (int e = 0; e < EPC; ++e) tmp[e] = from_f<T>(v[q * EPC + e]);
-              *reinterpret_cast<uint4*>(out + nb + q * EPC) = *reinterpret_cast<uint4*>(tmp);
+              for (int e = 0; e < 16; ++e)
+                if (nb + e < N) out[nb + e] = v[e];
+            }
+          }
+        } else {
+          const int nvalid = a.n_valid > 0 ? a.n_valid : N;
+          if (a.bias != nullptr) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (nb + e < nvalid) v[e] += a.bias[nb + e];
+          }
+          if (a.residual != nullptr && mok) {
+            const T* res = reinterpret_cast<const T*>(a.residual) + (size_t)m * a.ldd;
+            if (nb + 16 <= N && (a.ldd % EPC) == 0) {
+#pragma unroll
+              for (int qq = 0; qq < 16 / EPC; ++qq) {
+                uint4 raw = *reinterpret_cast<const uint4*>(res + nb + qq * EPC);
+                const T* e8 = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) v[qq * EPC + e] += to_f<T>(e8[e]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (nb + e < N) v[e] += to_f<T>(res[nb + e]);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (nb + e >= nvalid) v[e] = 0.f;
+          if (a.out_f32 & 1) {
+            float* out = reinterpret_cast<float*>(a.D) + (size_t)m * a.ldd;
+            if (mok) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (nb + e < N) out[nb + e] = v[e];
             }
           } else {
+            T* out = reinterpret_cast<T*>(a.D) + (size_t)m * a.ldd;
+            // round to the storage type first so BN statistics describe the stored tensor
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (nb + i < N) out[nb + i] = from_f<T>(v[i]);
+            for (int e = 0; e < 16; ++e) v[e] = to_f<T>(from_f<T>(v[e]));
+            if (mok) {
+              if (nb + 16 <= N && (a.ldd % EPC) == 0) {
+#pragma unroll
+                for (int qq = 0; qq < 16 / EPC; ++qq) {
+                  uint4 raw;
+                  T* e8 = reinterpret_cast<T*>(&raw);
+#pragma unroll
+                  for (int e = 0; e < EPC; ++e) e8[e] = from_f<T>(v[qq * EPC + e]);
+                  *reinterpret_cast<uint4*>(out + nb + qq * EPC) = raw;
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                  if (nb + e < N) out[nb + e] = from_f<T>(v[e]);
+              }
+            }
+          }
+          if (want_stats) {
+            float sq[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              v[e] = mok ? v[e] : 0.f;
+              sq[e] = v[e] * v[e];
+            }
+            const float s1 = colsum16(v, lane);
+            const float s2 = colsum16(sq, lane);
+            if ((lane & 1) == 0) {  // this warp's private running sums (same n-tile every tile)
+              red[q][cc * 16 + (lane >> 1)][0] += s1;
+              red[q][cc * 16 + (lane >> 1)][1] += s2;
+            }
           }
         }
       }
-      if (want_stats) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float x = mok ? v[i] : 0.f;
-          const float s1 = warp_sum(x);
-          const float s2 = warp_sum(x * x);
-          if (lane == 0) {
-            red[warp][cc * 16 + i][0] = s1;
-            red[warp][cc * 16 + i][1] = s2;
-          }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      IG_TRACE(145 + 2 * i, et == 0 && i < 16);
+    }
+    if (want_stats) {
+      epi_barrier();
+      const int n0c = (blockIdx.x % nt) * BN;
+      for (int c = et; c < BN; c += 128) {
+        const int n = n0c + c;
+        if (n < N) {
+          a.stats[((size_t)blockIdx.x * 2 + 0) * N + n] = (red[0][c][0] + red[1][c][0]) + (red[2][c][0] + red[3][c][0]);
+          a.stats[((size_t)blockIdx.x * 2 + 1) * N + n] = (red[0][c][1] + red[1][c][1]) + (red[2][c][1] + red[3][c][1]);
         }
       }
     }
   }
-  if (want_stats) {
+
+  // ---------------- fused BatchNorm finalize by the last CTA ----------------
+  const bool fuse_fin = want_stats && a.stat_out != nullptr && a.sem != nullptr;
+  if (fuse_fin) {
+    __threadfence();
     __syncthreads();
-    for (int c = tid; c < BN; c += IG_THREADS) {
-      const int n = n0 + c;
-      if (n < N) {
-        const float s1 = (red[0][c][0] + red[1][c][0]) + (red[2][c][0] + red[3][c][0]);
-        const float s2 = (red[0][c][1] + red[1][c][1]) + (red[2][c][1] + red[3][c][1]);
-        a.stats[((size_t)blockIdx.x * 2 + 0) * N + n] = s1;
-        a.stats[((size_t)blockIdx.x * 2 + 1) * N + n] = s2;
+    if (tid == 0) last_cta_s = (atomicAdd(a.sem, 1) == (int)gridDim.x - 1);
+    __syncthreads();
+    if (last_cta_s) {
+      __threadfence();
+      const int nvalid = a.n_valid > 0 ? a.n_valid : N;
+      const double count = (double)M;
+      for (int cb = 0; cb < N; cb += 256) {
+        const int cols = min(256, N - cb);
+        const int parts = 256 / cols;
+        if (tid < parts * cols) {
+          const int c = cb + tid % cols, p = tid / cols;
+          // only the CTAs that own column c's n-tile (c/BN == cta % nt) hold its sums
+          const int step = parts * nt;
+          const int G = (int)gridDim.x;
+          double s1 = 0.0, s2 = 0.0;
+          for (int b0 = c / BN + p * nt; b0 < G; b0 += 8 * step) {
+            float v1[8], v2[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {  // 8 independent loads in flight
+              const int b = b0 + e * step;
+              v1[e] = b < G ? __ldcg(&a.stats[((size_t)b * 2 + 0) * N + c]) : 0.f;
+              v2[e] = b < G ? __ldcg(&a.stats[((size_t)b * 2 + 1) * N + c]) : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              s1 += (double)v1[e];
+              s2 += (double)v2[e];
+            }
+          }
+          fin[tid][0] = s1;
+          fin[tid][1] = s2;
+        }
+        __syncthreads();
+        if (tid < cols) {
+          const int c = cb + tid;
+          double s1 = 0.0, s2 = 0.0;
+          for (int p = 0; p < parts; ++p) {
+            s1 += fin[p * cols + tid][0];
+            s2 += fin[p * cols + tid][1];
+          }
+          float mean = 0.f, inv = 0.f, scale = 0.f, shift = 0.f;
+          if (c < nvalid) {
+            const double mu = s1 / count;
+            double var = s2 / count - mu * mu;
+            if (var < 0.0) var = 0.0;
+            const double iv = 1.0 / sqrt(var + 1e-5);
+            mean = (float)mu;
+            inv = (float)iv;
+            scale = (float)((double)a.gamma[c] * iv);
+            shift = (float)((double)a.beta[c] - mu * (double)a.gamma[c] * iv);
+          }
+          a.stat_out[c] = mean;
+          a.stat_out[N + c] = inv;
+          a.stat_out[2 * N + c] = scale;
+          a.stat_out[3 * N + c] = shift;
+        }
+        __syncthreads();
       }
+      if (tid == 0) *a.sem = 0;
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == IG_MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem_d, TMEM_COLS);
+    tmem_dealloc(tmem_d, Cfg::TMEM_COLS);
+    IG_TRACE(177, lane == 0);
   }
 }
 
 template <typename T, int MODE, int BN>
 static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
-  const int smem = IG_STAGES * (IG_BM * 128 + BN * 128);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  using Cfg = IgCfg<BN>;
+  static int attr_state = 0;
+  static int num_sms = 148;
+  if (!attr_state) {
+    cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr_state = 1;
   }
-  dim3 grid((a.M + IG_BM - 1) / IG_BM, (a.N + BN - 1) / BN, MODE == DSP_IGEMM_WGRAD ? splits : 1);
-  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, smem, st>>>(a);
+  const int EPC = 16 / (int)sizeof(T);
+  const int KS = 8 * EPC;
+  const int nkb = (a.Kd + KS - 1) / KS;
+  const int ns = MODE == DSP_IGEMM_WGRAD ? (nkb + a.kb_per_split - 1) / a.kb_per_split : 1;
+  const int units = ((a.M + IG_BM - 1) / IG_BM) * ((a.N + BN - 1) / BN) * ns;
+  int grid = std::min(units, std::min(DSP_IGEMM_MAX_CTAS, num_sms * Cfg::CTAS_PER_SM));
+  if (MODE != DSP_IGEMM_WGRAD) {  // each CTA owns one n-tile: grid must be a multiple of nt
+    const int nt = (a.N + BN - 1) / BN;
+    grid = std::max(nt, grid / nt * nt);
+  }
+  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, Cfg::SMEM, st>>>(a);
+  (void)splits;
   note_launch();
   return cudaGetLastError();
 }
@@ -413,8 +618,6 @@ cudaError_t igemm_launch(int mode, int dtype, const dsp_igemm_args_t& a, int spl
     if (mode == DSP_IGEMM_WGRAD) return launch_mode<bf16, DSP_IGEMM_WGRAD>(a, splits, st);
   } else if (dtype == DSP_DTYPE_F32) {
     if (mode == DSP_IGEMM_FPROP) return launch_mode<float, DSP_IGEMM_FPROP>(a, splits, st);
-    if (mode == DSP_IGEMM_DGRAD) return launch_mode<float, DSP_IGEMM_DGRAD>(a, splits, st);
-    if (mode == DSP_IGEMM_WGRAD) return launch_mode<float, DSP_IGEMM_WGRAD>(a, splits, st);
   }
   return cudaErrorInvalidValue;
 }

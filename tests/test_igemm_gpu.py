@@ -42,7 +42,7 @@ def _geom(nimg, H, W, C_, K, R, stride, pad):
 
 
 def _run(mode, dtype, g, M, N, Kd, A, B, D, splits=1, kb=1, stats=None, residual=None, bias=None, ldd=None,
-         out_f32=0):
+         out_f32=0, stat_out=None, gamma=None, beta=None, sem=None, n_valid=0):
     a = L.IgemmArgs()
     a.geom = g
     a.M, a.N, a.Kd = M, N, Kd
@@ -53,6 +53,9 @@ def _run(mode, dtype, g, M, N, Kd, A, B, D, splits=1, kb=1, stats=None, residual
     a.bias = bias.data_ptr() if bias is not None else None
     a.stats = stats.data_ptr() if stats is not None else None
     a.kb_per_split = kb
+    a.n_valid = n_valid
+    for name, t in (("stat_out", stat_out), ("gamma", gamma), ("beta", beta), ("sem", sem)):
+        setattr(a, name, t.data_ptr() if t is not None else None)
     L.check(L.load().dsp_igemm(mode, dtype, C.byref(a), splits, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
 
@@ -84,14 +87,35 @@ def test_fprop(case, dt):
     M = nimg * P * Q
     y = torch.empty(nimg, P, Q, K, device="cuda", dtype=dt)
     ntiles = (M + 127) // 128
-    stats = torch.zeros(ntiles, 2, K, device="cuda")
-    _run(L.DSP_IGEMM_FPROP, dcode, g, M, K, R * R * Cc, x, w, y, stats=stats)
+    stats = torch.full((L.IGEMM_MAX_CTAS, 2, K), float("nan"), device="cuda")
+    stat_out = torch.full((4, K), float("nan"), device="cuda")
+    gamma = torch.rand(K, device="cuda") + 0.5
+    beta = torch.randn(K, device="cuda")
+    sem = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nvalid = K - 8 if K > 8 else K
+    _run(L.DSP_IGEMM_FPROP, dcode, g, M, K, R * R * Cc, x, w, y, stats=stats, stat_out=stat_out, gamma=gamma,
+         beta=beta, sem=sem, n_valid=nvalid)
     ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), stride=stride,
                    padding=pad).permute(0, 2, 3, 1)
+    ref[..., nvalid:] = 0.0
     torch.testing.assert_close(y.float(), ref, rtol=rtol, atol=atol)
     yv = y.float().reshape(-1, K)
-    torch.testing.assert_close(stats[:, 0].sum(0), yv.sum(0), rtol=1e-3, atol=1e-2)
-    torch.testing.assert_close(stats[:, 1].sum(0), (yv * yv).sum(0), rtol=1e-3, atol=1e-2)
+    bn = next(b for b in (16, 32, 64, 128, 256) if K <= b or b == 256)
+    nt = (K + bn - 1) // bn
+    ctas = min(296 if bn <= 64 else 148, (M + 127) // 128 * nt) // nt * nt
+    # CTA c holds the partial sums of n-tile c % nt only
+    owner = (torch.arange(ctas, device="cuda")[:, None] % nt) == (torch.arange(K, device="cuda")[None, :] // bn)
+    part = torch.where(owner[:, None, :], stats[:ctas], torch.zeros_like(stats[:ctas]))
+    torch.testing.assert_close(part[:, 0].sum(0), yv.sum(0), rtol=1e-3, atol=1e-2)
+    torch.testing.assert_close(part[:, 1].sum(0), (yv * yv).sum(0), rtol=1e-3, atol=1e-2)
+    # fused BatchNorm finalize (last CTA): mean / invstd / scale / shift, pad columns zero
+    mean = yv.double().mean(0)
+    var = yv.double().var(0, unbiased=False)
+    inv = 1.0 / torch.sqrt(var + 1e-5)
+    want = torch.stack([mean, inv, gamma.double() * inv, beta.double() - mean * gamma.double() * inv]).float()
+    want[:, nvalid:] = 0.0
+    torch.testing.assert_close(stat_out, want, rtol=2e-3, atol=2e-3)
+    assert int(sem.item()) == 0
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16])
