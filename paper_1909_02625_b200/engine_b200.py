@@ -1,11 +1,20 @@
 """B200 runtime behind ``TrainEngine``: the device half of ``_iterate_block``.
 
-One ``DeviceBlock`` per local block, all issued on one CUDA stream per
-process (blocks of one step are independent -- every packet they consume was
-produced in an earlier step -- so a single in-order stream is race-free and
-the GPU overlaps back-to-back kernels). Packets are device tensors; the
-per-(step, block) loss and squared gradient norm stay on the device until the
-log is read, so the training loop never synchronises with the host.
+One ``DeviceBlock`` per local block. Packets live in fixed device rings: the
+packet a block produces at step n occupies slot n mod R of its ring, where R
+exceeds every packet's lifetime in steps (an out-packet of block k lives
+p_k + m_{k+1} steps, an input packet m_0, a gradient packet q_k), so the
+buffers a step touches depend only on n mod R.
+
+That makes a step's device work periodic, and the runtime turns it into CUDA
+graphs (``graph_step``): once the zero prefill packets have drained, step n is
+captured once per phase n mod R -- each of the K local blocks on its own forked
+stream, since within a step the blocks are independent (every packet they read
+was produced in an earlier step) -- and afterwards replayed with one graph
+launch. A phase is re-captured if its learning rates / update flags change
+(lr decay). The per-step loss and squared grad norm land in per-phase slots
+that are copied into a device log after each replay; the host reads them
+lazily, so the training loop never synchronises.
 """
 
 from __future__ import annotations
@@ -14,7 +23,7 @@ import numpy as np
 
 from . import _lib as L
 from .optim import RULES, OptimizerState
-from .runtime import DeviceBlock, pack_input, require_cuda, torch_mod
+from .runtime import DeviceBlock, pack_input, ptr, require_cuda, stream_ptr, torch_mod
 
 
 def _pad8(c: int) -> int:
@@ -27,10 +36,10 @@ def act_elems(batch: int, shape: tuple) -> int:
 
 
 class B200Runtime:
-    SLOTS = 4096
+    LOG_CHUNK = 4096
 
     def __init__(self, model, local, batch: int, rule: str = "sgd", beta: float = 0.0, s: float = 1.0,
-                 weight_decay: float = 0.0, device=None):
+                 weight_decay: float = 0.0, device=None, config=None, use_graphs: bool = True):
         torch = torch_mod()
         self.torch = torch
         self.device = require_cuda(device)
@@ -38,15 +47,16 @@ class B200Runtime:
         self.model = model
         self.B = batch
         self.K = model.k
+        self.local = list(local)
         self.rule = rule
         self.rule_code = RULES[rule]
         self.beta = beta
         self.s = s
         self.wd = weight_decay
+        self.num_classes = model.output_dim
         self.dev = {}
         self.ys = {}
-        self.num_classes = model.output_dim
-        for k in local:
+        for k in self.local:
             blk = model.blocks[k]
             db = DeviceBlock(blk, batch, is_last=(k == self.K - 1), device=self.device, stream=self.stream)
             blk.dev = db
@@ -54,37 +64,111 @@ class B200Runtime:
             if rule == "sum":
                 with torch.cuda.stream(self.stream):
                     self.ys[k] = db.params.clone()
-        self._chunks = []
-        self._fill = self.SLOTS
-        self.launches = 0
+        # ---- rings (slot = step mod R) -------------------------------------------
+        if config is not None:
+            p, m, q = config.p, config.m, config.q
+            life = [m[0] + 1] + [p[k] + m[k + 1] + 1 for k in range(self.K - 1)] + [q[k] + 1 for k in range(1, self.K)]
+            self.R = max(life) + 1
+        else:
+            self.R = 8
+        R = self.R
+        self.ring_out = {k: [self._empty(self.dev[k].out_elems) for _ in range(R)]
+                         for k in self.local if k < self.K - 1}
+        self.ring_gin = {k: [self._empty(self.dev[k].in_elems) for _ in range(R)] for k in self.local if k > 0}
+        self.ring_in = [self._empty(self.in_elems(0)) for _ in range(R)] if 0 in self.local else []
+        self.ring_lab = [self._empty(batch, dtype=torch.int64, zero=True) for _ in range(R)] if 0 in self.local else []
+        self._pinned = {}
+        # ---- scalar slots: per phase, per block: [loss, grad_sq] ------------------
+        self.slots = self._empty(R * self.K * 2, dtype=torch.float32, zero=True)
+        self._log = []          # device chunks [LOG_CHUNK][K][2]
+        self._log_rows = 0
+        self._row_of_step = {}
+        # ---- graphs -----------------------------------------------------------------
+        self.use_graphs = use_graphs and torch.cuda.is_available()
+        self.graphs = {}        # phase -> (CUDAGraph, signature)
+        self.mode = "eager"     # eager | capture | replay
+        self._cur_stream = self.stream
+        self._block_streams = {k: torch.cuda.Stream(self.device) for k in self.local}
+        self.replayed_kernels = 0  # library kernels executed through graph replays
 
-    # ---------------------------------------------------------------- packets
+    def kernels_executed(self) -> int:
+        """Library kernels run so far: eager launches (dsp_launch_count, which also counts
+        the launches recorded while capturing) plus every graph replay's kernels."""
+        return int(L.load().dsp_launch_count()) + self.replayed_kernels
+
+    # ---------------------------------------------------------------- buffers
     def _empty(self, n, dtype=None, zero=False):
         torch = self.torch
         dtype = dtype or torch.bfloat16
         with torch.cuda.stream(self.stream):
-            return (torch.zeros if zero else torch.empty)(n, dtype=dtype, device=self.device)
+            return (torch.zeros if zero else torch.empty)(max(n, 1), dtype=dtype, device=self.device)
 
     def in_elems(self, k: int) -> int:
         return act_elems(self.B, self.model.blocks[k].in_shape)
 
-    def make_input(self, x, labels):
+    def _s(self, k):
+        """Stream for block k's work: its own forked stream while capturing a step graph."""
+        return self._block_streams[k] if self.mode == "capture" else self.stream
+
+    def make_input(self, x, labels, n: int = 0):
         from .data import DeviceBatch
 
-        if isinstance(x, DeviceBatch):  # already packed in HBM
-            return x.act, x.labels
+        torch = self.torch
+        slot = n % self.R
+        act, lab = self.ring_in[slot], self.ring_lab[slot]
+        if isinstance(x, DeviceBatch):
+            if self.mode == "eager":
+                self._copy_device_batch(x, slot)
+            else:  # graph steps copy the batch in right before the launch
+                self._pending_input = (x, slot)
+            return act, lab
         if x.shape[0] != self.B:
             raise ValueError(f"batch of {x.shape[0]} rows, engine sized for {self.B}")
-        lab = np.asarray(labels, dtype=np.int64)
-        if lab.shape != (self.B,):
-            raise ValueError(f"labels must have shape ({self.B},), got {lab.shape}")
-        if lab.size and (lab.min() < 0 or lab.max() >= self.num_classes):
+        lab_h = np.asarray(labels, dtype=np.int64)
+        if lab_h.shape != (self.B,):
+            raise ValueError(f"labels must have shape ({self.B},), got {lab_h.shape}")
+        if lab_h.size and (lab_h.min() < 0 or lab_h.max() >= self.num_classes):
             raise ValueError(f"label out of range [0, {self.num_classes})")
-        act = pack_input(np.asarray(x), self.model.blocks[0].in_shape, self.device, self.stream)
+        # host batch -> pinned staging slot -> device (H2D + pack run on the stream).
+        # Graph steps defer all of it to just before the launch (no syncs in capture).
+        if self.mode == "eager":
+            self._stage_host_input(x, lab_h, slot)
+            self._issue_host_input(slot)
+        else:
+            self._pending_input = ("host", slot, x, lab_h)
+        return act, lab
+
+    def _stage_host_input(self, x, lab_h, slot):
         torch = self.torch
+        ev = self._pinned.get(("ev", slot))
+        if ev is not None:
+            ev.synchronize()  # the previous H2D out of this pinned slot has completed
+        xs = self._pinned.get(("x", slot))
+        if xs is None:
+            xs = torch.empty(x.shape, dtype=torch.float32).pin_memory()
+            ls = torch.empty(self.B, dtype=torch.int64).pin_memory()
+            xd = self._empty(int(np.prod(x.shape)), dtype=torch.float32)
+            self._pinned[("x", slot)], self._pinned[("l", slot)], self._pinned[("xd", slot)] = xs, ls, xd
+        xs.numpy()[...] = x
+        self._pinned[("l", slot)].numpy()[...] = lab_h
+
+    def _copy_device_batch(self, db, slot):
+        with self.torch.cuda.stream(self.stream):
+            self.ring_in[slot].copy_(db.act, non_blocking=True)
+            self.ring_lab[slot].copy_(db.labels, non_blocking=True)
+
+    def _issue_host_input(self, slot):
+        torch = self.torch
+        xs, ls, xd = self._pinned[("x", slot)], self._pinned[("l", slot)], self._pinned[("xd", slot)]
+        c, h, w = self.model.blocks[0].in_shape
         with torch.cuda.stream(self.stream):
-            labd = torch.from_numpy(lab).pin_memory().to(self.device, non_blocking=True)
-        return act, labd
+            xd.copy_(xs.view(-1), non_blocking=True)
+            self.ring_lab[slot].copy_(ls, non_blocking=True)
+        L.check(L.load().dsp_pack_input(ptr(xd), ptr(self.ring_in[slot]), self.B, c, h, w, _pad8(c),
+                                        L.DSP_DTYPE_BF16, 1, stream_ptr(self.stream)))
+        ev = self._pinned.get(("ev", slot)) or torch.cuda.Event()
+        ev.record(self.stream)
+        self._pinned[("ev", slot)] = ev
 
     def zero_act(self, k: int):
         return self._empty(self.in_elems(k), zero=True)
@@ -122,62 +206,145 @@ class B200Runtime:
         return int(hdr[0].item())
 
     # ---------------------------------------------------------------- compute
-    def _slot(self):
-        if self._fill >= self.SLOTS:
-            self._chunks.append(self._empty(self.SLOTS, dtype=self.torch.float32, zero=True))
-            self._fill = 0
-        h = (len(self._chunks) - 1, self._fill)
-        self._fill += 1
-        return h
+    def _slot(self, n: int, k: int, which: int):
+        return ("slot", n, k, which)
 
-    def _slot_tensor(self, h):
-        return self._chunks[h[0]][h[1]:h[1] + 1]
+    def _slot_tensor(self, n: int, k: int, which: int):
+        i = ((n % self.R) * self.K + k) * 2 + which
+        return self.slots[i:i + 1]
 
-    def forward(self, k: int, x):
-        db = self.dev[k]
-        y = db.new_activation(db.out_elems)
-        db.forward(x, y, record=False)
+    def forward(self, k: int, x, n: int = 0):
+        y = self.ring_out[k][n % self.R]
+        if self.mode != "replay":
+            self.dev[k].forward(x, y, record=False, stream=self._s(k))
         return y
 
-    def forward_record(self, k: int, x) -> None:
-        self.dev[k].forward(x, None, record=True)
+    def forward_record(self, k: int, x, n: int = 0) -> None:
+        if self.mode != "replay":
+            self.dev[k].forward(x, None, record=True, stream=self._s(k))
 
-    def loss(self, k: int, labels):
-        h = self._slot()
-        self.dev[k].loss(labels, self._slot_tensor(h))
-        return h
+    def loss(self, k: int, labels, n: int = 0):
+        if self.mode != "replay":
+            self.dev[k].loss(labels, self._slot_tensor(n, k, 0), stream=self._s(k))
+        return self._slot(n, k, 0)
 
-    def backward(self, k: int, upstream, need_grad_in: bool):
-        db = self.dev[k]
-        gin = db.new_activation(db.in_elems) if need_grad_in else None
-        db.backward(upstream, gin)
+    def backward(self, k: int, upstream, need_grad_in: bool, n: int = 0):
+        gin = self.ring_gin[k][n % self.R] if need_grad_in else None
+        if self.mode != "replay":
+            self.dev[k].backward(upstream, gin, stream=self._s(k))
         return gin
 
-    def update(self, k: int, lr: float, slr: float, apply: bool):
-        h = self._slot()
-        self.dev[k].update(self.rule_code, self.ys.get(k), lr, slr, self.beta, self.wd, apply, self._slot_tensor(h))
-        return h
+    def update(self, k: int, lr: float, slr: float, apply: bool, n: int = 0):
+        if self.mode != "replay":
+            self.dev[k].update(self.rule_code, self.ys.get(k), lr, slr, self.beta, self.wd, apply,
+                               self._slot_tensor(n, k, 1), stream=self._s(k))
+        return self._slot(n, k, 1)
 
     def opt_state(self, k: int) -> OptimizerState:
         st = OptimizerState(rule=self.rule, beta=self.beta, s=self.s)
         st.ys = self.ys.get(k)
         return st
 
+    # ---------------------------------------------------------------- graph steps
+    def graph_step(self, n: int, signature, issue) -> None:
+        """Run step n's device work through the phase graph (capture on first use).
+
+        issue(): runs the engine's host-side loop body for all local blocks; in
+        capture mode it issues kernels, in replay mode it only does bookkeeping."""
+        torch = self.torch
+        phase = n % self.R
+        entry = self.graphs.get(phase)
+        if entry is not None and entry[1] == signature:
+            self.mode = "replay"
+            try:
+                issue()
+            finally:
+                self.mode = "eager"
+            self._pre_replay()
+            entry[0].replay()
+            self.replayed_kernels += entry[2]
+        else:
+            lib = L.load()
+            before = lib.dsp_launch_count()
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(self.device)
+            cs.wait_stream(self.stream)
+            self.mode = "capture"
+            saved = self.stream
+            try:
+                with torch.cuda.graph(g, stream=cs):
+                    fork = torch.cuda.Event()
+                    fork.record(cs)
+                    for k in self.local:
+                        self._block_streams[k].wait_event(fork)
+                    issue_stream = cs
+                    self.stream = issue_stream
+                    issue()
+                    for k in self.local:
+                        cs.wait_stream(self._block_streams[k])
+            finally:
+                self.mode = "eager"
+                self.stream = saved
+            self.stream.wait_stream(cs)
+            captured = lib.dsp_launch_count() - before
+            self.graphs[phase] = (g, signature, captured)
+            self._pre_replay()  # this step's input batch -> its ring slot, outside the graph
+            g.replay()  # (its kernels were counted once by dsp_launch_count while capturing)
+        self._post_step(n)
+
+    def _pre_replay(self):
+        pend = getattr(self, "_pending_input", None)
+        self._pending_input = None
+        if pend is None:
+            return
+        if pend[0] == "host":
+            _, slot, x, lab_h = pend
+            self._stage_host_input(x, lab_h, slot)
+            self._issue_host_input(slot)
+        else:
+            self._copy_device_batch(pend[0], pend[1])
+
+    def _post_step(self, n: int) -> None:
+        """Copy phase slots of step n into the device log (eager steps write slots too)."""
+        torch = self.torch
+        row = self._log_rows
+        if row % self.LOG_CHUNK == 0:
+            self._log.append(self._empty(self.LOG_CHUNK * self.K * 2, dtype=torch.float32, zero=True))
+        chunk = self._log[row // self.LOG_CHUNK]
+        r = row % self.LOG_CHUNK
+        ph = n % self.R
+        with torch.cuda.stream(self.stream):
+            chunk[r * self.K * 2:(r + 1) * self.K * 2].copy_(self.slots[ph * self.K * 2:(ph + 1) * self.K * 2],
+                                                             non_blocking=True)
+        self._row_of_step[n] = row
+        self._log_rows += 1
+
+    def end_step(self, n: int) -> None:
+        """Eager step finished (no graph): log its slots."""
+        self._pending_input = None
+        self._post_step(n)
+
     def synchronize(self) -> None:
         self.stream.synchronize()
 
+    def _value(self, h, host_chunks):
+        _, n, k, which = h
+        row = self._row_of_step[n]
+        return float(host_chunks[row // self.LOG_CHUNK][((row % self.LOG_CHUNK) * self.K + k) * 2 + which])
+
     def read_scalar(self, h) -> float:
-        return float(self._chunks[h[0]][h[1]].item())
+        _, n, k, which = h
+        row = self._row_of_step.get(n)
+        if row is None:  # not yet copied into the log: read the live slot
+            return float(self._slot_tensor(n, k, which).item())
+        c = self._log[row // self.LOG_CHUNK]
+        i = ((row % self.LOG_CHUNK) * self.K + k) * 2 + which
+        return float(c[i:i + 1].item())
 
     def read_scalars(self, pairs):
         self.stream.synchronize()
-        host = [c.cpu().numpy() for c in self._chunks]
-        out = []
-        for lh, gh in pairs:
-            lv = None if lh is None else float(host[lh[0]][lh[1]])
-            gv = float(host[gh[0]][gh[1]])
-            out.append((lv, gv))
-        return out
+        host = [c.cpu().numpy() for c in self._log]
+        return [(None if lh is None else self._value(lh, host), self._value(gh, host)) for lh, gh in pairs]
 
 
 def eval_forward(model, x: np.ndarray) -> np.ndarray:
@@ -194,13 +361,13 @@ def eval_forward(model, x: np.ndarray) -> np.ndarray:
             db = DeviceBlock(blk, B, is_last=(k == K - 1), device=device, stream=stream)
         if k < K - 1:
             y = db.new_activation(db.out_elems)
-            db.forward(h, y, record=False)
+            db.forward(h, y, record=False, stream=stream)
             h = y
         else:
             cp = _pad8(model.output_dim)
             with torch.cuda.stream(stream):
                 logits = torch.empty(B * cp, dtype=torch.float32, device=device)
-            db.forward(h, logits, record=False)
+            db.forward(h, logits, record=False, stream=stream)
             stream.synchronize()
             return logits.view(B, cp)[:, : model.output_dim].double().cpu().numpy()
     raise L.DspError(1, "empty model")

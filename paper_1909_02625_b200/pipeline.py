@@ -285,7 +285,7 @@ class TrainEngine:
         if _runtime is None:
             from .engine_b200 import B200Runtime
 
-            _runtime = B200Runtime(model, self.local, self.batch_size, rule=rule, beta=beta, s=s,
+            _runtime = B200Runtime(model, self.local, self.batch_size, rule=rule, beta=beta, s=s, config=config,
                                    weight_decay=weight_decay, device=device)
         self.rt = _runtime
 
@@ -339,7 +339,7 @@ class TrainEngine:
 
         if k == 0:
             x, labels = self._next_batch()
-            act, lab = rt.make_input(x, labels)
+            act, lab = rt.make_input(x, labels, n)
             fresh = ActivationPacket(n, act, lab)
         else:
             fresh = self.out_queues[k - 1].get()
@@ -351,27 +351,27 @@ class TrainEngine:
 
         loss_h = None
         if k < last:
-            h_out = rt.forward(k, fresh.tensor)
+            h_out = rt.forward(k, fresh.tensor, n)
             pkt = ActivationPacket(fresh.batch_index, h_out, fresh.labels)
             if self.placement[k + 1] == self.rank:
                 self.out_queues[k].put(pkt)
             else:
                 self._outbox_act[k] = pkt
-            rt.forward_record(k, stale.tensor)
+            rt.forward_record(k, stale.tensor, n)
             gpkt = self.grad_queues[k + 1].get()
             if gpkt.batch_index != stale.batch_index:
                 raise ProtocolError(f"block {k} step {n}: gradient batch {gpkt.batch_index} "
                                     f"does not meet activation batch {stale.batch_index}")
             upstream = gpkt.tensor
         else:
-            rt.forward_record(k, stale.tensor)
-            loss_h = rt.loss(k, stale.labels)
+            rt.forward_record(k, stale.tensor, n)
+            loss_h = rt.loss(k, stale.labels, n)
             upstream = None
 
         if self.straggler is not None:
             self.straggler.sleep_maybe(k, n, 1)
 
-        grad_in = rt.backward(k, upstream, need_grad_in=k > 0)
+        grad_in = rt.backward(k, upstream, k > 0, n)
         if k > 0:
             gp = GradPacket(stale.batch_index, grad_in)
             if self.placement[k - 1] == self.rank:
@@ -381,7 +381,7 @@ class TrainEngine:
 
         discard = cfg.warmup == "discard_warmup_updates" and stale.batch_index < 0
         lr = lr_at(self.schedule, n)
-        gsq_h = rt.update(k, lr, self.s * lr, apply=not discard)
+        gsq_h = rt.update(k, lr, self.s * lr, not discard, n)
         st = self.opt_states[k]
         if st is not None and not discard:
             st.n += 1
@@ -435,10 +435,36 @@ class TrainEngine:
     def run(self, n_steps: int) -> None:
         if n_steps < 0:
             raise ValueError("n_steps must be non-negative")
+        graphs = getattr(self.rt, "use_graphs", False) and self._transport.world <= 1
         for _ in range(n_steps):
-            for k in self.local:
-                self._iterate_block(k)
-            self._exchange()
+            n = self.block_steps[self.local[0]] if self.local else 0
+            if graphs and n >= self._graph_horizon():
+                self.rt.graph_step(n, self._step_signature(n), self._issue_step)
+            else:
+                self._issue_step()
+                end = getattr(self.rt, "end_step", None)
+                if end is not None:
+                    end(n)
+
+    def _issue_step(self) -> None:
+        for k in self.local:
+            self._iterate_block(k)
+        self._exchange()
+
+    def _graph_horizon(self) -> int:
+        """First step from which every queued packet is a ring slot (zero prefill drained)."""
+        c = self.config
+        return max(c.m) + max(c.p) + max(c.q) + 1
+
+    def _step_signature(self, n: int) -> tuple:
+        """Everything a step graph bakes in besides ring-slot addresses."""
+        sig = []
+        for k in self.local:
+            lr = lr_at(self.schedule, n)
+            tag = n - self._cum_p[k] - self.config.m[k]
+            discard = self.config.warmup == "discard_warmup_updates" and tag < 0
+            sig.append((lr, self.s * lr, not discard))
+        return tuple(sig)
 
     def synchronize(self) -> None:
         self.rt.synchronize()

@@ -100,18 +100,21 @@ class DeviceBlock:
                 return torch.zeros(n_elems, dtype=torch.bfloat16, device=self.device)
             return torch.empty(n_elems, dtype=torch.bfloat16, device=self.device)
 
-    def forward(self, x, y=None, record: bool = False) -> None:
-        L.check(self.lib.dsp_block_forward(self.h, ptr(x), ptr(y), int(record), stream_ptr(self.stream)))
+    def forward(self, x, y=None, record: bool = False, stream=None) -> None:
+        st = stream_ptr(stream or self.stream)
+        L.check(self.lib.dsp_block_forward(self.h, ptr(x), ptr(y), int(record), st))
 
-    def loss(self, labels, loss_out) -> None:
-        L.check(self.lib.dsp_block_loss(self.h, ptr(labels), ptr(loss_out), stream_ptr(self.stream)))
+    def loss(self, labels, loss_out, stream=None) -> None:
+        L.check(self.lib.dsp_block_loss(self.h, ptr(labels), ptr(loss_out), stream_ptr(stream or self.stream)))
 
-    def backward(self, upstream, grad_in) -> None:
-        L.check(self.lib.dsp_block_backward(self.h, ptr(upstream), ptr(grad_in), stream_ptr(self.stream)))
+    def backward(self, upstream, grad_in, stream=None) -> None:
+        L.check(self.lib.dsp_block_backward(self.h, ptr(upstream), ptr(grad_in), stream_ptr(stream or self.stream)))
 
-    def update(self, rule: int, ys, lr: float, slr: float, beta: float, wd: float, apply: bool, grad_sq_out) -> None:
+    def update(self, rule: int, ys, lr: float, slr: float, beta: float, wd: float, apply: bool, grad_sq_out,
+               stream=None) -> None:
         L.check(self.lib.dsp_block_update(self.h, rule, ptr(ys), C.c_double(lr), C.c_double(slr), C.c_double(beta),
-                                          C.c_double(wd), int(apply), ptr(grad_sq_out), stream_ptr(self.stream)))
+                                          C.c_double(wd), int(apply), ptr(grad_sq_out),
+                                          stream_ptr(stream or self.stream)))
 
 
 def pack_input(x_host: np.ndarray, shape: tuple, device, stream):

@@ -25,7 +25,7 @@ class OracleRuntime:
         self.tapes, self.tops, self.grads, self.vals = {}, {}, {}, []
 
     # packets
-    def make_input(self, x, labels):
+    def make_input(self, x, labels, n=0):
         return torch.from_numpy(np.asarray(x, dtype=np.float64)), torch.from_numpy(np.asarray(labels, dtype=np.int64))
 
     def zero_act(self, k):
@@ -65,25 +65,25 @@ class OracleRuntime:
         self.vals.append(v)
         return len(self.vals) - 1
 
-    def forward(self, k, x):
+    def forward(self, k, x, n=0):
         h, _ = R.block_forward(self.m.blocks[k], x.numpy())
         return torch.from_numpy(h)
 
-    def forward_record(self, k, x):
+    def forward_record(self, k, x, n=0):
         self.tops[k], self.tapes[k] = R.block_forward(self.m.blocks[k], x.numpy(), record=True)
 
-    def loss(self, k, labels):
+    def loss(self, k, labels, n=0):
         loss, up = R.softmax_xent(self.tops[k], labels.numpy())
         self._up = up
         return self._h(loss)
 
-    def backward(self, k, upstream, need_grad_in):
+    def backward(self, k, upstream, need_grad_in, n=0):
         up = self._up if upstream is None else upstream.numpy()
         g, gin = R.block_backward(self.m.blocks[k], self.tapes.pop(k), up)
         self.grads[k] = g
         return torch.from_numpy(gin) if need_grad_in else None
 
-    def update(self, k, lr, slr, apply):
+    def update(self, k, lr, slr, apply, n=0):
         blk = self.m.blocks[k]
         g0 = self.grads.pop(k)
         h = self._h(float((g0 ** 2).sum()))
