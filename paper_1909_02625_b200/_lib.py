@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libdsp_b200.so"
+LIB_PATH = Path(os.environ.get("DSP_B200_LIB", Path(__file__).resolve().parent / "libdsp_b200.so"))
 
 DSP_DTYPE_BF16 = 0
 DSP_DTYPE_F32 = 1

@@ -33,7 +33,12 @@
 #include "kernels.cuh"
 #include "../../include/dsp_b200.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace dsp {
 
@@ -57,13 +62,19 @@ struct MmaTraits<float> {
   __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t i, uint32_t acc) { umma_tf32(d, a, b, i, acc); }
 };
 
+#ifndef IG_STAGES_SMALL
+#define IG_STAGES_SMALL 5
+#endif
+#ifndef IG_MAX_CTAS_PER_SM
+#define IG_MAX_CTAS_PER_SM 2
+#endif
 template <int BN>
 struct IgCfg {
-  static constexpr int STAGES = BN <= 32 ? 5 : (BN <= 128 ? 4 : 3);
+  static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? 4 : 3);
   static constexpr int SMEM = STAGES * (IG_BM * 128 + BN * 128);
   static constexpr int NACC = BN <= 128 ? 4 : 2;  // TMEM accumulators: MMA runs NACC-1 tiles ahead
   static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
-  static constexpr int CTAS_PER_SM = (SMEM <= 100 * 1024 && TMEM_COLS <= 256) ? 2 : 1;
+  static constexpr int CTAS_PER_SM = (SMEM <= 100 * 1024 && TMEM_COLS <= 256) ? IG_MAX_CTAS_PER_SM : 1;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -103,8 +114,39 @@ __device__ __forceinline__ float colsum16(const float (&v)[16], int lane) {
   return w1;
 }
 
+// TMA configuration of one launch (host-decided, see tma_plan()).
+//   A (FPROP / stride-1 DGRAD): per k-block, 64/cbox boxes, one per (tap, channel
+//   chunk), each a 128-pixel im2col tile of cbox channels at tap-shifted
+//   coordinates; out-of-image taps are zero-filled by the TMA unit.
+//   B (FPROP weights [Cout][Kd]): one 64 x BN box per k-block, SWIZZLE_128B.
+struct IgTma {
+  int on_a, on_b;
+  int cbox;       // channels per A box (8, 16, 32, 64)
+  int hb, nb;     // A box extent in output rows / images (box = OW x hb x nb pixels)
+  int box_a;      // bytes per A box = 128 rows x cbox x 2
+  int swz_a;      // UMMA layout type of A (0 none, 6 SW32, 4 SW64, 2 SW128)
+  int box_b;      // bytes per B box = BN rows x 128
+  // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
+  // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
+  uint32_t fd_d[5], fd_mul[5], fd_shr[5];
+};
+
+static void fastdiv_host(uint32_t d, uint32_t& mul, uint32_t& shr) {
+  if (d <= 1) {
+    mul = 0;
+    shr = 0;
+    return;
+  }
+  uint32_t l = 0;
+  while ((1u << l) < d) ++l;
+  mul = (uint32_t)((((uint64_t)1 << (31 + l)) + d - 1) / d);
+  shr = 31 + l - 32;
+}
+
 template <typename T, int MODE, int BN>
-__global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kernel(const dsp_igemm_args_t a) {
+__global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
+    igemm_kernel(const dsp_igemm_args_t a, const __grid_constant__ CUtensorMap tmA,
+                 const __grid_constant__ CUtensorMap tmB, const IgTma tm) {
   using Cfg = IgCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NACC = Cfg::NACC;
@@ -165,9 +207,12 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
   };
   (void)units;
 
+  // full[s] arrivals: the TMA thread's arrive.expect_tx (if A uses TMA) plus one
+  // cp.async arrival per producer thread (if any operand is still gathered)
+  const bool gather = !(tm.on_a && tm.on_b);
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], 128);
+      mbar_init(&full_bar[s], (tm.on_a ? 1 : 0) + (gather ? 128 : 0));
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < NACC; ++s) {
@@ -195,25 +240,34 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
 
   if (warp < 4) {
     // =============================== producers ===============================
+    // (all-TMA launches: only thread 0 produces; the other producer threads go idle)
+    if (gather || warp == 0) {
     const int aj = tid & 7;
     const int ag = tid % AG;
     // every runtime divisor of the gathers as a multiply-shift (FastDiv)
-    FastDiv fd_pix, fd_row, fd_ch, fd_s, fd_k;
-    fd_pix.init(MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q);
-    fd_row.init(MODE == DSP_IGEMM_DGRAD ? g.W : g.Q);
-    fd_ch.init(MODE == DSP_IGEMM_DGRAD ? g.K : g.C);
-    fd_s.init(g.S);
-    fd_k.init(g.K);
+    FastDiv fd_pix{tm.fd_d[0], tm.fd_mul[0], tm.fd_shr[0]}, fd_row{tm.fd_d[1], tm.fd_mul[1], tm.fd_shr[1]},
+        fd_ch{tm.fd_d[2], tm.fd_mul[2], tm.fd_shr[2]}, fd_s{tm.fd_d[3], tm.fd_mul[3], tm.fd_shr[3]},
+        fd_k{tm.fd_d[4], tm.fd_mul[4], tm.fd_shr[4]};
     const int sh = g.stride == 2 ? 1 : 0;  // stride is 1 or 2
     const int img_stride = MODE == DSP_IGEMM_DGRAD ? g.P * g.Q * g.K : g.H * g.W * g.C;
+    const int out_hw = MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q;
+    const int out_w = MODE == DSP_IGEMM_DGRAD ? g.W : g.Q;
+    if (tm.on_a && tid == 0) {
+      tma_prefetch_desc(&tmA);
+      if (tm.on_b) tma_prefetch_desc(&tmB);
+    }
     int gcount = 0;
     int m0, n0, z, kb0, kb1;
     for (int j = 0; get_unit(j, m0, n0, z, kb0, kb1); ++j) {
+      const int t_n0 = m0 / out_hw;              // TMA tile origin: image, output row
+      const int t_h0 = (m0 - t_n0 * out_hw) / out_w;
       // per-tile A-row precompute
       int a_h[8], a_w[8], a_img[8];
       int wg_r = 0, wg_s = 0, wg_c = 0;
       bool wg_ok = false;
-      if (MODE != DSP_IGEMM_WGRAD) {
+      if (tm.on_a) {
+        // TMA computes the im2col addresses: nothing to decode per row
+      } else if (MODE != DSP_IGEMM_WGRAD) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int m = m0 + (tid >> 3) + 16 * i;
@@ -253,11 +307,40 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
         const uint32_t sA = sA0 + s * A_BYTES;
         const uint32_t sB = sB0 + s * B_BYTES;
         if (a.out_f32 & 2) {  // ablation: skip operand loads
-          cp_async_arrive_noinc(&full_bar[s]);
+          if (tm.on_a && tid == 0) mbar_arrive_expect_tx(&full_bar[s], 0);
+          if (gather) cp_async_arrive_noinc(&full_bar[s]);
           continue;
         }
         // ---------------- A operand ----------------
-        if (MODE != DSP_IGEMM_WGRAD) {
+        if (tm.on_a) {
+          // warp 0 issues the stage's TMA boxes in parallel, one per lane
+          const int nbox = KS / tm.cbox;
+          if (warp == 0) {
+            if (lane == 0)
+              mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(nbox * tm.box_a + (tm.on_b ? tm.box_b : 0)));
+            __syncwarp();
+            if (lane < nbox) {
+              const int jb = lane;
+              const int k0 = kb * KS + jb * tm.cbox;
+              int c0 = 0, rr = 0, ss2 = 0;
+              if (k0 < Kd) {
+                const int tap = fd_ch.divmod(k0, c0);
+                rr = fd_s.divmod(tap, ss2);
+              }
+              int cw, ch;
+              if (MODE == DSP_IGEMM_FPROP) {
+                cw = ss2 - g.pad;
+                ch = t_h0 * g.stride + rr - g.pad;
+              } else {
+                cw = g.pad - ss2;
+                ch = t_h0 + g.pad - rr;
+              }
+              if (k0 >= Kd) cw = -(1 << 20);  // no such tap: a fully out-of-bounds (zero) box
+              tma_load_4d(sA + jb * tm.box_a, &tmA, &full_bar[s], c0, cw, ch, t_n0);
+            }
+            if (tm.on_b && lane == 31) tma_load_2d(sB, &tmB, &full_bar[s], kb * KS, n0);
+          }
+        } else if (MODE != DSP_IGEMM_WGRAD) {
           const int k0 = kb * KS + aj * EPC;
           const bool kok = k0 < Kd;
           int c0 = 0, s2 = 0, r = 0;
@@ -308,7 +391,9 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
         }
         // ---------------- B operand ----------------
         constexpr int BCH = 8 * BN;
-        if (MODE == DSP_IGEMM_FPROP) {
+        if (tm.on_b) {
+          // loaded by the TMA thread above
+        } else if (MODE == DSP_IGEMM_FPROP) {
 #pragma unroll
           for (int c = tid; c < BCH; c += 128) {
             const int n = c >> 3, jj = c & 7;
@@ -336,17 +421,47 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
           }
         }
         // arrive on full[s] when this thread's copies land; never block the producer
-        cp_async_arrive_noinc(&full_bar[s]);
+        if (gather) cp_async_arrive_noinc(&full_bar[s]);
         IG_TRACE(2 * gcount + 1, tid == 0 && gcount < 32);
       }
     }
     cp_async_wait<0>();
+    }
   } else if (warp == IG_MMA_WARP) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, A_MN ? 1u : 0u, B_MN ? 1u : 0u, IG_BM, BN);
-      const uint32_t lbo_a = A_MN ? (IG_BM / EPC) * 128 : IG_BM * 16;
-      const uint32_t lbo_b = B_MN ? (BN / EPC) * 128 : BN * 16;
+      constexpr int NKK = KS / MmaTraits<T>::MMA_K;
+      // descriptor templates (start address 0) and per-MMA byte offsets, hoisted
+      // out of the loop: the issuing thread only adds the stage base.
+      uint64_t a_tpl, b_tpl;
+      uint32_t a_off[NKK], b_off[NKK];
+      if (tm.on_a) {
+        if (tm.cbox == 8) {  // two 16-byte-row boxes per MMA, SWIZZLE_NONE
+          a_tpl = umma_sdesc(0, tm.box_a, 128, 0);
+        } else {
+          a_tpl = umma_sdesc(0, 16, 8 * tm.cbox * 2, tm.swz_a);
+        }
+#pragma unroll
+        for (int kk = 0; kk < NKK; ++kk) {
+          const int e = kk * MmaTraits<T>::MMA_K;  // MMA kk reads K elements [e, e+16) of the stage
+          a_off[kk] = tm.cbox == 8 ? (e / 8) * tm.box_a : (e / tm.cbox) * tm.box_a + (e % tm.cbox) * 2;
+        }
+      } else {
+        a_tpl = umma_sdesc(0, A_MN ? (IG_BM / EPC) * 128 : IG_BM * 16, 128);
+#pragma unroll
+        for (int kk = 0; kk < NKK; ++kk) a_off[kk] = kk * 32 * IG_BM;
+      }
+      if (tm.on_b) {
+        b_tpl = umma_sdesc(0, 16, 1024, 2);  // [BN][128 B] SWIZZLE_128B
+#pragma unroll
+        for (int kk = 0; kk < NKK; ++kk) b_off[kk] = kk * 32;
+      } else {
+        b_tpl = umma_sdesc(0, B_MN ? (BN / EPC) * 128 : BN * 16, 128);
+#pragma unroll
+        for (int kk = 0; kk < NKK; ++kk) b_off[kk] = kk * 32 * BN;
+      }
+      const bool skip_mma = (a.out_f32 & 4) != 0;
       int gcount = 0, i = 0;
       int m0, n0, z, kb0, kb1;
       for (; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
@@ -362,11 +477,13 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
           tc_fence_after();
           const uint32_t sa = sA0 + s * A_BYTES;
           const uint32_t sb = sB0 + s * B_BYTES;
+          if (!skip_mma) {
 #pragma unroll
-          for (int kk = 0; kk < KS / MmaTraits<T>::MMA_K; ++kk) {
-            const uint64_t ad = umma_sdesc(sa + kk * 32 * IG_BM, lbo_a, 128);
-            const uint64_t bd = umma_sdesc(sb + kk * 32 * BN, lbo_b, 128);
-            if (!(a.out_f32 & 4)) MmaTraits<T>::mma(td, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < NKK; ++kk) {
+              const uint64_t ad = a_tpl | (uint64_t)(((sa + a_off[kk]) >> 4) & 0x3FFF);
+              const uint64_t bd = b_tpl | (uint64_t)(((sb + b_off[kk]) >> 4) & 0x3FFF);
+              MmaTraits<T>::mma(td, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty_bar[s]);
           IG_TRACE(65 + 2 * gcount, gcount < 32);
@@ -573,6 +690,84 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM) igemm_kern
   }
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Decide whether this launch's A (and B) operands can be fetched with TMA and
+// build the tensor maps. A: bf16 FPROP (stride 1/2) or stride-1 DGRAD whose
+// 128-row M tile is a whole box of output pixels (OW | 128 and the rows fit
+// the image, or whole images). B: FPROP weights [Cout_p][Kd].
+template <typename T, int MODE, int BN>
+static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB) {
+  tm = IgTma{};
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  static const bool disabled = getenv("DSP_B200_NO_TMA") != nullptr;
+  if (disabled || sizeof(T) != 2 || MODE == DSP_IGEMM_WGRAD) return;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (enc == nullptr) return;
+  const dsp_conv_geom_t& g = a.geom;
+  if (MODE == DSP_IGEMM_DGRAD && g.stride != 1) return;
+  if (g.stride != 1 && g.stride != 2) return;
+  const int cdim = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the gathered tensor
+  const int oh = MODE == DSP_IGEMM_FPROP ? g.P : g.H, ow = MODE == DSP_IGEMM_FPROP ? g.Q : g.W;
+  const int ih = MODE == DSP_IGEMM_FPROP ? g.H : g.P, iw = MODE == DSP_IGEMM_FPROP ? g.W : g.Q;
+  const int st = MODE == DSP_IGEMM_FPROP ? g.stride : 1;
+  const int cbox = std::min(cdim, 64);
+  if (cdim % cbox || (cbox != 8 && cbox != 16 && cbox != 32 && cbox != 64)) return;
+  if (IG_BM % ow) return;
+  int hb = IG_BM / ow, nb = 1;
+  if (hb <= oh) {
+    if (oh % hb) return;
+  } else {
+    if (IG_BM % (oh * ow) || g.nimg % (IG_BM / (oh * ow))) return;
+    nb = IG_BM / (oh * ow);
+    hb = oh;
+  }
+  if (ow * st > 256 || hb * st > 256 || (reinterpret_cast<uintptr_t>(a.A) & 15)) return;
+  cuuint64_t dims[4] = {(cuuint64_t)cdim, (cuuint64_t)iw, (cuuint64_t)ih, (cuuint64_t)g.nimg};
+  cuuint64_t strides[3] = {(cuuint64_t)cdim * 2, (cuuint64_t)iw * cdim * 2, (cuuint64_t)ih * iw * cdim * 2};
+  cuuint32_t box[4] = {(cuuint32_t)cbox, (cuuint32_t)(ow * st), (cuuint32_t)(hb * st), (cuuint32_t)nb};
+  cuuint32_t estr[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+  const CUtensorMapSwizzle swz = cbox == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                 : cbox == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : cbox == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
+  if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.A), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  tm.on_a = 1;
+  tm.cbox = cbox;
+  tm.hb = hb;
+  tm.nb = nb;
+  tm.box_a = IG_BM * cbox * 2;
+  tm.swz_a = cbox == 8 ? 0 : cbox == 16 ? 6 : cbox == 32 ? 4 : 2;
+  if (MODE == DSP_IGEMM_FPROP && (a.Kd % 8) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0) {
+    cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)g.K};
+    cuuint64_t bs[1] = {(cuuint64_t)a.Kd * 2};
+    cuuint32_t bb[2] = {64, (cuuint32_t)BN};
+    cuuint32_t be[2] = {1, 1};
+    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.B), bd, bs, bb, be,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      tm.on_b = 1;
+      tm.box_b = BN * 128;
+    }
+  }
+}
+
 template <typename T, int MODE, int BN>
 static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   using Cfg = IgCfg<BN>;
@@ -596,7 +791,20 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
     const int nt = (a.N + BN - 1) / BN;
     grid = std::max(nt, grid / nt * nt);
   }
-  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, Cfg::SMEM, st>>>(a);
+  IgTma tm;
+  CUtensorMap tmA, tmB;
+  tma_plan<T, MODE, BN>(a, tm, tmA, tmB);
+  {
+    const dsp_conv_geom_t& g = a.geom;
+    const uint32_t divs[5] = {(uint32_t)(MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q),
+                              (uint32_t)(MODE == DSP_IGEMM_DGRAD ? g.W : g.Q),
+                              (uint32_t)(MODE == DSP_IGEMM_DGRAD ? g.K : g.C), (uint32_t)g.S, (uint32_t)g.K};
+    for (int i = 0; i < 5; ++i) {
+      tm.fd_d[i] = divs[i];
+      fastdiv_host(divs[i], tm.fd_mul[i], tm.fd_shr[i]);
+    }
+  }
+  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tm);
   (void)splits;
   note_launch();
   return cudaGetLastError();
