@@ -186,17 +186,14 @@ int bn_backward_pair(dsp_block* b, const void* gsrc, const void* mask, const Con
                      void* dy2, void* g_out, cudaStream_t st) {
   const int64_t M = c1.M();
   const int Cp = c1.g.K;
-  const int chunks = bn_bwd_chunks(M, Cp);
-  DSP_CUDA(bn_bwd_reduce(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, b->bpart), M, Cp, st));
-  DSP_CUDA(bn_bwd_finalize(at<float>(b, b->bpart), chunks, Cp, c1.co_real, M, b->params + c1.gamma_off,
-                           at<float>(b, c1.stat), b->grads + c1.gamma_off, b->grads + c1.beta_off,
-                           at<float>(b, c1.coef), st));
+  int* sem = at<int32_t>(b, b->sem);
+  DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, b->bpart), M, Cp,
+                        c1.co_real, b->params + c1.gamma_off, b->grads + c1.gamma_off, b->grads + c1.beta_off,
+                        at<float>(b, c1.coef), sem, st));
   if (c2) {
-    DSP_CUDA(bn_bwd_reduce(b->dtype, gsrc, mask, b->ws + c2->y, at<float>(b, c2->stat), at<float>(b, b->bpart2), M, Cp,
-                           st));
-    DSP_CUDA(bn_bwd_finalize(at<float>(b, b->bpart2), chunks, Cp, c2->co_real, M, b->params + c2->gamma_off,
-                             at<float>(b, c2->stat), b->grads + c2->gamma_off, b->grads + c2->beta_off,
-                             at<float>(b, c2->coef), st));
+    DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mask, b->ws + c2->y, at<float>(b, c2->stat), at<float>(b, b->bpart2), M, Cp,
+                          c2->co_real, b->params + c2->gamma_off, b->grads + c2->gamma_off, b->grads + c2->beta_off,
+                          at<float>(b, c2->coef), sem, st));
   }
   DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, c1.coef), dy1,
                         c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
@@ -273,11 +270,9 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
   const int dt = b->dtype;
   switch (l.d.kind) {
     case DSP_LAYER_DENSE: {
-      if (l.b_off >= 0) {
-        const int chunks = bn_bwd_chunks(b->B, l.out_cp);
-        DSP_CUDA(bn_bwd_reduce(dt, u, nullptr, nullptr, nullptr, at<float>(b, b->bpart), b->B, l.out_cp, st));
-        DSP_CUDA(bn_bwd_finalize(at<float>(b, b->bpart), chunks, l.out_cp, l.out_real, b->B, nullptr, nullptr, nullptr,
-                                 b->grads + l.b_off, nullptr, st));
+      if (l.b_off >= 0) {  // bias gradient = column sums of u
+        DSP_CUDA(bn_bwd_stats(dt, u, nullptr, nullptr, nullptr, at<float>(b, b->bpart), b->B, l.out_cp, l.out_real,
+                              nullptr, nullptr, b->grads + l.b_off, nullptr, at<int32_t>(b, b->sem), st));
       }
       const ConvP& c = l.dense;
       dsp_igemm_args_t a{};

@@ -127,10 +127,21 @@ __global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ st
 
 // ------------------------------------------------------------------ BatchNorm backward
 // Layout of a reduction CTA: G = Cp/VE channel groups, TR = 256/G row lanes.
+struct BnBwdFin {  // fused finalize (last CTA) of the BatchNorm-backward reduction
+  int c_real;
+  double count;
+  const float* gamma;
+  const float* stat;
+  float* dgamma;
+  float* dbeta;
+  float* coef;
+  int* sem;
+};
+
 template <typename T>
 __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                 const float* __restrict__ stat, float* __restrict__ part, int64_t M, int Cp,
-                                int rows_per_chunk) {
+                                int rows_per_chunk, const BnBwdFin fin) {
   constexpr int VE = V16<T>::N;
   __shared__ float red[kThreads][2 * VE];
   const int G = Cp / VE;
@@ -191,6 +202,60 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
     part[((size_t)blockIdx.x * 2 + 0) * Cp + c] = a;
     part[((size_t)blockIdx.x * 2 + 1) * Cp + c] = b;
   }
+  if (fin.sem == nullptr) return;
+  // ---- last CTA to finish reduces the per-chunk partials in fixed order ----
+  __shared__ int last;
+  __shared__ double fs[kThreads][2];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(fin.sem, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int chunks = gridDim.x;
+  for (int cb = 0; cb < Cp; cb += kThreads) {
+    const int cols = min(kThreads, Cp - cb);
+    const int parts = kThreads / cols;
+    if (tid < parts * cols) {
+      const int c = cb + tid % cols, p0 = tid / cols;
+      double s1 = 0.0, s2 = 0.0;
+      for (int q0 = p0; q0 < chunks; q0 += 8 * parts) {
+        float v1[8], v2[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u * parts;
+          v1[u] = q < chunks ? __ldcg(&part[((size_t)q * 2 + 0) * Cp + c]) : 0.f;
+          v2[u] = q < chunks ? __ldcg(&part[((size_t)q * 2 + 1) * Cp + c]) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s1 += (double)v1[u];
+          s2 += (double)v2[u];
+        }
+      }
+      fs[tid][0] = s1;
+      fs[tid][1] = s2;
+    }
+    __syncthreads();
+    if (tid < cols) {
+      const int c = cb + tid;
+      double s1 = 0.0, s2 = 0.0;
+      for (int p = 0; p < parts; ++p) {
+        s1 += fs[p * cols + tid][0];
+        s2 += fs[p * cols + tid][1];
+      }
+      const bool real = c < fin.c_real;
+      if (real && fin.dbeta) fin.dbeta[c] = (float)s1;
+      if (real && fin.dgamma && fin.gamma) fin.dgamma[c] = (float)s2;
+      if (fin.coef) {
+        fin.coef[c] = (real && fin.gamma) ? fin.gamma[c] * fin.stat[Cp + c] : 0.f;
+        fin.coef[Cp + c] = real ? (float)(s1 / fin.count) : 0.f;
+        fin.coef[2 * Cp + c] = real ? (float)(s2 / fin.count) : 0.f;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *fin.sem = 0;
 }
 
 __global__ void bn_bwd_finalize_k(const float* __restrict__ part, int chunks, int Cp, int c_real, double count,
@@ -461,9 +526,17 @@ __global__ void wgrad_reduce_k(const float* __restrict__ part, int splits, int M
       if (ci >= ci_real || tap >= RS) continue;
       dst = ((int64_t)n * RS + tap) * ci_real + ci;
     }
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[((size_t)z * Mw + m) * N + n];
-    grad[dst] = s;
+    // 8 independent accumulators keep 8 loads in flight; fixed association -> deterministic
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const size_t zs = (size_t)Mw * N;
+    const float* p = part + (size_t)m * N + n;
+    int z = 0;
+    for (; z + 8 <= splits; z += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += __ldcg(p + (size_t)(z + u) * zs);
+    }
+    for (; z < splits; ++z) acc[0] += __ldcg(p + (size_t)z * zs);
+    grad[dst] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   }
 }
 
@@ -653,7 +726,22 @@ cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const v
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     bn_bwd_reduce_k<T><<<chunks, kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
-                                                    rows);
+                                                    rows, BnBwdFin{});
+    return note_launch(), cudaGetLastError();
+  });
+}
+
+cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
+                         int64_t M, int Cp, int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef,
+                         int* sem, cudaStream_t st) {
+  const int chunks = bn_bwd_chunks(M, Cp);
+  const int rows = (int)bn_rows_per_chunk(M, Cp);
+  const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sem};
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
+    bn_bwd_reduce_k<T><<<chunks, kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
+                                                    rows, fin);
     return note_launch(), cudaGetLastError();
   });
 }

@@ -125,7 +125,11 @@ struct IgTma {
   int hb, nb;     // A box extent in output rows / images (box = OW x hb x nb pixels)
   int box_a;      // bytes per A box = 128 rows x cbox x 2
   int swz_a;      // UMMA layout type of A (0 none, 6 SW32, 4 SW64, 2 SW128)
-  int box_b;      // bytes per B box = BN rows x 128
+  int box_b;      // bytes per B box (FPROP: BN rows x 128; WGRAD: 64 pixels x cbox_b x 2)
+  // WGRAD (both operands MN-major, k = 64 output pixels per stage):
+  int cbox_b;     // channels per B (dY) box
+  int swz_b;      // UMMA layout type of B
+  int kb_rows, kb_imgs;  // a 64-pixel k-block = Q x kb_rows x kb_imgs output pixels
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
   // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
   uint32_t fd_d[5], fd_mul[5], fd_shr[5];
@@ -312,7 +316,32 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
           continue;
         }
         // ---------------- A operand ----------------
-        if (tm.on_a) {
+        if (tm.on_a && MODE == DSP_IGEMM_WGRAD) {
+          // WGRAD: k-block = 64 output pixels; A box j = tap-shifted X pixels x cbox
+          // channels of MN range [m0 + j*cbox, +cbox); B box j = dY pixels x cbox_b
+          const int nbox_a = IG_BM / tm.cbox, nbox_b = BN / tm.cbox_b;
+          if (warp == 0) {
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(nbox_a * tm.box_a + nbox_b * tm.box_b));
+            __syncwarp();
+            int rem;
+            const int kn = fd_pix.divmod(kb * KS, rem);  // k-block origin: image, output row
+            const int kh = fd_row.div(rem);
+            if (lane < nbox_a) {
+              const int mm = m0 + lane * tm.cbox;
+              int c0 = 0, rr = 0, ss2 = 0;
+              const bool ok = mm < M;
+              if (ok) {
+                const int tap = fd_ch.divmod(mm, c0);
+                rr = fd_s.divmod(tap, ss2);
+              }
+              const int cw = ok ? ss2 - g.pad : -(1 << 20);  // rows past R*S*C: zero box
+              tma_load_4d(sA + lane * tm.box_a, &tmA, &full_bar[s], c0, cw, kh * g.stride + rr - g.pad, kn);
+            } else if (lane >= 32 - nbox_b) {
+              const int jb = lane - (32 - nbox_b);
+              tma_load_4d(sB + jb * tm.box_b, &tmB, &full_bar[s], n0 + jb * tm.cbox_b, 0, kh, kn);
+            }
+          }
+        } else if (tm.on_a) {
           // warp 0 issues the stage's TMA boxes in parallel, one per lane
           const int nbox = KS / tm.cbox;
           if (warp == 0) {
@@ -436,7 +465,21 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
       // out of the loop: the issuing thread only adds the stage base.
       uint64_t a_tpl, b_tpl;
       uint32_t a_off[NKK], b_off[NKK];
-      if (tm.on_a) {
+      // MN-major TMA tiles (WGRAD): rows = 64 pixels of rowbytes = cbox*2; an MMA
+      // reads 16 pixel rows; MN groups (boxes) are box bytes apart.
+      auto mn_tpl = [](int cbox, int box, int swz) -> uint64_t {
+        return swz == 0 ? umma_sdesc(0, 128, box, 0)                 // NONE: LBO = K-group, SBO = MN-group
+                        : umma_sdesc(0, box, 8 * cbox * 2, swz);     // swizzled: LBO = MN-group, SBO = 8 rows
+      };
+      if (tm.on_a && MODE == DSP_IGEMM_WGRAD) {
+        a_tpl = mn_tpl(tm.cbox, tm.box_a, tm.swz_a);
+        b_tpl = mn_tpl(tm.cbox_b, tm.box_b, tm.swz_b);
+#pragma unroll
+        for (int kk = 0; kk < NKK; ++kk) {
+          a_off[kk] = kk * 16 * tm.cbox * 2;
+          b_off[kk] = kk * 16 * tm.cbox_b * 2;
+        }
+      } else if (tm.on_a) {
         if (tm.cbox == 8) {  // two 16-byte-row boxes per MMA, SWIZZLE_NONE
           a_tpl = umma_sdesc(0, tm.box_a, 128, 0);
         } else {
@@ -452,7 +495,9 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
 #pragma unroll
         for (int kk = 0; kk < NKK; ++kk) a_off[kk] = kk * 32 * IG_BM;
       }
-      if (tm.on_b) {
+      if (MODE == DSP_IGEMM_WGRAD && tm.on_a) {
+        // set above
+      } else if (tm.on_b) {
         b_tpl = umma_sdesc(0, 16, 1024, 2);  // [BN][128 B] SWIZZLE_128B
 #pragma unroll
         for (int kk = 0; kk < NKK; ++kk) b_off[kk] = kk * 32;
@@ -714,10 +759,62 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   memset(&tmA, 0, sizeof(tmA));
   memset(&tmB, 0, sizeof(tmB));
   static const bool disabled = getenv("DSP_B200_NO_TMA") != nullptr;
-  if (disabled || sizeof(T) != 2 || MODE == DSP_IGEMM_WGRAD) return;
+  if (disabled || sizeof(T) != 2) return;
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (enc == nullptr) return;
   const dsp_conv_geom_t& g = a.geom;
+  auto swz_of = [](int cbox, int& umma) {
+    umma = cbox == 8 ? 0 : cbox == 16 ? 6 : cbox == 32 ? 4 : 2;
+    return cbox == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+           : cbox == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+           : cbox == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                        : CU_TENSOR_MAP_SWIZZLE_128B;
+  };
+  if (MODE == DSP_IGEMM_WGRAD) {
+    // k-block = 64 output pixels = Q x rows x imgs; A = X boxes per (tap, channel chunk), B = dY boxes
+    if (g.stride != 1 && g.stride != 2) return;
+    const int ca = std::min(g.C, 64), cb = std::min(std::min(g.K, 64), BN);
+    auto okc = [](int c) { return c == 8 || c == 16 || c == 32 || c == 64; };
+    if (!okc(ca) || !okc(cb) || g.C % ca || g.K % cb || BN % cb || IG_BM % ca) return;
+    if (64 % g.Q) return;
+    int rows = 64 / g.Q, imgs = 1;
+    if (rows <= g.P) {
+      if (g.P % rows) return;
+    } else {
+      if (64 % (g.P * g.Q) || g.nimg % (64 / (g.P * g.Q))) return;
+      imgs = 64 / (g.P * g.Q);
+      rows = g.P;
+    }
+    if (g.Q * g.stride > 256 || rows * g.stride > 256 || imgs > 256) return;
+    if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15)) return;
+    int ua, ub;
+    cuuint64_t xd[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.nimg};
+    cuuint64_t xs[3] = {(cuuint64_t)g.C * 2, (cuuint64_t)g.W * g.C * 2, (cuuint64_t)g.H * g.W * g.C * 2};
+    cuuint32_t xb[4] = {(cuuint32_t)ca, (cuuint32_t)(g.Q * g.stride), (cuuint32_t)(rows * g.stride), (cuuint32_t)imgs};
+    cuuint32_t xe[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+    cuuint64_t yd[4] = {(cuuint64_t)g.K, (cuuint64_t)g.Q, (cuuint64_t)g.P, (cuuint64_t)g.nimg};
+    cuuint64_t ys[3] = {(cuuint64_t)g.K * 2, (cuuint64_t)g.Q * g.K * 2, (cuuint64_t)g.P * g.Q * g.K * 2};
+    cuuint32_t yb[4] = {(cuuint32_t)cb, (cuuint32_t)g.Q, (cuuint32_t)rows, (cuuint32_t)imgs};
+    cuuint32_t ye[4] = {1, 1, 1, 1};
+    if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.A), xd, xs, xb, xe,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(ca, ua), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return;
+    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.B), yd, ys, yb, ye,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(cb, ub), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return;
+    tm.on_a = tm.on_b = 1;
+    tm.cbox = ca;
+    tm.box_a = 64 * ca * 2;
+    tm.swz_a = ua;
+    tm.cbox_b = cb;
+    tm.box_b = 64 * cb * 2;
+    tm.swz_b = ub;
+    tm.kb_rows = rows;
+    tm.kb_imgs = imgs;
+    return;
+  }
   if (MODE == DSP_IGEMM_DGRAD && g.stride != 1) return;
   if (g.stride != 1 && g.stride != 2) return;
   const int cdim = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the gathered tensor

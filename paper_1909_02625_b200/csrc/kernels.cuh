@@ -29,6 +29,12 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
 int bn_bwd_chunks(int64_t M, int Cp);
 cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
                           float* part, int64_t M, int Cp, cudaStream_t st);
+// Reduction + finalize in one launch: the last CTA to finish (atomic ticket on
+// *sem, which must be 0 and is left 0) sums the partials in fixed order and
+// writes dgamma/dbeta/coef exactly like bn_bwd_finalize.
+cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
+                         int64_t M, int Cp, int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef,
+                         int* sem, cudaStream_t st);
 // Finalize: sum partials -> dgamma/dbeta into the flat grad (if non-null) and
 // coefficients coef[0]=gamma*invstd, coef[1]=sum(g)/M, coef[2]=sum(g*xhat)/M.
 // With gamma == null (bias gradient) only dbeta = sum(g) is produced.
