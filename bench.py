@@ -189,6 +189,17 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ B200 arm
+def ncu_traffic():
+    """DRAM bytes (read + write) per launch of the roofline kernel from the committed
+    ncu --set full capture (profiles/ncu_roofline.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_roofline.json")) as f:
+            d = json.load(f)
+        return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
+    except Exception:
+        return None
+
+
 def kernel_roofline(torch, peaks, batch):
     """Time the dominant kernel alone (CUDA events, launching stream) on rotating
     buffers larger than L2; achieved = algorithmic bytes / average duration."""
@@ -233,7 +244,7 @@ def kernel_roofline(torch, peaks, batch):
     achieved = algo / t / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "igemm_kernel<bf16,FPROP,16> (ResNet-56 stage-1 conv3x3 16->16 + BN stats, B=128)",
+            "traffic": ncu_traffic(), "kernel": "igemm_kernel<bf16,FPROP,16> (ResNet-56 stage-1 conv3x3 16->16 + BN stats, B=128)",
             "algorithmic_bytes_per_launch": algo, "launch_us": t * 1e6,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
 
