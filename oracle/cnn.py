@@ -112,7 +112,7 @@ def conv_fwd(x, w, stride, pad):
     """y[b,co,p,q] = sum_{r,s,ci} x[b,ci,p*st+r-pad,q*st+s-pad] w[co,r,s,ci]."""
     co, k = w.shape[0], w.shape[1]
     cols, P, Q = _im2col(x, k, stride, pad)
-    y = cols @ w.reshape(co, -1).T
+    y = _mm(cols, w.reshape(co, -1).T)
     return y.reshape(x.shape[0], P, Q, co).transpose(0, 3, 1, 2), cols
 
 
@@ -120,8 +120,8 @@ def conv_bwd(dy, cols, x_shape, w, stride, pad):
     B, C, H, W = x_shape
     co, k = w.shape[0], w.shape[1]
     dyf = dy.transpose(0, 2, 3, 1).reshape(-1, co)
-    dw = (dyf.T @ cols).reshape(w.shape)
-    dcols = (dyf @ w.reshape(co, -1)).reshape(B, dy.shape[2], dy.shape[3], k, k, C)
+    dw = _mm(dyf.T, cols).reshape(w.shape)
+    dcols = _mm(dyf, w.reshape(co, -1)).reshape(B, dy.shape[2], dy.shape[3], k, k, C)
     dxp = np.zeros((B, H + 2 * pad, W + 2 * pad, C))  # NHWC scatter: contiguous inner dim
     P, Q = dy.shape[2], dy.shape[3]
     for r in range(k):
@@ -154,7 +154,16 @@ def bn_bwd(g, cache, gamma):
 # the device stores in bf16 at exactly the device's storage points (conv
 # outputs, BN/ReLU outputs, unit outputs, activation gradients, the bf16
 # weight shadow) so that ReLU masks match the device; sums stay float64.
-STORAGE = {"mode": "f64"}
+STORAGE = {"mode": "f64", "acc": "f64"}
+
+
+def _mm(a, b):
+    """Matrix product in the accumulation precision: float64, or float32 ("acc": "f32") to
+    measure how far an equally valid accumulation order moves the bf16 emulation from itself
+    (the noise floor the parity tolerances must sit above)."""
+    if STORAGE["acc"] == "f32":
+        return (a.astype(np.float32) @ b.astype(np.float32)).astype(np.float64)
+    return a @ b
 
 
 def bf16_round(x):

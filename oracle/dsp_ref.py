@@ -751,20 +751,22 @@ def stale_gradient(model: Model, fwd, bwd, x, labels, loss_and_grad=softmax_xent
 
 
 class storage:
-    """Context manager selecting the oracle's storage emulation ("f64" or "bf16")."""
+    """Context manager selecting the oracle's storage emulation ("f64" or "bf16") and the conv
+    accumulation precision ("f64", or "f32" for the noise-floor measurement of cnn._mm)."""
 
-    def __init__(self, mode: str):
-        if mode not in ("f64", "bf16"):
-            raise ValueError(mode)
-        self.mode = mode
+    def __init__(self, mode: str, acc: str = "f64"):
+        if mode not in ("f64", "bf16") or acc not in ("f64", "f32"):
+            raise ValueError((mode, acc))
+        self.mode, self.acc = mode, acc
 
     def __enter__(self):
-        self.prev = cnn.STORAGE["mode"]
-        cnn.STORAGE["mode"] = self.mode
+        self.prev = dict(cnn.STORAGE)
+        cnn.STORAGE.update(mode=self.mode, acc=self.acc)
         return self
 
     def __exit__(self, *exc):
-        cnn.STORAGE["mode"] = self.prev
+        cnn.STORAGE.clear()
+        cnn.STORAGE.update(self.prev)
         return False
 
 
