@@ -89,7 +89,8 @@ typedef struct {
   const float* gamma;
   const float* beta;
   int32_t* sem;
-  int64_t* trace;          /* optional profiling: clock64() stamps of CTA 0's pipeline events (>= 192 slots) */
+  int64_t* trace;          /* optional profiling: clock64() stamps of CTA 0's pipeline events (slots 0..191), then
+                              per-CTA %globaltimer start/setup/work/end (4 slots per CTA from 192) */
 } dsp_igemm_args_t;
 
 #define DSP_IGEMM_MAX_CTAS 296
@@ -174,6 +175,15 @@ const char* dsp_last_error(void);
 int dsp_abi_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */
 int64_t dsp_launch_count(void);
+
+/* Step-graph execution (the engine's replacement for the reference's per-step
+ * Python loop, pipeline.py:416-449).  graph: a captured cudaGraph_t; flags:
+ * DSP_GRAPH_NODE_PRIORITY honours each kernel node's priority (inherited from the
+ * capturing stream), so the pipeline's critical-path block is scheduled first. */
+#define DSP_GRAPH_NODE_PRIORITY 1
+int dsp_graph_instantiate(void* graph, int flags, void** exec_out);
+int dsp_graph_launch(void* exec, void* stream);
+int dsp_graph_destroy(void* exec);
 
 #ifdef __cplusplus
 }

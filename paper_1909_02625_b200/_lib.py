@@ -14,6 +14,7 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("DSP_B200_LIB", Path(__file__).resolve().parent / "libdsp_b200.so"))
 
 DSP_DTYPE_BF16 = 0
+DSP_GRAPH_NODE_PRIORITY = 1
 DSP_DTYPE_F32 = 1
 
 DSP_IGEMM_FPROP = 0
@@ -101,6 +102,9 @@ _SIGNATURES = {
     "dsp_last_error": (C.c_char_p, []),
     "dsp_abi_version": (C.c_int, []),
     "dsp_launch_count": (C.c_int64, []),
+    "dsp_graph_instantiate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "dsp_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dsp_graph_destroy": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None

@@ -35,6 +35,26 @@ extern "C" const char* dsp_last_error(void) { return g_last_error; }
 extern "C" int dsp_abi_version(void) { return DSP_ABI_VERSION; }
 extern "C" int64_t dsp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+extern "C" int dsp_graph_instantiate(void* graph, int flags, void** exec_out) {
+  if (graph == nullptr || exec_out == nullptr) return set_error(DSP_E_INVALID, "dsp_graph_instantiate: null argument");
+  cudaGraphExec_t exec = nullptr;
+  const unsigned long long f = (flags & DSP_GRAPH_NODE_PRIORITY) ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
+  DSP_CUDA(cudaGraphInstantiateWithFlags(&exec, static_cast<cudaGraph_t>(graph), f));
+  *exec_out = exec;
+  return DSP_OK;
+}
+
+extern "C" int dsp_graph_launch(void* exec, void* stream) {
+  if (exec == nullptr) return set_error(DSP_E_INVALID, "dsp_graph_launch: null graph");
+  DSP_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), static_cast<cudaStream_t>(stream)));
+  return DSP_OK;
+}
+
+extern "C" int dsp_graph_destroy(void* exec) {
+  if (exec != nullptr) DSP_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec)));
+  return DSP_OK;
+}
+
 extern "C" int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int splits, void* stream) {
   if (args == nullptr) return set_error(DSP_E_INVALID, "dsp_igemm: null args");
   if (mode < DSP_IGEMM_FPROP || mode > DSP_IGEMM_WGRAD) return set_error(DSP_E_INVALID, "dsp_igemm: bad mode %d", mode);

@@ -19,6 +19,77 @@ namespace dsp {
 typedef __nv_bfloat16 bf16;
 
 // ---------------------------------------------------------------- mbarrier
+// Last-CTA ticket for fused grid reductions. Every thread of the CTA calls it after
+// writing its partials; returns true (CTA-uniformly) in the CTA that arrives last, with
+// every other CTA's earlier global writes visible to all of its threads (read them with
+// ld.global.cg). One thread fences at gpu scope (release before the ticket, acquire
+// after it), the bar.syncs extend the ordering to the rest of the CTA; a per-thread
+// __threadfence() (MEMBAR.SC.GPU in every warp) cost 5-7 us per launch here.
+__device__ __forceinline__ bool last_cta_ticket(int* sem, int total, int* flag_smem, int dbg = 0) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int old = 0;
+    if (!(dbg & 1)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (!(dbg & 2)) asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(sem) : "memory");
+    const int last = old == total - 1;
+    if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    *flag_smem = last;
+  }
+  __syncthreads();
+  return *flag_smem != 0;
+}
+
+// Fixed-order reduction of per-CTA partial rows part[b][2][N] (two statistics per column)
+// over columns [w0, w0 + cols), cols % 4 == 0, cols <= 512, by the first 256 threads:
+// thread = (part p, lane = (statistic, 4-column group)); a lane reads its float4 of rows
+// b = tile + (p + k * np) * nt (tile = column / BN: only those CTAs own the columns),
+// 8 rows in flight per batch, into fin4[256][4] (smem). part_sums_get() then adds the np
+// parts of one column in order. Deterministic: the assignment never depends on timing.
+template <int DEPTH = 8>
+__device__ __forceinline__ void part_sums_load(const float* part, int G, int N, int w0, int cols, int BN, int nt,
+                                               double* fin4) {
+  const int tid = threadIdx.x;
+  const int g4 = cols / 4, lanes = 2 * g4, np = 256 / lanes;
+  if (tid >= np * lanes) return;
+  const int ln = tid % lanes, p0 = tid / lanes;
+  const int stat = ln / g4, c = w0 + (ln % g4) * 4;
+  const int tile = c / BN;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b0 = tile + p0 * nt; b0 < G; b0 += DEPTH * np * nt) {
+    float4 v[DEPTH];
+#pragma unroll
+    for (int e = 0; e < DEPTH; ++e) {
+      const int b = b0 + e * np * nt;
+      v[e] = b < G ? __ldcg(reinterpret_cast<const float4*>(&part[((size_t)b * 2 + stat) * N + c]))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int e = 0; e < DEPTH; ++e) {
+      acc[0] += (double)v[e].x;
+      acc[1] += (double)v[e].y;
+      acc[2] += (double)v[e].z;
+      acc[3] += (double)v[e].w;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) fin4[tid * 4 + e] = acc[e];
+}
+__device__ __forceinline__ void part_sums_get(const double* fin4, int cols, int cc, double& s1, double& s2) {
+  const int g4 = cols / 4, lanes = 2 * g4, np = 256 / lanes;
+  s1 = 0.0;
+  s2 = 0.0;
+  for (int p = 0; p < np; ++p) {
+    s1 += fin4[(p * lanes + cc / 4) * 4 + (cc & 3)];
+    s2 += fin4[(p * lanes + g4 + cc / 4) * 4 + (cc & 3)];
+  }
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -169,6 +240,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA tensor store smem -> global (bulk-group completion), and its waits.
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap), "r"(src),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }

@@ -65,13 +65,31 @@ struct MmaTraits<float> {
 #ifndef IG_STAGES_SMALL
 #define IG_STAGES_SMALL 5
 #endif
+#ifndef IG_REG_BLOCKS  // register budget as if this many CTAs shared an SM (headroom for other streams)
+#define IG_REG_BLOCKS 3
+#endif
 #ifndef IG_MAX_CTAS_PER_SM
 #define IG_MAX_CTAS_PER_SM 2
 #endif
+// Instrumentation (clock64 pipeline stamps of CTA 0, per-CTA %globaltimer timeline into
+// a.trace) is compiled in only with -DIG_TRACE_BUILD: it costs registers, and register
+// headroom decides how many of the other blocks' CTAs fit beside a conv CTA.
+#ifdef IG_TRACE_BUILD
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
+
 template <int BN>
 struct IgCfg {
   static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? 4 : 3);
-  static constexpr int SMEM = STAGES * (IG_BM * 128 + BN * 128);
+  static constexpr int RING = STAGES * (IG_BM * 128 + BN * 128);
+#ifdef IG_TMA_STORE
+  static constexpr int OUT_BYTES = IG_BM * BN * 2;  // bf16 output tile staged for the TMA store
+#else
+  static constexpr int OUT_BYTES = 0;
+#endif
+  static constexpr int SMEM = RING + OUT_BYTES;
   static constexpr int NACC = BN <= 128 ? 4 : 2;  // TMEM accumulators: MMA runs NACC-1 tiles ahead
   static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
   static constexpr int CTAS_PER_SM = (SMEM <= 100 * 1024 && TMEM_COLS <= 256) ? IG_MAX_CTAS_PER_SM : 1;
@@ -130,6 +148,9 @@ struct IgTma {
   int cbox_b;     // channels per B (dY) box
   int swz_b;      // UMMA layout type of B
   int kb_rows, kb_imgs;  // a 64-pixel k-block = Q x kb_rows x kb_imgs output pixels
+  // D (bf16 FPROP / DGRAD output): epilogue stages the 128 x BN tile in smem, one TMA
+  // store per box of d_cols columns (rows of d_cols*2 bytes, swizzle mask d_swz)
+  int on_d, d_cols, d_swz;
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
   // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
   uint32_t fd_d[5], fd_mul[5], fd_shr[5];
@@ -148,9 +169,11 @@ static void fastdiv_host(uint32_t d, uint32_t& mul, uint32_t& shr) {
 }
 
 template <typename T, int MODE, int BN>
-__global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
+__global__ void __launch_bounds__(IG_THREADS, IG_REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM ? IG_REG_BLOCKS
+                                                                                : IgCfg<BN>::CTAS_PER_SM)
     igemm_kernel(const dsp_igemm_args_t a, const __grid_constant__ CUtensorMap tmA,
-                 const __grid_constant__ CUtensorMap tmB, const IgTma tm) {
+                 const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmD,
+                 const IgTma tm) {
   using Cfg = IgCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NACC = Cfg::NACC;
@@ -168,11 +191,11 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
   __shared__ uint32_t tmem_base_s;
   __shared__ int last_cta_s;
   __shared__ float red[4][BN][2];
-  __shared__ double fin[256][2];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  if (kTrace && a.trace != nullptr && tid == 0) a.trace[192 + 8 * blockIdx.x] = (int64_t)globaltimer_ns();
   const dsp_conv_geom_t g = a.geom;
   const int M = a.M, N = a.N, Kd = a.Kd;
   const T* __restrict__ Asrc = reinterpret_cast<const T*>(a.A);
@@ -233,12 +256,15 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_d = tmem_base_s;
-  int64_t* const trace = (a.trace != nullptr && blockIdx.x == 0) ? a.trace : nullptr;
+  int64_t* const trace = (kTrace && a.trace != nullptr && blockIdx.x == 0) ? a.trace : nullptr;
 #define IG_TRACE(slot, cond)                                   \
   do {                                                          \
     if (trace != nullptr && (cond) && (slot) < 192) trace[(slot)] = clock64(); \
   } while (0)
   IG_TRACE(176, tid == 0);
+  // per-CTA global timeline (ns) after CTA 0's detail slots: start, setup done, work done, end
+  int64_t* const ctat = (kTrace && a.trace != nullptr) ? a.trace + 192 + 8 * blockIdx.x : nullptr;
+  if (ctat != nullptr && tid == 0) ctat[1] = (int64_t)globaltimer_ns();
   const uint32_t sA0 = smem_u32(smem);
   const uint32_t sB0 = sA0 + STAGES * A_BYTES;
 
@@ -542,6 +568,8 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;
     const int et = tid - IG_EPI_WARP0 * 32;  // 0..127
+    const bool tma_out = Cfg::OUT_BYTES > 0 && MODE != DSP_IGEMM_WGRAD && sizeof(T) == 2 && tm.on_d;
+    const uint32_t sOut = sA0 + Cfg::RING;  // 1024-aligned staging tile, boxes of 128 x d_cols
     int i = 0;
     int m0, n0, z, kb0, kb1;
     for (; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
@@ -549,6 +577,10 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
       mbar_wait(&tfull_bar[acc], (i / NACC) & 1);
       IG_TRACE(144 + 2 * i, et == 0 && i < 16);
       tc_fence_after();
+      if (tma_out && i > 0) {  // the previous tile's store must have read the staging tile
+        if (et == 0) bulk_wait_read0();
+        epi_barrier();
+      }
       const int m = m0 + row;
       const bool mok = m < M;
       const uint32_t tl = tmem_d + acc * BN + ((uint32_t)(q * 32) << 16);
@@ -604,6 +636,25 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
               for (int e = 0; e < 16; ++e)
                 if (nb + e < N) out[nb + e] = v[e];
             }
+          } else if (tma_out) {
+            // round to bf16 (BN statistics describe the stored tensor) and stage two 16-byte
+            // chunks of this row in the TMA swizzle pattern (conflict-free across lanes)
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = to_f<T>(from_f<T>(v[e]));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = cc * 16 + h * 8;
+              const uint32_t off = (uint32_t)((col / tm.d_cols) * (IG_BM * tm.d_cols * 2) + row * tm.d_cols * 2 +
+                                              (col % tm.d_cols) * 2);
+              const uint32_t sw = off ^ (((off >> 7) & (uint32_t)tm.d_swz) << 4);
+              uint4 raw;
+              T* e8 = reinterpret_cast<T*>(&raw);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) e8[e] = from_f<T>(v[h * 8 + e]);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sOut + sw), "r"(raw.x), "r"(raw.y),
+                           "r"(raw.z), "r"(raw.w)
+                           : "memory");
+            }
           } else {
             T* out = reinterpret_cast<T*>(a.D) + (size_t)m * a.ldd;
             // round to the storage type first so BN statistics describe the stored tensor
@@ -644,8 +695,18 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
+      if (tma_out) {  // whole tile staged: one thread stores it (rows >= M / cols >= N are clipped)
+        fence_proxy_async_smem();
+        epi_barrier();
+        if (et == 0) {
+          for (int b = 0; b * tm.d_cols < BN; ++b)
+            tma_store_2d(&tmD, sOut + b * (IG_BM * tm.d_cols * 2), n0 + b * tm.d_cols, m0);
+          bulk_commit();
+        }
+      }
       IG_TRACE(145 + 2 * i, et == 0 && i < 16);
     }
+    if (tma_out && et == 0) bulk_wait0();
     if (want_stats) {
       epi_barrier();
       const int n0c = (blockIdx.x % nt) * BN;
@@ -660,78 +721,94 @@ __global__ void __launch_bounds__(IG_THREADS, IgCfg<BN>::CTAS_PER_SM)
   }
 
   // ---------------- fused BatchNorm finalize by the last CTA ----------------
+  if (ctat != nullptr) {
+    __syncthreads();
+    if (tid == 0) ctat[2] = (int64_t)globaltimer_ns();
+  }
   const bool fuse_fin = want_stats && a.stat_out != nullptr && a.sem != nullptr;
   if (fuse_fin) {
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last_cta_s = (atomicAdd(a.sem, 1) == (int)gridDim.x - 1);
-    __syncthreads();
-    if (last_cta_s) {
-      __threadfence();
+    if (last_cta_ticket(a.sem, (int)gridDim.x, &last_cta_s, (a.out_f32 >> 8) & 3)) {
+      if (kTrace && a.trace != nullptr && tid == 0) a.trace[186] = (int64_t)globaltimer_ns();
       const int nvalid = a.n_valid > 0 ? a.n_valid : N;
       const double count = (double)M;
-      for (int cb = 0; cb < N; cb += 256) {
-        const int cols = min(256, N - cb);
-        const int parts = 256 / cols;
-        if (tid < parts * cols) {
-          const int c = cb + tid % cols, p = tid / cols;
-          // only the CTAs that own column c's n-tile (c/BN == cta % nt) hold its sums
-          const int step = parts * nt;
-          const int G = (int)gridDim.x;
-          double s1 = 0.0, s2 = 0.0;
-          for (int b0 = c / BN + p * nt; b0 < G; b0 += 8 * step) {
-            float v1[8], v2[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {  // 8 independent loads in flight
-              const int b = b0 + e * step;
-              v1[e] = b < G ? __ldcg(&a.stats[((size_t)b * 2 + 0) * N + c]) : 0.f;
-              v2[e] = b < G ? __ldcg(&a.stats[((size_t)b * 2 + 1) * N + c]) : 0.f;
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              s1 += (double)v1[e];
-              s2 += (double)v2[e];
-            }
-          }
-          fin[tid][0] = s1;
-          fin[tid][1] = s2;
+      const int G = (int)gridDim.x;
+      auto finish = [&](int c, double s1, double s2) {
+        float mean = 0.f, inv = 0.f, scale = 0.f, shift = 0.f;
+        if (c < nvalid) {
+          const double mu = s1 / count;
+          double var = s2 / count - mu * mu;
+          if (var < 0.0) var = 0.0;
+          const double iv = 1.0 / sqrt(var + 1e-5);
+          mean = (float)mu;
+          inv = (float)iv;
+          scale = (float)((double)a.gamma[c] * iv);
+          shift = (float)((double)a.beta[c] - mu * (double)a.gamma[c] * iv);
         }
-        __syncthreads();
-        if (tid < cols) {
-          const int c = cb + tid;
-          double s1 = 0.0, s2 = 0.0;
-          for (int p = 0; p < parts; ++p) {
-            s1 += fin[p * cols + tid][0];
-            s2 += fin[p * cols + tid][1];
+        a.stat_out[c] = mean;
+        a.stat_out[N + c] = inv;
+        a.stat_out[2 * N + c] = scale;
+        a.stat_out[3 * N + c] = shift;
+      };
+      if ((N & 3) == 0) {
+        // One L2 round trip: 256 threads = (part, lane), lane = (statistic, 4-column group);
+        // a lane reads its column group of every owning CTA's partial row as float4,
+        // 8 rows in flight per batch; then a fixed-order sum over parts (deterministic).
+        double* fin4 = reinterpret_cast<double*>(smem);  // operand ring is idle by now
+        for (int w0 = 0; w0 < N; w0 += 512) {
+          const int cols = min(512, N - w0);
+          part_sums_load<4>(a.stats, G, N, w0, cols, BN, nt, fin4);
+          __syncthreads();
+          if (kTrace && a.trace != nullptr && tid == 0 && w0 == 0) a.trace[187] = (int64_t)globaltimer_ns();
+          for (int cc = tid; cc < cols; cc += IG_THREADS) {
+            double s1, s2;
+            part_sums_get(fin4, cols, cc, s1, s2);
+            finish(w0 + cc, s1, s2);
           }
-          float mean = 0.f, inv = 0.f, scale = 0.f, shift = 0.f;
-          if (c < nvalid) {
-            const double mu = s1 / count;
-            double var = s2 / count - mu * mu;
-            if (var < 0.0) var = 0.0;
-            const double iv = 1.0 / sqrt(var + 1e-5);
-            mean = (float)mu;
-            inv = (float)iv;
-            scale = (float)((double)a.gamma[c] * iv);
-            shift = (float)((double)a.beta[c] - mu * (double)a.gamma[c] * iv);
-          }
-          a.stat_out[c] = mean;
-          a.stat_out[N + c] = inv;
-          a.stat_out[2 * N + c] = scale;
-          a.stat_out[3 * N + c] = shift;
+          __syncthreads();
         }
-        __syncthreads();
+      } else {
+        double(*fin)[2] = reinterpret_cast<double(*)[2]>(smem);
+        for (int cb = 0; cb < N; cb += 256) {
+          const int cols = min(256, N - cb);
+          const int parts = 256 / cols;
+          if (tid < parts * cols) {
+            const int c = cb + tid % cols, p = tid / cols;
+            const int step = parts * nt;
+            double s1 = 0.0, s2 = 0.0;
+            for (int b = c / BN + p * nt; b < G; b += step) {
+              s1 += (double)__ldcg(&a.stats[((size_t)b * 2 + 0) * N + c]);
+              s2 += (double)__ldcg(&a.stats[((size_t)b * 2 + 1) * N + c]);
+            }
+            fin[tid][0] = s1;
+            fin[tid][1] = s2;
+          }
+          __syncthreads();
+          if (tid < cols) {
+            double s1 = 0.0, s2 = 0.0;
+            for (int p = 0; p < parts; ++p) {
+              s1 += fin[p * cols + tid][0];
+              s2 += fin[p * cols + tid][1];
+            }
+            finish(cb + tid, s1, s2);
+          }
+          __syncthreads();
+        }
       }
       if (tid == 0) *a.sem = 0;
+      if (kTrace && a.trace != nullptr && tid == 0) a.trace[188] = (int64_t)globaltimer_ns();
     }
   }
 
+  if (ctat != nullptr && tid == 0) ctat[4] = (int64_t)globaltimer_ns();
   tc_fence_before();
   __syncthreads();
+  if (ctat != nullptr && tid == 0) ctat[5] = (int64_t)globaltimer_ns();
   if (warp == IG_MMA_WARP) {
+    if (ctat != nullptr && lane == 0) ctat[6] = (int64_t)globaltimer_ns();
     tc_fence_after();
     tmem_dealloc(tmem_d, Cfg::TMEM_COLS);
     IG_TRACE(177, lane == 0);
+    if (ctat != nullptr && lane == 0) ctat[3] = (int64_t)globaltimer_ns();
   }
 }
 
@@ -865,6 +942,34 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   }
 }
 
+// D through TMA stores: bf16 FPROP / DGRAD outputs with 16-byte aligned rows.
+template <typename T, int MODE, int BN>
+static void tma_out_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
+  memset(&tmD, 0, sizeof(tmD));
+  tm.on_d = 0;
+  // Measured on B200 (ResNet-56 shapes): no gain over per-row st.global.v4 once the
+  // staging tile costs ring stages, so it is compiled in only with -DIG_TMA_STORE.
+  if (IgCfg<BN>::OUT_BYTES == 0) return;
+  if (MODE == DSP_IGEMM_WGRAD || sizeof(T) != 2 || (a.out_f32 & 1)) return;
+  if ((reinterpret_cast<uintptr_t>(a.D) & 15) || (a.ldd % 8) || a.N % 8) return;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (enc == nullptr) return;
+  const int cols = std::min(BN, 64);
+  const CUtensorMapSwizzle swz = cols == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
+  cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
+  cuuint64_t strides[1] = {(cuuint64_t)a.ldd * 2};
+  cuuint32_t box[2] = {(cuuint32_t)cols, (cuuint32_t)IG_BM};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&tmD, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  tm.on_d = 1;
+  tm.d_cols = cols;
+  tm.d_swz = cols == 16 ? 1 : cols == 32 ? 3 : 7;
+}
+
 template <typename T, int MODE, int BN>
 static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   using Cfg = IgCfg<BN>;
@@ -889,8 +994,9 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
     grid = std::max(nt, grid / nt * nt);
   }
   IgTma tm;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmD;
   tma_plan<T, MODE, BN>(a, tm, tmA, tmB);
+  tma_out_plan<T, MODE, BN>(a, tm, tmD);
   {
     const dsp_conv_geom_t& g = a.geom;
     const uint32_t divs[5] = {(uint32_t)(MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q),
@@ -901,7 +1007,7 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
       fastdiv_host(divs[i], tm.fd_mul[i], tm.fd_shr[i]);
     }
   }
-  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tm);
+  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tmD, tm);
   (void)splits;
   note_launch();
   return cudaGetLastError();
