@@ -93,7 +93,7 @@ typedef struct {
                               per-CTA %globaltimer start/setup/work/end (4 slots per CTA from 192) */
 } dsp_igemm_args_t;
 
-#define DSP_IGEMM_MAX_CTAS 296
+#define DSP_IGEMM_MAX_CTAS 444
 
 /* Implicit-GEMM conv/dense on tcgen05 tensor cores (igemm.cu).  `splits` is the
  * WGRAD split-K factor (ignored otherwise). */

@@ -62,7 +62,7 @@ class IgemmArgs(C.Structure):
     ]
 
 
-IGEMM_MAX_CTAS = 296
+IGEMM_MAX_CTAS = 444
 
 
 class LayerDesc(C.Structure):

@@ -63,7 +63,10 @@ struct MmaTraits<float> {
 };
 
 #ifndef IG_STAGES_SMALL
-#define IG_STAGES_SMALL 5
+#define IG_STAGES_SMALL 3
+#endif
+#ifndef IG_STAGES_MID
+#define IG_STAGES_MID 2
 #endif
 #ifndef IG_REG_BLOCKS  // register budget as if this many CTAs shared an SM (headroom for other streams)
 #define IG_REG_BLOCKS 3
@@ -82,7 +85,7 @@ constexpr bool kTrace = false;
 
 template <int BN>
 struct IgCfg {
-  static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? 4 : 3);
+  static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 3);
   static constexpr int RING = STAGES * (IG_BM * 128 + BN * 128);
 #ifdef IG_TMA_STORE
   static constexpr int OUT_BYTES = IG_BM * BN * 2;  // bf16 output tile staged for the TMA store
@@ -92,7 +95,10 @@ struct IgCfg {
   static constexpr int SMEM = RING + OUT_BYTES;
   static constexpr int NACC = BN <= 128 ? 4 : 2;  // TMEM accumulators: MMA runs NACC-1 tiles ahead
   static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
-  static constexpr int CTAS_PER_SM = (SMEM <= 100 * 1024 && TMEM_COLS <= 256) ? IG_MAX_CTAS_PER_SM : 1;
+  static constexpr int BY_SMEM = SMEM <= 70 * 1024 ? 3 : SMEM <= 100 * 1024 ? 2 : 1;
+  static constexpr int BY_TMEM = 512 / TMEM_COLS;
+  static constexpr int CTAS_PER_SM = IG_MAX_CTAS_PER_SM < BY_SMEM ? (IG_MAX_CTAS_PER_SM < BY_TMEM ? IG_MAX_CTAS_PER_SM : BY_TMEM)
+                                                                  : (BY_SMEM < BY_TMEM ? BY_SMEM : BY_TMEM);
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
