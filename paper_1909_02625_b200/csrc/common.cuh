@@ -40,16 +40,16 @@ __device__ __forceinline__ bool last_cta_ticket(int* sem, int total, int* flag_s
 }
 
 // Fixed-order reduction of per-CTA partial rows part[b][2][N] (two statistics per column)
-// over columns [w0, w0 + cols), cols % 4 == 0, cols <= 512, by the first 256 threads:
+// over columns [w0, w0 + cols), cols % 4 == 0, cols <= 2 * NTH, by the first NTH threads:
 // thread = (part p, lane = (statistic, 4-column group)); a lane reads its float4 of rows
 // b = tile + (p + k * np) * nt (tile = column / BN: only those CTAs own the columns),
 // 8 rows in flight per batch, into fin4[256][4] (smem). part_sums_get() then adds the np
 // parts of one column in order. Deterministic: the assignment never depends on timing.
-template <int DEPTH = 8>
+template <int DEPTH = 8, int NTH = 256>
 __device__ __forceinline__ void part_sums_load(const float* part, int G, int N, int w0, int cols, int BN, int nt,
                                                double* fin4) {
   const int tid = threadIdx.x;
-  const int g4 = cols / 4, lanes = 2 * g4, np = 256 / lanes;
+  const int g4 = cols / 4, lanes = 2 * g4, np = NTH / lanes;
   if (tid >= np * lanes) return;
   const int ln = tid % lanes, p0 = tid / lanes;
   const int stat = ln / g4, c = w0 + (ln % g4) * 4;
@@ -74,8 +74,9 @@ __device__ __forceinline__ void part_sums_load(const float* part, int G, int N, 
 #pragma unroll
   for (int e = 0; e < 4; ++e) fin4[tid * 4 + e] = acc[e];
 }
+template <int NTH = 256>
 __device__ __forceinline__ void part_sums_get(const double* fin4, int cols, int cc, double& s1, double& s2) {
-  const int g4 = cols / 4, lanes = 2 * g4, np = 256 / lanes;
+  const int g4 = cols / 4, lanes = 2 * g4, np = NTH / lanes;
   s1 = 0.0;
   s2 = 0.0;
   for (int p = 0; p < np; ++p) {

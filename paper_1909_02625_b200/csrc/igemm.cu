@@ -43,9 +43,6 @@
 namespace dsp {
 
 constexpr int IG_BM = 128;
-constexpr int IG_THREADS = 288;
-constexpr int IG_MMA_WARP = 4;
-constexpr int IG_EPI_WARP0 = 5;
 
 template <typename T>
 struct MmaTraits;
@@ -174,13 +171,29 @@ static void fastdiv_host(uint32_t d, uint32_t& mul, uint32_t& shr) {
   shr = 31 + l - 32;
 }
 
-template <typename T, int MODE, int BN>
-__global__ void __launch_bounds__(IG_THREADS, IG_REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM ? IG_REG_BLOCKS
-                                                                                : IgCfg<BN>::CTAS_PER_SM)
+// Warp roles for NPW producer warps: 4 when operands are gathered with cp.async (128
+// threads), 1 when every operand comes through TMA (one lane issues the boxes).
+// Registers are budgeted as if REG_BLOCKS CTAs shared an SM, leaving room for the other
+// block streams' kernels beside a conv CTA (<= 75 regs at 288 threads, <= 68 at 192).
+template <int NPW>
+struct IgWarps {
+  static constexpr int THREADS = (NPW + 5) * 32;
+  static constexpr int MMA_WARP = NPW;
+  static constexpr int EPI_WARP0 = NPW + 1;
+  static constexpr int REG_BLOCKS = NPW == 4 ? IG_REG_BLOCKS : IG_REG_BLOCKS + 2;
+};
+
+template <typename T, int MODE, int BN, int NPW>
+__global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM
+                                                             ? IgWarps<NPW>::REG_BLOCKS
+                                                             : IgCfg<BN>::CTAS_PER_SM)
     igemm_kernel(const dsp_igemm_args_t a, const __grid_constant__ CUtensorMap tmA,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmD,
                  const IgTma tm) {
   using Cfg = IgCfg<BN>;
+  constexpr int IG_THREADS = IgWarps<NPW>::THREADS;
+  constexpr int IG_MMA_WARP = IgWarps<NPW>::MMA_WARP;
+  constexpr int IG_EPI_WARP0 = IgWarps<NPW>::EPI_WARP0;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NACC = Cfg::NACC;
   constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
@@ -274,7 +287,7 @@ __global__ void __launch_bounds__(IG_THREADS, IG_REG_BLOCKS > IgCfg<BN>::CTAS_PE
   const uint32_t sA0 = smem_u32(smem);
   const uint32_t sB0 = sA0 + STAGES * A_BYTES;
 
-  if (warp < 4) {
+  if (warp < NPW) {
     // =============================== producers ===============================
     // (all-TMA launches: only thread 0 produces; the other producer threads go idle)
     if (gather || warp == 0) {
@@ -760,23 +773,25 @@ __global__ void __launch_bounds__(IG_THREADS, IG_REG_BLOCKS > IgCfg<BN>::CTAS_PE
         // a lane reads its column group of every owning CTA's partial row as float4,
         // 8 rows in flight per batch; then a fixed-order sum over parts (deterministic).
         double* fin4 = reinterpret_cast<double*>(smem);  // operand ring is idle by now
-        for (int w0 = 0; w0 < N; w0 += 512) {
-          const int cols = min(512, N - w0);
-          part_sums_load<4>(a.stats, G, N, w0, cols, BN, nt, fin4);
+        constexpr int NTH = IG_THREADS >= 256 ? 256 : 128;  // threads of the load phase
+        for (int w0 = 0; w0 < N; w0 += 2 * NTH) {
+          const int cols = min(2 * NTH, N - w0);
+          part_sums_load<4, NTH>(a.stats, G, N, w0, cols, BN, nt, fin4);
           __syncthreads();
           if (kTrace && a.trace != nullptr && tid == 0 && w0 == 0) a.trace[187] = (int64_t)globaltimer_ns();
           for (int cc = tid; cc < cols; cc += IG_THREADS) {
             double s1, s2;
-            part_sums_get(fin4, cols, cc, s1, s2);
+            part_sums_get<NTH>(fin4, cols, cc, s1, s2);
             finish(w0 + cc, s1, s2);
           }
           __syncthreads();
         }
       } else {
         double(*fin)[2] = reinterpret_cast<double(*)[2]>(smem);
-        for (int cb = 0; cb < N; cb += 256) {
-          const int cols = min(256, N - cb);
-          const int parts = 256 / cols;
+        constexpr int NTH = IG_THREADS >= 256 ? 256 : 128;
+        for (int cb = 0; cb < N; cb += NTH) {
+          const int cols = min(NTH, N - cb);
+          const int parts = NTH / cols;
           if (tid < parts * cols) {
             const int c = cb + tid % cols, p = tid / cols;
             const int step = parts * nt;
@@ -982,7 +997,10 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   static int attr_state = 0;
   static int num_sms = 148;
   if (!attr_state) {
-    cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -994,7 +1012,8 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   const int nkb = (a.Kd + KS - 1) / KS;
   const int ns = MODE == DSP_IGEMM_WGRAD ? (nkb + a.kb_per_split - 1) / a.kb_per_split : 1;
   const int units = ((a.M + IG_BM - 1) / IG_BM) * ((a.N + BN - 1) / BN) * ns;
-  int grid = std::min(units, std::min(DSP_IGEMM_MAX_CTAS, num_sms * Cfg::CTAS_PER_SM));
+  static const int cap = getenv("DSP_B200_GRID_CAP") ? atoi(getenv("DSP_B200_GRID_CAP")) : DSP_IGEMM_MAX_CTAS;
+  int grid = std::min(units, std::min(cap, num_sms * Cfg::CTAS_PER_SM));
   if (MODE != DSP_IGEMM_WGRAD) {  // each CTA owns one n-tile: grid must be a multiple of nt
     const int nt = (a.N + BN - 1) / BN;
     grid = std::max(nt, grid / nt * nt);
@@ -1013,7 +1032,11 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
       fastdiv_host(divs[i], tm.fd_mul[i], tm.fd_shr[i]);
     }
   }
-  igemm_kernel<T, MODE, BN><<<grid, IG_THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tmD, tm);
+  static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
+  if (tm.on_a && tm.on_b && !force4)  // nothing to gather: one producer warp
+    igemm_kernel<T, MODE, BN, 1><<<grid, IgWarps<1>::THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tmD, tm);
+  else
+    igemm_kernel<T, MODE, BN, 4><<<grid, IgWarps<4>::THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tmD, tm);
   (void)splits;
   note_launch();
   return cudaGetLastError();
