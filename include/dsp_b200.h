@@ -66,6 +66,18 @@ typedef struct {
   int32_t R, S, stride, pad;
 } dsp_conv_geom_t;
 
+/* One BatchNorm whose backward statistics a DGRAD epilogue accumulates (see
+ * dsp_igemm_args_t.bnb): the BN sits below the conv whose input gradient the
+ * DGRAD produces, g = dX * (mask > 0) is its upstream gradient. */
+typedef struct {
+  const void* y;           /* the BN's input (conv output), storage dtype, same [M][ldd] layout as D */
+  const float* stat;       /* its forward statistics block: row 0 mean, row 1 invstd ([4][N]) */
+  const float* gamma;      /* [c_real] */
+  float* dgamma;           /* out [c_real]: sum g * xhat */
+  float* dbeta;            /* out [c_real]: sum g */
+  float* coef;             /* out [3][N]: gamma*invstd, mean(g), mean(g*xhat) (0 past c_real) */
+} dsp_bnb_target_t;
+
 typedef struct {
   dsp_conv_geom_t geom;
   int32_t M, N, Kd;        /* GEMM extents (see igemm.cu header comment) */
@@ -89,8 +101,17 @@ typedef struct {
   const float* gamma;
   const float* beta;
   int32_t* sem;
-  int64_t* trace;          /* optional profiling: clock64() stamps of CTA 0's pipeline events (slots 0..191), then
-                              per-CTA %globaltimer start/setup/work/end (4 slots per CTA from 192) */
+  int64_t* trace;          /* optional profiling (builds with -DIG_TRACE_BUILD only): clock64() stamps of CTA 0's
+                              pipeline events (slots 0..191), then per-CTA %globaltimer stamps (8 slots per CTA) */
+  /* DGRAD fused BatchNorm-backward statistics (optional; needs stats and sem):
+   * with g = stored dX * (bnb_mask > 0), per column the kernel accumulates sum g
+   * and sum g * xhat_t for each of bnb_count (1 or 2) BNs sharing g (stats rows:
+   * [CTA][1 + bnb_count][N]); the last CTA finalizes into bnb[t].dgamma / dbeta /
+   * coef, exactly what bn_bwd_stats writes, for channels < bnb_c_real. */
+  const void* bnb_mask;
+  int32_t bnb_count;
+  int32_t bnb_c_real;
+  dsp_bnb_target_t bnb[2];
 } dsp_igemm_args_t;
 
 #define DSP_IGEMM_MAX_CTAS 444

@@ -48,6 +48,11 @@ class ConvGeom(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("nimg", "H", "W", "C", "P", "Q", "K", "R", "S", "stride", "pad")]
 
 
+class BnbTarget(C.Structure):
+    _fields_ = [("y", C.c_void_p), ("stat", C.c_void_p), ("gamma", C.c_void_p), ("dgamma", C.c_void_p),
+                ("dbeta", C.c_void_p), ("coef", C.c_void_p)]
+
+
 class IgemmArgs(C.Structure):
     _fields_ = [
         ("geom", ConvGeom),
@@ -59,6 +64,8 @@ class IgemmArgs(C.Structure):
         ("n_valid", C.c_int32),
         ("stat_out", C.c_void_p), ("gamma", C.c_void_p), ("beta", C.c_void_p), ("sem", C.c_void_p),
         ("trace", C.c_void_p),
+        ("bnb_mask", C.c_void_p), ("bnb_count", C.c_int32), ("bnb_c_real", C.c_int32),
+        ("bnb", BnbTarget * 2),
     ]
 
 

@@ -169,7 +169,24 @@ int conv_wgrad(dsp_block* b, const ConvP& c, const void* x, const void* dy, cuda
   return DSP_OK;
 }
 
-int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const void* residual, cudaStream_t st) {
+// The BatchNorm below a DGRAD output whose backward statistics the DGRAD epilogue computes.
+struct BnbFuse {
+  const void* mask;  // ReLU mask tensor (the BN's stored output)
+  const ConvP* c1;   // the BN's conv (its y / stat / coef / gamma, beta grads)
+  const ConvP* c2;   // optional second BN sharing g (projection shortcut)
+};
+
+void set_bnb_target(dsp_block* b, const ConvP& c, dsp_bnb_target_t& t) {
+  t.y = b->ws + c.y;
+  t.stat = at<float>(b, c.stat);
+  t.gamma = b->params + c.gamma_off;
+  t.dgamma = b->grads + c.gamma_off;
+  t.dbeta = b->grads + c.beta_off;
+  t.coef = at<float>(b, c.coef);
+}
+
+int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const void* residual, cudaStream_t st,
+               const BnbFuse* fuse = nullptr) {
   dsp_igemm_args_t a{};
   a.geom = c.g;
   a.M = (int)c.Min();
@@ -181,7 +198,25 @@ int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const voi
   a.ldd = c.g.C;
   a.residual = residual;
   a.n_valid = c.ci_real;
+  if (fuse != nullptr) {
+    a.stats = at<float>(b, b->fpart);
+    a.sem = at<int32_t>(b, b->sem);
+    a.bnb_mask = fuse->mask;
+    a.bnb_count = fuse->c2 ? 2 : 1;
+    a.bnb_c_real = fuse->c1->co_real;
+    set_bnb_target(b, *fuse->c1, a.bnb[0]);
+    if (fuse->c2) set_bnb_target(b, *fuse->c2, a.bnb[1]);
+  }
   DSP_CUDA(igemm_launch(DSP_IGEMM_DGRAD, b->dtype, a, 1, st));
+  return DSP_OK;
+}
+
+// Second pass of the BN backward once its statistics (coef, dgamma, dbeta) exist.
+int bn_backward_apply(dsp_block* b, const void* gsrc, const void* mask, const ConvP& c1, void* dy1, const ConvP* c2,
+                      void* dy2, void* g_out, cudaStream_t st) {
+  DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, c1.coef), dy1,
+                        c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
+                        c2 ? at<float>(b, c2->coef) : nullptr, c2 ? dy2 : nullptr, g_out, c1.M(), c1.g.K, st));
   return DSP_OK;
 }
 
@@ -199,10 +234,7 @@ int bn_backward_pair(dsp_block* b, const void* gsrc, const void* mask, const Con
                           c2->co_real, b->params + c2->gamma_off, b->grads + c2->gamma_off, b->grads + c2->beta_off,
                           at<float>(b, c2->coef), sem, st));
   }
-  DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, c1.coef), dy1,
-                        c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
-                        c2 ? at<float>(b, c2->coef) : nullptr, c2 ? dy2 : nullptr, g_out, M, Cp, st));
-  return DSP_OK;
+  return bn_backward_apply(b, gsrc, mask, c1, dy1, c2, dy2, g_out, st);
 }
 
 // ------------------------------------------------------------------ layer forward / backward
@@ -334,10 +366,12 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
         const void* cin = i == 0 ? x : b->ws + (i == 1 ? l.z1 : l.z2);
         DSP_TRY(conv_wgrad(b, c, cin, S0, st));
         if (i == 0) break;
-        DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st));  // dz_{i}
+        // dz_{i}, with the BN-backward statistics of conv i-1 accumulated in the epilogue
         const ConvP& cb = l.convs[i - 1];
         const void* zmask = b->ws + (i == 1 ? l.z1 : l.z2);
-        DSP_TRY(bn_backward_pair(b, S2, zmask, cb, S0, nullptr, nullptr, nullptr, st));
+        const BnbFuse fuse{zmask, &cb, nullptr};
+        DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st, &fuse));
+        DSP_TRY(bn_backward_apply(b, S2, zmask, cb, S0, nullptr, nullptr, nullptr, st));
       }
       const void* res = S1;
       if (cs) {
@@ -504,7 +538,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       c.stat = pl.take((size_t)4 * c.g.K * 4);
       c.coef = pl.take((size_t)3 * c.g.K * 4);
       max_act = std::max(max_act, std::max(c.M() * c.g.K, c.Min() * c.g.C));
-      max_fpart = std::max<int64_t>(max_fpart, (int64_t)DSP_IGEMM_MAX_CTAS * 2 * c.g.K);
+      max_fpart = std::max<int64_t>(max_fpart, (int64_t)DSP_IGEMM_MAX_CTAS * 3 * std::max(c.g.K, c.g.C));
       max_bpart = std::max<int64_t>(max_bpart, (int64_t)bn_bwd_chunks(c.M(), c.g.K) * 2 * c.g.K);
       int kb = 1;
       const int sp = wgrad_splits(c, &kb, dtype);

@@ -39,17 +39,18 @@ __device__ __forceinline__ bool last_cta_ticket(int* sem, int total, int* flag_s
   return *flag_smem != 0;
 }
 
-// Fixed-order reduction of per-CTA partial rows part[b][2][N] (two statistics per column)
-// over columns [w0, w0 + cols), cols % 4 == 0, cols <= 2 * NTH, by the first NTH threads:
-// thread = (part p, lane = (statistic, 4-column group)); a lane reads its float4 of rows
-// b = tile + (p + k * np) * nt (tile = column / BN: only those CTAs own the columns),
-// 8 rows in flight per batch, into fin4[256][4] (smem). part_sums_get() then adds the np
-// parts of one column in order. Deterministic: the assignment never depends on timing.
+// Fixed-order reduction of per-CTA partial rows part[b][NS][N] (NS statistics per column)
+// over columns [w0, w0 + cols), cols % 4 == 0, NS * cols / 4 <= NTH, by the first NTH
+// threads: thread = (part p, lane = (statistic, 4-column group)); a lane reads its float4
+// of rows b = tile + (p + k * np) * nt (tile = column / BN: only those CTAs own the
+// columns), DEPTH rows in flight per batch, into fin4[NTH][4] (smem). part_sums_get()
+// then adds the np parts of one column in order. Deterministic: the assignment never
+// depends on timing.
 template <int DEPTH = 8, int NTH = 256>
-__device__ __forceinline__ void part_sums_load(const float* part, int G, int N, int w0, int cols, int BN, int nt,
-                                               double* fin4) {
+__device__ __forceinline__ void part_sums_load(const float* part, int G, int N, int NS, int w0, int cols, int BN,
+                                               int nt, double* fin4) {
   const int tid = threadIdx.x;
-  const int g4 = cols / 4, lanes = 2 * g4, np = NTH / lanes;
+  const int g4 = cols / 4, lanes = NS * g4, np = NTH / lanes;
   if (tid >= np * lanes) return;
   const int ln = tid % lanes, p0 = tid / lanes;
   const int stat = ln / g4, c = w0 + (ln % g4) * 4;
@@ -60,7 +61,7 @@ __device__ __forceinline__ void part_sums_load(const float* part, int G, int N, 
 #pragma unroll
     for (int e = 0; e < DEPTH; ++e) {
       const int b = b0 + e * np * nt;
-      v[e] = b < G ? __ldcg(reinterpret_cast<const float4*>(&part[((size_t)b * 2 + stat) * N + c]))
+      v[e] = b < G ? __ldcg(reinterpret_cast<const float4*>(&part[((size_t)b * NS + stat) * N + c]))
                    : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
@@ -75,15 +76,14 @@ __device__ __forceinline__ void part_sums_load(const float* part, int G, int N, 
   for (int e = 0; e < 4; ++e) fin4[tid * 4 + e] = acc[e];
 }
 template <int NTH = 256>
-__device__ __forceinline__ void part_sums_get(const double* fin4, int cols, int cc, double& s1, double& s2) {
-  const int g4 = cols / 4, lanes = 2 * g4, np = NTH / lanes;
-  s1 = 0.0;
-  s2 = 0.0;
-  for (int p = 0; p < np; ++p) {
-    s1 += fin4[(p * lanes + cc / 4) * 4 + (cc & 3)];
-    s2 += fin4[(p * lanes + g4 + cc / 4) * 4 + (cc & 3)];
-  }
+__device__ __forceinline__ double part_sums_get(const double* fin4, int NS, int cols, int cc, int stat) {
+  const int g4 = cols / 4, lanes = NS * g4, np = NTH / lanes;
+  double s = 0.0;
+  for (int p = 0; p < np; ++p) s += fin4[(p * lanes + stat * g4 + cc / 4) * 4 + (cc & 3)];
+  return s;
 }
+// widest column window part_sums_load can cover with NTH threads
+__host__ __device__ constexpr int part_sums_window(int NTH, int NS) { return NS <= 2 ? 2 * NTH : NTH; }
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

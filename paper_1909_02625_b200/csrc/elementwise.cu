@@ -211,12 +211,11 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
   double* fin4 = reinterpret_cast<double*>(&red[0][0]);
   for (int w0 = 0; w0 < Cp; w0 += 512) {
     const int cols = min(512, Cp - w0);
-    part_sums_load(part, (int)gridDim.x, Cp, w0, cols, Cp, 1, fin4);
+    part_sums_load(part, (int)gridDim.x, Cp, 2, w0, cols, Cp, 1, fin4);
     __syncthreads();
     for (int cc = tid; cc < cols; cc += kThreads) {
       const int c = w0 + cc;
-      double s1, s2;
-      part_sums_get(fin4, cols, cc, s1, s2);
+      const double s1 = part_sums_get(fin4, 2, cols, cc, 0), s2 = part_sums_get(fin4, 2, cols, cc, 1);
       const bool real = c < fin.c_real;
       if (real && fin.dbeta) fin.dbeta[c] = (float)s1;
       if (real && fin.dgamma && fin.gamma) fin.dgamma[c] = (float)s2;

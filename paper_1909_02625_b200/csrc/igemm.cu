@@ -135,6 +135,26 @@ __device__ __forceinline__ float colsum16(const float (&v)[16], int lane) {
   return w1;
 }
 
+// 16 consecutive columns [nb, nb + 16) of row m of a [M][ld] storage-dtype tensor as
+// floats (zeros for rows the tile does not own and columns >= N).
+template <typename T>
+__device__ __forceinline__ void ld_row16(const void* base, bool mok, int m, int ld, int nb, int N, float (&out)[16]) {
+  constexpr int EPC = 16 / (int)sizeof(T);
+  const T* p = reinterpret_cast<const T*>(base) + (size_t)m * ld + nb;
+  if (mok && nb + 16 <= N && (ld % EPC) == 0) {
+#pragma unroll
+    for (int qq = 0; qq < 16 / EPC; ++qq) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(p + qq * EPC);
+      const T* e8 = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) out[qq * EPC + e] = to_f<T>(e8[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) out[e] = (mok && nb + e < N) ? to_f<T>(p[e]) : 0.f;
+  }
+}
+
 // TMA configuration of one launch (host-decided, see tma_plan()).
 //   A (FPROP / stride-1 DGRAD): per k-block, 64/cbox boxes, one per (tap, channel
 //   chunk), each a 128-pixel im2col tile of cbox channels at tap-shifted
@@ -209,7 +229,8 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
   __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[NACC], tempty_bar[NACC];
   __shared__ uint32_t tmem_base_s;
   __shared__ int last_cta_s;
-  __shared__ float red[4][BN][2];
+  __shared__ float red[4][BN][3];
+  __shared__ float bst[2][2][BN];  // DGRAD BN-backward targets: mean / invstd of this CTA's columns
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -226,7 +247,11 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
   const int kbps = MODE == DSP_IGEMM_WGRAD ? a.kb_per_split : nkb_total;
   const int ns = MODE == DSP_IGEMM_WGRAD ? (nkb_total + kbps - 1) / kbps : 1;
   const int units = mt * nt * ns;
-  const bool want_stats = (MODE == DSP_IGEMM_FPROP) && a.stats != nullptr;
+  // FPROP: BatchNorm forward statistics of the output (sum, sum of squares).
+  // DGRAD: BatchNorm backward statistics of the layer below (sum g, sum g*xhat_t).
+  const bool bnb = MODE == DSP_IGEMM_DGRAD && a.bnb_count > 0;
+  const bool want_stats = a.stats != nullptr && (MODE == DSP_IGEMM_FPROP || bnb);
+  const int NS = MODE == DSP_IGEMM_FPROP ? 2 : 1 + a.bnb_count;  // statistics per column
 
   // Work assignment. FPROP/DGRAD: CTA c owns n-tile c % nt (so per-column BN
   // statistics can accumulate in registers) and m-tiles c/nt, c/nt + G/nt, ...
@@ -269,7 +294,16 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
   }
   if (warp == IG_MMA_WARP) tmem_alloc(&tmem_base_s, Cfg::TMEM_COLS);
   if (want_stats && warp >= IG_EPI_WARP0) {
-    for (int c = lane; c < BN; c += 32) red[warp & 3][c][0] = red[warp & 3][c][1] = 0.f;
+    for (int c = lane; c < BN; c += 32) red[warp & 3][c][0] = red[warp & 3][c][1] = red[warp & 3][c][2] = 0.f;
+    if (bnb && warp == IG_EPI_WARP0) {
+      const int n0c = (blockIdx.x % nt) * BN;  // the n-tile this CTA owns
+      for (int c = lane; c < BN; c += 32)
+        for (int t = 0; t < 2; ++t) {
+          const bool ok = t < a.bnb_count && n0c + c < N;
+          bst[t][0][c] = ok ? a.bnb[t].stat[n0c + c] : 0.f;
+          bst[t][1][c] = ok ? a.bnb[t].stat[N + n0c + c] : 0.f;
+        }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -696,7 +730,7 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
               }
             }
           }
-          if (want_stats) {
+          if (want_stats && MODE == DSP_IGEMM_FPROP) {
             float sq[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -708,6 +742,34 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
             if ((lane & 1) == 0) {  // this warp's private running sums (same n-tile every tile)
               red[q][cc * 16 + (lane >> 1)][0] += s1;
               red[q][cc * 16 + (lane >> 1)][1] += s2;
+            }
+          } else if (want_stats) {
+            // g = stored dX * (mask > 0); xhat_t = (y_t - mean_t) * invstd_t of the BN below
+            const int cl = cc * 16;  // column within the CTA's n-tile
+            float g[16], pr[16];
+            {
+              float mk[16];
+              ld_row16<T>(a.bnb_mask, mok, m, a.ldd, nb, N, mk);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) g[e] = mk[e] > 0.f ? v[e] : 0.f;
+            }
+            const float s1 = colsum16(g, lane);
+            float yv[16];
+            ld_row16<T>(a.bnb[0].y, mok, m, a.ldd, nb, N, yv);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pr[e] = g[e] * ((yv[e] - bst[0][0][cl + e]) * bst[0][1][cl + e]);
+            const float s2 = colsum16(pr, lane);
+            float s3 = 0.f;
+            if (a.bnb_count > 1) {
+              ld_row16<T>(a.bnb[1].y, mok, m, a.ldd, nb, N, yv);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pr[e] = g[e] * ((yv[e] - bst[1][0][cl + e]) * bst[1][1][cl + e]);
+              s3 = colsum16(pr, lane);
+            }
+            if ((lane & 1) == 0) {
+              red[q][cl + (lane >> 1)][0] += s1;
+              red[q][cl + (lane >> 1)][1] += s2;
+              red[q][cl + (lane >> 1)][2] += s3;
             }
           }
         }
@@ -732,8 +794,8 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       for (int c = et; c < BN; c += 128) {
         const int n = n0c + c;
         if (n < N) {
-          a.stats[((size_t)blockIdx.x * 2 + 0) * N + n] = (red[0][c][0] + red[1][c][0]) + (red[2][c][0] + red[3][c][0]);
-          a.stats[((size_t)blockIdx.x * 2 + 1) * N + n] = (red[0][c][1] + red[1][c][1]) + (red[2][c][1] + red[3][c][1]);
+          for (int k = 0; k < NS; ++k)
+            a.stats[((size_t)blockIdx.x * NS + k) * N + n] = (red[0][c][k] + red[1][c][k]) + (red[2][c][k] + red[3][c][k]);
         }
       }
     }
@@ -744,7 +806,7 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     __syncthreads();
     if (tid == 0) ctat[2] = (int64_t)globaltimer_ns();
   }
-  const bool fuse_fin = want_stats && a.stat_out != nullptr && a.sem != nullptr;
+  const bool fuse_fin = want_stats && a.sem != nullptr && (bnb || a.stat_out != nullptr);
   if (fuse_fin) {
     if (last_cta_ticket(a.sem, (int)gridDim.x, &last_cta_s, (a.out_f32 >> 8) & 3)) {
       if (kTrace && a.trace != nullptr && tid == 0) a.trace[186] = (int64_t)globaltimer_ns();
@@ -768,25 +830,43 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
         a.stat_out[2 * N + c] = scale;
         a.stat_out[3 * N + c] = shift;
       };
+      // DGRAD: what bn_bwd_stats' finalize writes, per target t (g shared)
+      auto finish_bnb = [&](int c, double sg, double sgx, int t) {
+        const dsp_bnb_target_t& tg = a.bnb[t];
+        const bool real = c < a.bnb_c_real;
+        if (real) {
+          tg.dbeta[c] = (float)sg;
+          tg.dgamma[c] = (float)sgx;
+        }
+        tg.coef[c] = real ? tg.gamma[c] * __ldcg(&tg.stat[N + c]) : 0.f;
+        tg.coef[N + c] = real ? (float)(sg / count) : 0.f;
+        tg.coef[2 * N + c] = real ? (float)(sgx / count) : 0.f;
+      };
       if ((N & 3) == 0) {
-        // One L2 round trip: 256 threads = (part, lane), lane = (statistic, 4-column group);
-        // a lane reads its column group of every owning CTA's partial row as float4,
-        // 8 rows in flight per batch; then a fixed-order sum over parts (deterministic).
+        // One L2 round trip per 4 rows: NTH threads = (part, lane), lane = (statistic,
+        // 4-column group) reading float4s of every owning CTA's partial row; then a
+        // fixed-order sum over parts (deterministic).
         double* fin4 = reinterpret_cast<double*>(smem);  // operand ring is idle by now
         constexpr int NTH = IG_THREADS >= 256 ? 256 : 128;  // threads of the load phase
-        for (int w0 = 0; w0 < N; w0 += 2 * NTH) {
-          const int cols = min(2 * NTH, N - w0);
-          part_sums_load<4, NTH>(a.stats, G, N, w0, cols, BN, nt, fin4);
+        const int win = part_sums_window(NTH, NS);
+        for (int w0 = 0; w0 < N; w0 += win) {
+          const int cols = min(win, N - w0);
+          part_sums_load<4, NTH>(a.stats, G, N, NS, w0, cols, BN, nt, fin4);
           __syncthreads();
           if (kTrace && a.trace != nullptr && tid == 0 && w0 == 0) a.trace[187] = (int64_t)globaltimer_ns();
           for (int cc = tid; cc < cols; cc += IG_THREADS) {
-            double s1, s2;
-            part_sums_get<NTH>(fin4, cols, cc, s1, s2);
-            finish(w0 + cc, s1, s2);
+            const double s1 = part_sums_get<NTH>(fin4, NS, cols, cc, 0);
+            const double s2 = part_sums_get<NTH>(fin4, NS, cols, cc, 1);
+            if (MODE == DSP_IGEMM_FPROP) {
+              finish(w0 + cc, s1, s2);
+            } else {
+              finish_bnb(w0 + cc, s1, s2, 0);
+              if (NS > 2) finish_bnb(w0 + cc, s1, part_sums_get<NTH>(fin4, NS, cols, cc, 2), 1);
+            }
           }
           __syncthreads();
         }
-      } else {
+      } else if (MODE == DSP_IGEMM_FPROP) {
         double(*fin)[2] = reinterpret_cast<double(*)[2]>(smem);
         constexpr int NTH = IG_THREADS >= 256 ? 256 : 128;
         for (int cb = 0; cb < N; cb += NTH) {
