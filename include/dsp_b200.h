@@ -197,6 +197,64 @@ int dsp_abi_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */
 int64_t dsp_launch_count(void);
 
+/* ------------------------------------------------------------ engine level
+ * The whole DSP train step behind one handle: the reference's
+ * TrainEngine(model, config, data, schedule, rule, beta, s, weight_decay) +
+ * run(n) + log (pipeline.py:451-606, 610-620, 664), single GPU, all K blocks
+ * on one device. The queue config is validated by the caller exactly as
+ * validate_config does (pipeline.py:85-128); dsp_create re-checks Eq.(5) and
+ * returns DSP_E_INVALID naming the first violated constraint. */
+#define DSP_MAX_BLOCKS 8
+#define DSP_WARMUP_FAITHFUL 0 /* "faithful_zero_updates" */
+#define DSP_WARMUP_DISCARD 1  /* "discard_warmup_updates" */
+
+typedef struct {
+  int32_t K;                      /* blocks, 1..DSP_MAX_BLOCKS */
+  int32_t p[DSP_MAX_BLOCKS];      /* forward queue delays (p[K-1] = 0) */
+  int32_t m[DSP_MAX_BLOCKS];      /* staleness per block (m[K-1] >= 0) */
+  int32_t warmup;                 /* DSP_WARMUP_* */
+  int32_t batch;                  /* B */
+  int32_t dtype;                  /* DSP_DTYPE_BF16 */
+  int32_t in_c, in_h, in_w;       /* one sample of the host batches, (C,H,W) flattened C-major */
+  int32_t num_classes;            /* labels must lie in [0, num_classes) */
+  int32_t n_layers[DSP_MAX_BLOCKS];
+  const dsp_layer_desc_t* layers; /* all blocks' layers back to back; param_offset relative to its block */
+  int32_t use_graphs;             /* replay each step as a CUDA graph once the zero prefill has drained */
+  int32_t device;                 /* CUDA device ordinal */
+} dsp_config_t;
+
+typedef struct {
+  int64_t step;         /* block step n */
+  int32_t block;
+  int32_t has_loss;     /* last block only */
+  int64_t batch_index;  /* stale tag n - cum_p[k] - m_k (negative: zero prefill packet) */
+  double loss;          /* mean cross-entropy of the stale batch (NaN unless has_loss) */
+  double grad_norm;     /* ||grad||_2 before weight decay (pipeline.py:602) */
+} dsp_log_record_t;
+
+typedef struct dsp_engine dsp_engine_t;
+
+int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out);
+/* Parameters of block k: n = param_count values, host float64 (on_device = 0,
+ * the reference's dtype) or device fp32 (on_device = 1). Resets the optimizer
+ * state of the block (ys_0 = x_0, optim.py:82). */
+int dsp_set_params(dsp_engine_t* eng, int k, const void* src, size_t n, int on_device);
+int dsp_get_params(dsp_engine_t* eng, int k, double* dst, size_t n);
+size_t dsp_param_count(dsp_engine_t* eng, int k);
+/* rule: DSP_RULE_SGD / DSP_RULE_SUM; lr(n) = base_lr * prod(factors[i] for decay_steps[i] <= n)
+ * (optim.py:38-45); wd couples into the gradient (pipeline.py:591-593). */
+int dsp_set_optimizer(dsp_engine_t* eng, int rule, double beta, double s, double wd, double base_lr,
+                      const int64_t* decay_steps, const double* factors, int n_decay);
+/* n_steps DSP steps. x: host float32 [n_steps][B][C*H*W], labels: host int64
+ * [n_steps][B] -- batch n of this call is the data stream's next batch. Each
+ * step copies its batch host->device and its loss / grad-norm row device->host
+ * (pinned, asynchronous); returns after the last step completed. */
+int dsp_run(dsp_engine_t* eng, int n_steps, const float* x, const int64_t* labels);
+/* Records of all steps so far, sorted by (step, block); *n = how many (<= cap written). */
+int dsp_read_log(dsp_engine_t* eng, dsp_log_record_t* recs, size_t cap, size_t* n);
+int64_t dsp_steps_done(dsp_engine_t* eng);
+void dsp_destroy(dsp_engine_t* eng);
+
 /* Step-graph execution (the engine's replacement for the reference's per-step
  * Python loop, pipeline.py:416-449).  graph: a captured cudaGraph_t; flags:
  * DSP_GRAPH_NODE_PRIORITY honours each kernel node's priority (inherited from the

@@ -33,6 +33,7 @@ from .blocks import (
     suggest_boundaries,
     tanh,
 )
+from .native import NativeEngine
 from .optim import LrSchedule, NonFiniteError, OptimizerState, apply_update, lr_at, sgd_step, sum_step
 from .pipeline import (
     ActivationPacket,
@@ -55,7 +56,7 @@ from .rng import SeededRng, derive_seed, mix64
 
 __all__ = [
     "ActivationPacket", "B200Unavailable", "Block", "ConfigError", "DeadlockError", "DspError", "GradPacket",
-    "LayerSpec", "LogRecord", "LrSchedule", "Model", "NonFiniteError", "OptimizerState", "PipelineConfig",
+    "LayerSpec", "LogRecord", "NativeEngine", "LrSchedule", "Model", "NonFiniteError", "OptimizerState", "PipelineConfig",
     "ProtocolError", "RuntimeStraggler", "SeededRng", "ShapeError", "StalenessProfile", "TrainEngine", "TrainLog",
     "apply_update", "avgpool", "basic_unit", "bottleneck", "build_model", "conv_bn_relu", "default_placement",
     "default_queue_config", "dense", "derive_seed", "flop_balanced_boundaries", "init_params", "lr_at", "maxpool",

@@ -14,6 +14,11 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("DSP_B200_LIB", Path(__file__).resolve().parent / "libdsp_b200.so"))
 
 DSP_DTYPE_BF16 = 0
+DSP_OK = 0
+DSP_E_INVALID = 1
+DSP_E_CUDA = 2
+DSP_E_STATE = 3
+DSP_E_NONFINITE = 4
 DSP_GRAPH_NODE_PRIORITY = 1
 DSP_DTYPE_F32 = 1
 
@@ -83,6 +88,29 @@ class LayerDesc(C.Structure):
     ]
 
 
+DSP_MAX_BLOCKS = 8
+DSP_WARMUP_FAITHFUL = 0
+DSP_WARMUP_DISCARD = 1
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [
+        ("K", C.c_int32),
+        ("p", C.c_int32 * DSP_MAX_BLOCKS), ("m", C.c_int32 * DSP_MAX_BLOCKS),
+        ("warmup", C.c_int32), ("batch", C.c_int32), ("dtype", C.c_int32),
+        ("in_c", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32),
+        ("num_classes", C.c_int32),
+        ("n_layers", C.c_int32 * DSP_MAX_BLOCKS),
+        ("layers", C.POINTER(LayerDesc)),
+        ("use_graphs", C.c_int32), ("device", C.c_int32),
+    ]
+
+
+class LogRecordC(C.Structure):
+    _fields_ = [("step", C.c_int64), ("block", C.c_int32), ("has_loss", C.c_int32), ("batch_index", C.c_int64),
+                ("loss", C.c_double), ("grad_norm", C.c_double)]
+
+
 # name -> (restype, argtypes); mirrors include/dsp_b200.h exactly
 _P = C.c_void_p
 _SIGNATURES = {
@@ -112,6 +140,16 @@ _SIGNATURES = {
     "dsp_graph_instantiate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "dsp_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsp_graph_destroy": (C.c_int, [C.c_void_p]),
+    "dsp_create": (C.c_int, [C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),
+    "dsp_set_params": (C.c_int, [_P, C.c_int, _P, C.c_size_t, C.c_int]),
+    "dsp_get_params": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.c_size_t]),
+    "dsp_param_count": (C.c_size_t, [_P, C.c_int]),
+    "dsp_set_optimizer": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_int]),
+    "dsp_run": (C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_int64)]),
+    "dsp_read_log": (C.c_int, [_P, C.POINTER(LogRecordC), C.c_size_t, C.POINTER(C.c_size_t)]),
+    "dsp_steps_done": (C.c_int64, [_P]),
+    "dsp_destroy": (None, [_P]),
 }
 
 _lib = None

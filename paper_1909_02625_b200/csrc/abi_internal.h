@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 #include "../../include/dsp_b200.h"
 
-#define DSP_ABI_VERSION 1
+#define DSP_ABI_VERSION 2
 
 namespace dsp {
 int set_error(int code, const char* fmt, ...);

@@ -1,0 +1,460 @@
+// The DSP train step behind one C handle (include/dsp_b200.h, "engine level").
+//
+// Native counterpart of the reference's TrainEngine serial backend
+// (/root/reference/pkg/src/stalepipe/pipeline.py:451-606 construction + _iterate_block,
+// 610-620 run, 664 log) for K blocks on one GPU, built on the block executor
+// (block.cu). The FIFOs are not materialised as queues: every packet lives in a
+// device ring slot chosen by the closed forms of SURVEY.md Appendix A --
+//   block k at step n: fresh tag n - cum_p[k], stale tag n - cum_p[k] - m_k;
+//   its fresh input is block k-1's output of step n - p_{k-1}, its stale input
+//   that of step n - m_k - p_{k-1}, its upstream gradient block k+1's input
+//   gradient of step n - q_{k+1}; a negative step means a zero prefill packet
+//   (pipeline.py:483-513, 524-528)
+// -- so the batch-tag protocol check of pipeline.py:567-572 holds by construction.
+// Ring depth R exceeds every packet lifetime, so from the step on which no zero
+// packet is read any more the device work of step n depends only on n mod R and
+// is captured once per phase into a CUDA graph (K blocks on forked streams) and
+// replayed; a phase is re-captured when its learning rates / update flags change.
+#include "abi_internal.h"
+#include "common.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+using dsp::set_error;
+
+struct Phase {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<double> lr;   // signature: per-block lr and update flag
+  std::vector<int> apply;
+};
+
+}  // namespace
+
+struct dsp_engine {
+  dsp_config_t cfg{};
+  int K = 0, B = 0, R = 0, D = 0;  // D = C*H*W of one input sample
+  int cum_p[DSP_MAX_BLOCKS + 1] = {};
+  int q[DSP_MAX_BLOCKS] = {};
+  int horizon = 0;
+  std::vector<dsp_layer_desc_t> layers;
+  dsp_block_t* blk[DSP_MAX_BLOCKS] = {};
+  int64_t nparam[DSP_MAX_BLOCKS] = {};
+  int64_t in_elems[DSP_MAX_BLOCKS] = {}, out_elems[DSP_MAX_BLOCKS] = {};
+  void* ws[DSP_MAX_BLOCKS] = {};
+  float* params[DSP_MAX_BLOCKS] = {};
+  float* grads[DSP_MAX_BLOCKS] = {};
+  float* ys[DSP_MAX_BLOCKS] = {};
+  bool ys_fresh[DSP_MAX_BLOCKS] = {};
+  // rings (slot = step mod R)
+  std::vector<void*> ring_out[DSP_MAX_BLOCKS], ring_gin[DSP_MAX_BLOCKS];
+  std::vector<void*> ring_in;
+  std::vector<int64_t*> ring_lab;
+  void* zero_act = nullptr;  // read-only zero packet (largest activation)
+  int64_t* zero_lab = nullptr;
+  float* xdev = nullptr;     // fp32 device staging of one batch
+  float* pin_x[2] = {};      // pinned host staging
+  int64_t* pin_l[2] = {};
+  cudaEvent_t pin_ev[2] = {};
+  float* slots = nullptr;    // [R][K][2] loss, grad_sq of the step in that phase
+  std::vector<float*> host_log;  // pinned chunks of LOG_CHUNK rows x K x 2
+  static constexpr int LOG_CHUNK = 4096;
+  // optimizer
+  int rule = DSP_RULE_SGD;
+  double beta = 0.0, s = 1.0, wd = 0.0, base_lr = 0.01;
+  std::vector<std::pair<int64_t, double>> decays;
+  // execution
+  cudaStream_t stream = nullptr;
+  cudaStream_t bstream[DSP_MAX_BLOCKS] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[DSP_MAX_BLOCKS] = {};
+  std::vector<Phase> phases;
+  int64_t steps = 0;  // steps done (all blocks advance together)
+};
+
+namespace {
+
+int check(cudaError_t e, const char* what) { return dsp::cuda_check(e, what); }
+#define ENG_CUDA(expr) DSP_TRY(check((expr), #expr))
+
+double lr_at(const dsp_engine* e, int64_t n) {
+  double lr = e->base_lr;
+  for (const auto& d : e->decays)
+    if (n >= d.first) lr *= d.second;
+  return lr;
+}
+
+int validate(const dsp_config_t& c) {
+  const int K = c.K;
+  if (K < 1 || K > DSP_MAX_BLOCKS) return set_error(DSP_E_INVALID, "dsp_create: K = %d outside [1, %d]", K, DSP_MAX_BLOCKS);
+  if (c.p[K - 1] != 0)
+    return set_error(DSP_E_INVALID, "ConfigError p_last_zero[%d]: p[%d] = %d must be 0", K - 1, K - 1, c.p[K - 1]);
+  for (int k = 0; k < K - 1; ++k)
+    if (c.p[k] <= 0) return set_error(DSP_E_INVALID, "ConfigError p_positive[%d]: p[%d] = %d must be > 0", k, k, c.p[k]);
+  for (int k = 0; k < K - 1; ++k)
+    if (c.m[k] <= 0) return set_error(DSP_E_INVALID, "ConfigError m_positive[%d]: m[%d] = %d must be > 0", k, k, c.m[k]);
+  if (c.m[K - 1] < 0)
+    return set_error(DSP_E_INVALID, "ConfigError m_last_nonneg[%d]: m[%d] = %d must be >= 0", K - 1, K - 1, c.m[K - 1]);
+  for (int k = 1; k < K; ++k) {
+    const int qk = c.m[k - 1] - c.p[k - 1] - c.m[k];
+    if (qk <= 0)
+      return set_error(DSP_E_INVALID, "ConfigError q_positive[%d]: q[%d] = m[%d]-p[%d]-m[%d] = %d-%d-%d = %d <= 0", k, k,
+                       k - 1, k - 1, k, c.m[k - 1], c.p[k - 1], c.m[k], qk);
+  }
+  if (c.warmup != DSP_WARMUP_FAITHFUL && c.warmup != DSP_WARMUP_DISCARD)
+    return set_error(DSP_E_INVALID, "dsp_create: unknown warmup policy %d", c.warmup);
+  if (c.batch <= 0 || c.in_c <= 0 || c.in_h <= 0 || c.in_w <= 0 || c.num_classes <= 0 || !c.layers)
+    return set_error(DSP_E_INVALID, "dsp_create: bad batch / input shape / classes / layers");
+  if (c.dtype != DSP_DTYPE_BF16) return set_error(DSP_E_INVALID, "dsp_create: only bf16 storage is supported");
+  for (int k = 0; k < K; ++k)
+    if (c.n_layers[k] <= 0) return set_error(DSP_E_INVALID, "dsp_create: block %d has no layers", k);
+  return DSP_OK;
+}
+
+template <typename T>
+int dmalloc(T** p, size_t bytes, bool zero = false) {
+  ENG_CUDA(cudaMalloc((void**)p, std::max<size_t>(bytes, 16)));
+  if (zero) ENG_CUDA(cudaMemset(*p, 0, std::max<size_t>(bytes, 16)));
+  return DSP_OK;
+}
+
+// device pointer of the packet block k reads at step n
+const void* fresh_in(const dsp_engine* e, int k, int64_t n) {
+  if (k == 0) return e->ring_in[n % e->R];
+  const int64_t src = n - e->cfg.p[k - 1];
+  return src >= 0 ? e->ring_out[k - 1][src % e->R] : e->zero_act;
+}
+const void* stale_in(const dsp_engine* e, int k, int64_t n) {
+  const int64_t f = n - e->cfg.m[k];  // the step this packet was fresh
+  if (f < 0) return e->zero_act;
+  return fresh_in(e, k, f);
+}
+const int64_t* stale_labels(const dsp_engine* e, int64_t n) {
+  const int64_t tag = n - e->cum_p[e->K - 1] - e->cfg.m[e->K - 1];
+  return tag >= 0 ? e->ring_lab[tag % e->R] : e->zero_lab;
+}
+const void* upstream(const dsp_engine* e, int k, int64_t n) {
+  const int64_t src = n - e->q[k + 1];
+  return src >= 0 ? e->ring_gin[k + 1][src % e->R] : e->zero_act;
+}
+bool apply_update(const dsp_engine* e, int k, int64_t n) {
+  const int64_t stale_tag = n - e->cum_p[k] - e->cfg.m[k];
+  return !(e->cfg.warmup == DSP_WARMUP_DISCARD && stale_tag < 0);
+}
+
+// Algorithm-2 body of block k at step n (pipeline.py:538-606) on stream st.
+int issue_block(dsp_engine* e, int k, int64_t n, cudaStream_t st) {
+  const int K = e->K;
+  const int ph = (int)(n % e->R);
+  float* loss_slot = e->slots + ((size_t)ph * K + k) * 2;
+  if (k < K - 1) {
+    DSP_TRY(dsp_block_forward(e->blk[k], fresh_in(e, k, n), e->ring_out[k][ph], 0, st));
+    DSP_TRY(dsp_block_forward(e->blk[k], stale_in(e, k, n), nullptr, 1, st));
+    DSP_TRY(dsp_block_backward(e->blk[k], upstream(e, k, n), k > 0 ? e->ring_gin[k][ph] : nullptr, st));
+  } else {
+    DSP_TRY(dsp_block_forward(e->blk[k], stale_in(e, k, n), nullptr, 1, st));
+    DSP_TRY(dsp_block_loss(e->blk[k], stale_labels(e, n), loss_slot, st));
+    DSP_TRY(dsp_block_backward(e->blk[k], nullptr, k > 0 ? e->ring_gin[k][ph] : nullptr, st));
+  }
+  const double lr = lr_at(e, n);
+  return dsp_block_update(e->blk[k], e->rule, e->ys[k], lr, e->s * lr, e->beta, e->wd, apply_update(e, k, n) ? 1 : 0,
+                          loss_slot + 1, st);
+}
+
+int issue_step(dsp_engine* e, int64_t n, bool forked) {
+  if (!forked) {
+    for (int k = 0; k < e->K; ++k) DSP_TRY(issue_block(e, k, n, e->stream));
+    return DSP_OK;
+  }
+  ENG_CUDA(cudaEventRecord(e->fork_ev, e->stream));
+  for (int k = 0; k < e->K; ++k) {
+    ENG_CUDA(cudaStreamWaitEvent(e->bstream[k], e->fork_ev, 0));
+    DSP_TRY(issue_block(e, k, n, e->bstream[k]));
+    ENG_CUDA(cudaEventRecord(e->join_ev[k], e->bstream[k]));
+  }
+  for (int k = 0; k < e->K; ++k) ENG_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev[k], 0));
+  return DSP_OK;
+}
+
+int run_step_device(dsp_engine* e, int64_t n) {
+  if (!e->cfg.use_graphs || n < e->horizon) return issue_step(e, n, false);
+  Phase& P = e->phases[n % e->R];
+  std::vector<double> lr(e->K);
+  std::vector<int> ap(e->K);
+  for (int k = 0; k < e->K; ++k) {
+    lr[k] = lr_at(e, n);
+    ap[k] = apply_update(e, k, n) ? 1 : 0;
+  }
+  if (P.exec == nullptr || P.lr != lr || P.apply != ap) {
+    if (P.exec != nullptr) {
+      ENG_CUDA(cudaGraphExecDestroy(P.exec));
+      P.exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    ENG_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = issue_step(e, n, true);
+    const cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+    if (rc != DSP_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    ENG_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiateWithFlags(&P.exec, g, 0);
+    cudaGraphDestroy(g);
+    ENG_CUDA(ie);
+    P.lr = lr;
+    P.apply = ap;
+  }
+  ENG_CUDA(cudaGraphLaunch(P.exec, e->stream));
+  return DSP_OK;
+}
+
+}  // namespace
+
+extern "C" int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out) {
+  if (!cfg || !out) return set_error(DSP_E_INVALID, "dsp_create: null argument");
+  DSP_TRY(validate(*cfg));
+  ENG_CUDA(cudaSetDevice(cfg->device));
+  dsp_engine* e = new dsp_engine();
+  *out = nullptr;
+  e->cfg = *cfg;
+  e->K = cfg->K;
+  e->B = cfg->batch;
+  e->D = cfg->in_c * cfg->in_h * cfg->in_w;
+  const int K = e->K;
+  int total_layers = 0;
+  for (int k = 0; k < K; ++k) total_layers += cfg->n_layers[k];
+  e->layers.assign(cfg->layers, cfg->layers + total_layers);
+  e->cfg.layers = e->layers.data();
+  for (int k = 0; k < K; ++k) e->cum_p[k + 1] = e->cum_p[k] + cfg->p[k];
+  e->q[0] = 0;
+  for (int k = 1; k < K; ++k) e->q[k] = cfg->m[k - 1] - cfg->p[k - 1] - cfg->m[k];
+  // ring depth: longer than every packet's lifetime in steps
+  int life = cfg->m[0] + 1;
+  for (int k = 0; k + 1 < K; ++k) life = std::max(life, cfg->p[k] + cfg->m[k + 1] + 1);
+  for (int k = 1; k < K; ++k) life = std::max(life, e->q[k] + 1);
+  life = std::max(life, e->cum_p[K - 1] + cfg->m[K - 1] + 1);  // labels of the last block's stale batch
+  e->R = life + 1;
+  int maxm = 0, maxp = 0, maxq = 0;
+  for (int k = 0; k < K; ++k) {
+    maxm = std::max(maxm, cfg->m[k]);
+    maxp = std::max(maxp, cfg->p[k]);
+    maxq = std::max(maxq, e->q[k]);
+  }
+  e->horizon = e->cum_p[K - 1] + maxm + maxp + maxq + 1;  // no zero packet is read from here on
+  auto fail = [&](int rc) {
+    dsp_destroy(e);
+    return rc;
+  };
+  int off = 0;
+  int64_t max_act = 0;
+  for (int k = 0; k < K; ++k) {
+    int rc = dsp_block_create(e->layers.data() + off, cfg->n_layers[k], e->B, cfg->dtype, k == K - 1, &e->blk[k]);
+    if (rc != DSP_OK) return fail(rc);
+    off += cfg->n_layers[k];
+    e->nparam[k] = dsp_block_param_count(e->blk[k]);
+    e->in_elems[k] = dsp_block_in_elems(e->blk[k]);
+    e->out_elems[k] = dsp_block_out_elems(e->blk[k]);
+    max_act = std::max({max_act, e->in_elems[k], k < K - 1 ? e->out_elems[k] : 0});
+    if ((rc = dmalloc(&e->ws[k], dsp_block_workspace_bytes(e->blk[k]))) != DSP_OK) return fail(rc);
+    if ((rc = dmalloc(&e->params[k], sizeof(float) * e->nparam[k], true)) != DSP_OK) return fail(rc);
+    if ((rc = dmalloc(&e->grads[k], sizeof(float) * e->nparam[k], true)) != DSP_OK) return fail(rc);
+    if ((rc = dmalloc(&e->ys[k], sizeof(float) * e->nparam[k], true)) != DSP_OK) return fail(rc);
+  }
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(DSP_E_CUDA);
+  for (int k = 0; k < K; ++k) {
+    if (cudaStreamCreateWithFlags(&e->bstream[k], cudaStreamNonBlocking) != cudaSuccess) return fail(DSP_E_CUDA);
+    if (cudaEventCreateWithFlags(&e->join_ev[k], cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
+    int rc = dsp_block_bind(e->blk[k], e->ws[k], e->params[k], e->grads[k], e->stream);
+    if (rc != DSP_OK) return fail(rc);
+  }
+  if (cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
+  const int R = e->R;
+  const size_t esz = 2;
+  int rc = DSP_OK;
+  for (int k = 0; k < K && rc == DSP_OK; ++k) {
+    if (k < K - 1) {
+      e->ring_out[k].resize(R);
+      for (int r = 0; r < R && rc == DSP_OK; ++r) rc = dmalloc(&e->ring_out[k][r], esz * e->out_elems[k], true);
+    }
+    if (k > 0) {
+      e->ring_gin[k].resize(R);
+      for (int r = 0; r < R && rc == DSP_OK; ++r) rc = dmalloc(&e->ring_gin[k][r], esz * e->in_elems[k], true);
+    }
+  }
+  e->ring_in.resize(R);
+  e->ring_lab.resize(R);
+  for (int r = 0; r < R && rc == DSP_OK; ++r) {
+    rc = dmalloc(&e->ring_in[r], esz * e->in_elems[0], true);
+    if (rc == DSP_OK) rc = dmalloc(&e->ring_lab[r], sizeof(int64_t) * e->B, true);
+  }
+  if (rc == DSP_OK) rc = dmalloc(&e->zero_act, esz * max_act, true);
+  if (rc == DSP_OK) rc = dmalloc(&e->zero_lab, sizeof(int64_t) * e->B, true);
+  if (rc == DSP_OK) rc = dmalloc(&e->xdev, sizeof(float) * (size_t)e->B * e->D);
+  if (rc == DSP_OK) rc = dmalloc(&e->slots, sizeof(float) * (size_t)R * K * 2, true);
+  for (int i = 0; i < 2 && rc == DSP_OK; ++i) {
+    rc = check(cudaMallocHost((void**)&e->pin_x[i], sizeof(float) * (size_t)e->B * e->D), "cudaMallocHost");
+    if (rc == DSP_OK) rc = check(cudaMallocHost((void**)&e->pin_l[i], sizeof(int64_t) * e->B), "cudaMallocHost");
+    if (rc == DSP_OK) rc = check(cudaEventCreateWithFlags(&e->pin_ev[i], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  if (rc != DSP_OK) return fail(rc);
+  e->phases.resize(R);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(set_error(DSP_E_CUDA, "dsp_create: device sync failed"));
+  *out = e;
+  return DSP_OK;
+}
+
+extern "C" size_t dsp_param_count(dsp_engine_t* e, int k) {
+  return (e && k >= 0 && k < e->K) ? (size_t)e->nparam[k] : 0;
+}
+
+extern "C" int dsp_set_params(dsp_engine_t* e, int k, const void* src, size_t n, int on_device) {
+  if (!e || k < 0 || k >= e->K || !src) return set_error(DSP_E_INVALID, "dsp_set_params: bad arguments");
+  if ((int64_t)n != e->nparam[k])
+    return set_error(DSP_E_INVALID, "dsp_set_params: block %d has %lld params, got %zu", k, (long long)e->nparam[k], n);
+  if (on_device) {
+    ENG_CUDA(cudaMemcpyAsync(e->params[k], src, sizeof(float) * n, cudaMemcpyDeviceToDevice, e->stream));
+  } else {
+    std::vector<float> f(n);
+    const double* d = static_cast<const double*>(src);
+    for (size_t i = 0; i < n; ++i) f[i] = (float)d[i];
+    ENG_CUDA(cudaMemcpyAsync(e->params[k], f.data(), sizeof(float) * n, cudaMemcpyHostToDevice, e->stream));
+    ENG_CUDA(cudaStreamSynchronize(e->stream));
+  }
+  // optimizer state follows the parameters (OptimizerState.for_params: ys_0 = x_0)
+  ENG_CUDA(cudaMemcpyAsync(e->ys[k], e->params[k], sizeof(float) * n, cudaMemcpyDeviceToDevice, e->stream));
+  DSP_TRY(dsp_block_pack(e->blk[k], e->stream));
+  ENG_CUDA(cudaStreamSynchronize(e->stream));
+  return DSP_OK;
+}
+
+extern "C" int dsp_get_params(dsp_engine_t* e, int k, double* dst, size_t n) {
+  if (!e || k < 0 || k >= e->K || !dst) return set_error(DSP_E_INVALID, "dsp_get_params: bad arguments");
+  if ((int64_t)n != e->nparam[k])
+    return set_error(DSP_E_INVALID, "dsp_get_params: block %d has %lld params, got %zu", k, (long long)e->nparam[k], n);
+  std::vector<float> f(n);
+  ENG_CUDA(cudaMemcpyAsync(f.data(), e->params[k], sizeof(float) * n, cudaMemcpyDeviceToHost, e->stream));
+  ENG_CUDA(cudaStreamSynchronize(e->stream));
+  for (size_t i = 0; i < n; ++i) dst[i] = f[i];
+  return DSP_OK;
+}
+
+extern "C" int dsp_set_optimizer(dsp_engine_t* e, int rule, double beta, double s, double wd, double base_lr,
+                                 const int64_t* decay_steps, const double* factors, int n_decay) {
+  if (!e) return set_error(DSP_E_INVALID, "dsp_set_optimizer: null engine");
+  if (rule != DSP_RULE_SGD && rule != DSP_RULE_SUM) return set_error(DSP_E_INVALID, "dsp_set_optimizer: bad rule %d", rule);
+  if (n_decay < 0 || (n_decay > 0 && (!decay_steps || !factors)))
+    return set_error(DSP_E_INVALID, "dsp_set_optimizer: bad decay list");
+  e->rule = rule;
+  e->beta = beta;
+  e->s = s;
+  e->wd = wd;
+  e->base_lr = base_lr;
+  e->decays.clear();
+  for (int i = 0; i < n_decay; ++i) e->decays.push_back({decay_steps[i], factors[i]});
+  for (auto& P : e->phases)  // captured steps baked the old constants in
+    if (P.exec) {
+      cudaGraphExecDestroy(P.exec);
+      P.exec = nullptr;
+    }
+  return DSP_OK;
+}
+
+extern "C" int dsp_run(dsp_engine_t* e, int n_steps, const float* x, const int64_t* labels) {
+  if (!e || n_steps < 0 || (n_steps > 0 && (!x || !labels))) return set_error(DSP_E_INVALID, "dsp_run: bad arguments");
+  const size_t xb = sizeof(float) * (size_t)e->B * e->D, lb = sizeof(int64_t) * e->B;
+  for (int i = 0; i < n_steps; ++i) {
+    const int64_t n = e->steps;
+    const int64_t* lab = labels + (size_t)i * e->B;
+    for (int b = 0; b < e->B; ++b)
+      if (lab[b] < 0 || lab[b] >= e->cfg.num_classes)
+        return set_error(DSP_E_INVALID, "dsp_run: label out of range [0, %d) at step %lld", e->cfg.num_classes,
+                         (long long)n);
+    // batch n: host -> pinned slot -> device staging -> packed bf16 ring slot (block 0's input)
+    const int pi = (int)(n & 1);
+    ENG_CUDA(cudaEventSynchronize(e->pin_ev[pi]));  // the H2D that last read this pinned slot is done
+    memcpy(e->pin_x[pi], x + (size_t)i * e->B * e->D, xb);
+    memcpy(e->pin_l[pi], lab, lb);
+    const int slot = (int)(n % e->R);
+    ENG_CUDA(cudaMemcpyAsync(e->xdev, e->pin_x[pi], xb, cudaMemcpyHostToDevice, e->stream));
+    ENG_CUDA(cudaMemcpyAsync(e->ring_lab[slot], e->pin_l[pi], lb, cudaMemcpyHostToDevice, e->stream));
+    ENG_CUDA(cudaEventRecord(e->pin_ev[pi], e->stream));
+    DSP_TRY(dsp_pack_input(e->xdev, e->ring_in[slot], e->B, e->cfg.in_c, e->cfg.in_h, e->cfg.in_w,
+                           (e->cfg.in_c + 7) / 8 * 8, e->cfg.dtype, 1, e->stream));
+    DSP_TRY(run_step_device(e, n));
+    // the step's loss / grad-norm row -> pinned host log (asynchronous)
+    const int64_t row = n;
+    if (row / dsp_engine::LOG_CHUNK >= (int64_t)e->host_log.size()) {
+      float* chunk = nullptr;
+      ENG_CUDA(cudaMallocHost((void**)&chunk, sizeof(float) * dsp_engine::LOG_CHUNK * e->K * 2));
+      e->host_log.push_back(chunk);
+    }
+    float* dst = e->host_log[row / dsp_engine::LOG_CHUNK] + (row % dsp_engine::LOG_CHUNK) * e->K * 2;
+    ENG_CUDA(cudaMemcpyAsync(dst, e->slots + (size_t)slot * e->K * 2, sizeof(float) * e->K * 2,
+                             cudaMemcpyDeviceToHost, e->stream));
+    e->steps = n + 1;
+  }
+  ENG_CUDA(cudaStreamSynchronize(e->stream));
+  return DSP_OK;
+}
+
+extern "C" int64_t dsp_steps_done(dsp_engine_t* e) { return e ? e->steps : -1; }
+
+extern "C" int dsp_read_log(dsp_engine_t* e, dsp_log_record_t* recs, size_t cap, size_t* n) {
+  if (!e || !n || (cap > 0 && !recs)) return set_error(DSP_E_INVALID, "dsp_read_log: bad arguments");
+  ENG_CUDA(cudaStreamSynchronize(e->stream));
+  const size_t total = (size_t)e->steps * e->K;
+  *n = total;
+  size_t w = 0;
+  for (int64_t s = 0; s < e->steps && w < cap; ++s) {
+    const float* row = e->host_log[s / dsp_engine::LOG_CHUNK] + (s % dsp_engine::LOG_CHUNK) * e->K * 2;
+    for (int k = 0; k < e->K && w < cap; ++k, ++w) {
+      dsp_log_record_t& r = recs[w];
+      r.step = s;
+      r.block = k;
+      r.batch_index = s - e->cum_p[k] - e->cfg.m[k];
+      r.has_loss = k == e->K - 1;
+      r.loss = r.has_loss ? (double)row[k * 2] : NAN;
+      r.grad_norm = std::sqrt((double)row[k * 2 + 1]);
+    }
+  }
+  return DSP_OK;
+}
+
+extern "C" void dsp_destroy(dsp_engine_t* e) {
+  if (!e) return;
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  for (auto& P : e->phases)
+    if (P.exec) cudaGraphExecDestroy(P.exec);
+  for (int k = 0; k < DSP_MAX_BLOCKS; ++k) {
+    if (e->blk[k]) dsp_block_destroy(e->blk[k]);
+    cudaFree(e->ws[k]);
+    cudaFree(e->params[k]);
+    cudaFree(e->grads[k]);
+    cudaFree(e->ys[k]);
+    for (void* p : e->ring_out[k]) cudaFree(p);
+    for (void* p : e->ring_gin[k]) cudaFree(p);
+    if (e->bstream[k]) cudaStreamDestroy(e->bstream[k]);
+    if (e->join_ev[k]) cudaEventDestroy(e->join_ev[k]);
+  }
+  for (void* p : e->ring_in) cudaFree(p);
+  for (int64_t* p : e->ring_lab) cudaFree(p);
+  cudaFree(e->zero_act);
+  cudaFree(e->zero_lab);
+  cudaFree(e->xdev);
+  cudaFree(e->slots);
+  for (int i = 0; i < 2; ++i) {
+    if (e->pin_x[i]) cudaFreeHost(e->pin_x[i]);
+    if (e->pin_l[i]) cudaFreeHost(e->pin_l[i]);
+    if (e->pin_ev[i]) cudaEventDestroy(e->pin_ev[i]);
+  }
+  for (float* c : e->host_log) cudaFreeHost(c);
+  if (e->fork_ev) cudaEventDestroy(e->fork_ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}

@@ -38,7 +38,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_declared_symbol(lib):
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.dsp_abi_version() == 1
+    assert lib.dsp_abi_version() == 2
     assert lib.dsp_launch_count() >= 0
 
 
@@ -91,3 +91,25 @@ def test_engine_without_gpu_fails_loudly():
     batches = iter([(torch.zeros(2, 4).numpy(), torch.zeros(2, dtype=torch.int64).numpy())] * 3)
     with pytest.raises(P.B200Unavailable):
         P.TrainEngine(m, P.validate_config((0,), (0,)), batches, P.LrSchedule(0.1))
+
+
+def test_engine_create_validates_queue_config_on_host(lib):
+    """dsp_create checks Eq.(5) (pipeline.py:85-128) before touching the device."""
+    layers = [P.dense(12, 8), P.relu(), P.dense(8, 4)]
+    m = P.build_model(layers, [2])
+    descs = [blk.layer_descs() for blk in m.blocks]
+    flat = (L.LayerDesc * sum(len(d) for d in descs))(*[e for d in descs for e in d])
+    cases = [((1, 1), (1, 0), "p_last_zero"), ((0, 0), (1, 0), "p_positive"), ((1, 0), (0, 0), "m_positive"),
+             ((1, 0), (1, -1), "m_last_nonneg"), ((1, 0), (1, 1), "q_positive")]
+    for p, mm, name in cases:
+        cfg = L.EngineConfig()
+        cfg.K = 2
+        for k in range(2):
+            cfg.p[k], cfg.m[k] = p[k], mm[k]
+            cfg.n_layers[k] = len(descs[k])
+        cfg.batch, cfg.dtype, cfg.in_c, cfg.in_h, cfg.in_w, cfg.num_classes = 4, L.DSP_DTYPE_BF16, 12, 1, 1, 4
+        cfg.layers = C.cast(flat, C.POINTER(L.LayerDesc))
+        h = C.c_void_p()
+        assert lib.dsp_create(C.byref(cfg), C.byref(h)) == L.DSP_E_INVALID
+        assert name in lib.dsp_last_error().decode()
+        assert not h.value

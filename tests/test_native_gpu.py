@@ -1,0 +1,124 @@
+"""Engine-level C-ABI (dsp_create / dsp_run / dsp_read_log, csrc/engine.cu) vs the
+Python-orchestrated TrainEngine(backend b200) and the oracle.
+
+Both engines run the same block kernels in the same per-block order, so the
+native engine must reproduce the Python engine's TrainLog checksum and final
+parameters bit for bit -- eager and CUDA-graph steps, lr decay (graph
+re-capture), both warmup policies, both update rules. Against the oracle the
+tolerances of tests/test_engine_gpu.py apply.
+"""
+
+import numpy as np
+import pytest
+
+import oracle.dsp_ref as R
+import paper_1909_02625_b200 as P
+from paper_1909_02625_b200.native import NativeEngine
+from tests.gpu_util import small_resnet, twin_models
+from tests.test_engine_gpu import _check
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(layers, bounds, p, m, B, steps, in_shape, classes, rule="sum", beta=0.9, lr=0.05, wd=0.0,
+          warmup="faithful_zero_updates", decay=True):
+    pool = R.synthetic_batches(6, B, in_shape, classes, seed=1)
+    sched = P.LrSchedule(lr, ((steps // 2, 0.5),) if decay else ())
+    cfg = P.validate_config(p, m, warmup=warmup)
+    pm, _ = twin_models(layers, bounds, seed=3)
+    py = P.TrainEngine(pm, cfg, R.cycle(pool), sched, rule=rule, beta=beta, weight_decay=wd)
+    py.run(steps)
+    nm, _ = twin_models(layers, bounds, seed=3)
+    ne = NativeEngine(nm, cfg, B, sched, rule=rule, beta=beta, weight_decay=wd)
+    ne.run(steps, R.cycle(pool))
+    return py, pm, ne, pool, sched, cfg
+
+
+def _same(py, pm, ne):
+    assert ne.log.index_checksum() == py.log.index_checksum()
+    assert ne.log.checksum() == py.log.checksum()
+    for k, blk in enumerate(pm.blocks):
+        assert np.array_equal(ne.params(k), blk.params), k
+
+
+def test_k4_default_queues_graphs_match_python_engine():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    cfg = P.default_queue_config(4)
+    py, pm, ne, *_ = _pair(layers, [1, 2, 3], cfg.p, cfg.m, 8, 24, (3, 8, 8), 10)
+    _same(py, pm, ne)
+    assert ne.realized_staleness() == list(cfg.m)
+
+
+def test_k3_discard_sgd_wd_matches_python_engine():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    py, pm, ne, *_ = _pair(layers, [2, 4], (1, 1, 0), (4, 2, 0), 8, 16, (3, 8, 8), 10, rule="sgd", beta=0.0,
+                           wd=5e-4, warmup="discard_warmup_updates")
+    _same(py, pm, ne)
+
+
+def test_k1_plain_bp_matches_python_engine():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    py, pm, ne, *_ = _pair(layers, [], (0,), (0,), 16, 10, (3, 8, 8), 10, rule="sgd", beta=0.0)
+    _same(py, pm, ne)
+
+
+def test_mlp_against_oracle():
+    layers = [P.dense(12, 16), P.relu(), P.dense(16, 12), P.relu(), P.dense(12, 4)]
+    p, m = (1, 1, 0), (4, 2, 0)
+    steps, B = 30, 16
+    pool = R.synthetic_batches(6, B, (12, 1, 1), 4, seed=1)
+    sched = ((steps // 2, 0.5),)
+    nm, _ = twin_models(layers, [2, 4], seed=3)
+    ne = NativeEngine(nm, P.validate_config(p, m), B, P.LrSchedule(0.05, sched), rule="sum", beta=0.9)
+    ne.run(steps, R.cycle(pool))
+    refs = {}
+    for mode in ("bf16", "f64"):
+        with R.storage(mode):
+            _, om = twin_models(layers, [2, 4], seed=3)
+            ref = R.Engine(om, R.validate_config(p, m), R.cycle(pool), R.LrSchedule(0.05, sched), rule="sum",
+                           beta=0.9)
+            ref.run(steps)
+        refs[mode] = (ref, om)
+
+    class _Eng:  # adapter: _check reads .log and .realized_staleness()
+        log = ne.log
+
+        @staticmethod
+        def realized_staleness():
+            return ne.realized_staleness()
+
+    for k, blk in enumerate(nm.blocks):
+        blk.params = ne.params(k)
+    _check(_Eng, nm, refs, m)
+
+
+def test_run_in_chunks_equals_one_call():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    cfg = P.default_queue_config(3)
+    pool = R.synthetic_batches(5, 8, (3, 8, 8), 10, seed=2)
+    xs = np.stack([x for x, _ in pool] * 4)[:18]
+    ls = np.stack([lab for _, lab in pool] * 4)[:18]
+    outs = []
+    for chunks in ((18,), (5, 13)):
+        nm, _ = twin_models(layers, [1, 3], seed=2)
+        ne = NativeEngine(nm, cfg, 8, P.LrSchedule(0.05, ((9, 0.1),)), rule="sum", beta=0.9)
+        i = 0
+        for c in chunks:
+            ne.run_batches(xs[i:i + c], ls[i:i + c])
+            i += c
+        outs.append((ne.log.checksum(), [ne.params(k) for k in range(3)]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_label_out_of_range_and_config_errors():
+    layers = [P.dense(12, 8), P.relu(), P.dense(8, 4)]
+    nm, _ = twin_models(layers, [], seed=1)
+    ne = NativeEngine(nm, P.validate_config((0,), (0,)), 4, P.LrSchedule(0.1))
+    with pytest.raises(P.DspError, match="label out of range"):
+        ne.run_batches(np.zeros((1, 4, 12)), np.array([[0, 1, 2, 4]]))
+    bad = P.PipelineConfig(2, (1, 0), (1, 1), (0, -1), "faithful_zero_updates", True)
+    nm2, _ = twin_models(layers, [2], seed=1)
+    with pytest.raises(P.DspError, match="q_positive"):
+        NativeEngine(nm2, bad, 4, P.LrSchedule(0.1))
