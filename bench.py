@@ -320,32 +320,56 @@ def run_b200(args):
         losses = [lv for _, lv in log.losses()]
         loss_ok = all(np.isfinite(losses))
 
-    # ---- end to end through the public API: host batches (pinned H2D each step) + D2H loss read
+    # ---- end to end through the public API with HOST buffers. One GPU: the engine-level
+    # C-ABI (dsp_run via NativeEngine) -- every step copies its batch host->device (pinned)
+    # and its loss / grad-norm row device->host inside the timed region. N GPUs: the
+    # Python-orchestrated TrainEngine on host batches with a per-step loss read.
     e2e = None
     if not args.no_e2e:
         model2 = P.build_model(layers, bounds)
         P.init_params(model2, 0)
-        eng2 = P.TrainEngine(model2, cfg, cycle(host_pool), P.LrSchedule(0.1), rule="sum", beta=0.9, s=1.0,
-                             weight_decay=5e-4, device=dev)
-        for _ in range(warm):
-            eng2.run(1)
-            eng2.last_loss()
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            eng2.run(1)
-            eng2.last_loss()  # device->host read of the step's result
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        tt = torch.tensor([el], device=dev)
-        if world > 1:
+        if world == 1:
+            from paper_1909_02625_b200.native import NativeEngine
+
+            eng2 = NativeEngine(model2, cfg, args.batch, P.LrSchedule(0.1), rule="sum", beta=0.9, s=1.0,
+                                weight_decay=5e-4, device=dev.index)
+            xs = np.stack([np.asarray(x, dtype=np.float32) for x, _ in host_pool])
+            ls = np.stack([np.asarray(lab, dtype=np.int64) for _, lab in host_pool])
+            warm2 = max(warm, eng2.horizon + eng2.ring + 1)  # every graph phase captured before timing
+            sel = np.arange(warm2 + args.steps) % len(host_pool)
+            xw, lw = xs[sel[:warm2]], ls[sel[:warm2]]
+            xt, lt = np.ascontiguousarray(xs[sel[warm2:]]), np.ascontiguousarray(ls[sel[warm2:]])
+            eng2.run_batches(xw, lw)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng2.run_batches(xt, lt)  # returns after the last step (and its D2H row) completed
+            el = time.perf_counter() - t0
+            h2d = int(xt[0].nbytes + lt[0].nbytes)
+            d2h = 4 * 2 * K
+            how = ("host wall clock around dsp_run (engine C-ABI): per step pinned H2D of the fp32 batch + labels "
+                   "and async D2H of the step's loss/grad-norm row; graphs replayed natively")
+        else:
+            eng2 = P.TrainEngine(model2, cfg, cycle(host_pool), P.LrSchedule(0.1), rule="sum", beta=0.9, s=1.0,
+                                 weight_decay=5e-4, device=dev)
+            for _ in range(warm):
+                eng2.run(1)
+                eng2.last_loss()
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                eng2.run(1)
+                eng2.last_loss()  # device->host read of the step's result
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            tt = torch.tensor([el], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        el = float(tt.item())
-        h2d = args.batch * int(np.prod(IN_SHAPE)) * 4 + args.batch * 8 if 0 in eng2.local else 0
-        d2h = 4 if (K - 1) in eng2.local else 0
+            el = float(tt.item())
+            h2d = args.batch * int(np.prod(IN_SHAPE)) * 4 + args.batch * 8 if 0 in eng2.local else 0
+            d2h = 4 if (K - 1) in eng2.local else 0
+            how = "host wall clock incl. pinned H2D + per-step loss D2H (Python engine, one rank per GPU)"
         e2e = {"value": args.batch * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "timing": "host wall clock incl. pinned H2D + per-step loss D2H"}
+               "d2h_bytes_per_step": d2h, "timing": how}
         del eng2, model2
 
     roof = kernel_roofline(torch, peaks, args.batch) if rank == 0 else None

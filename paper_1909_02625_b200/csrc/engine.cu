@@ -58,10 +58,14 @@ struct dsp_engine {
   std::vector<int64_t*> ring_lab;
   void* zero_act = nullptr;  // read-only zero packet (largest activation)
   int64_t* zero_lab = nullptr;
-  float* xdev = nullptr;     // fp32 device staging of one batch
-  float* pin_x[2] = {};      // pinned host staging
+  // input staging, double-buffered: batch n goes pinned host -> xdev[n&1] -> ring slot on
+  // the copy stream, overlapping step n-1's compute
+  float* xdev[2] = {};
+  float* pin_x[2] = {};
   int64_t* pin_l[2] = {};
-  cudaEvent_t pin_ev[2] = {};
+  cudaEvent_t pin_ev[2] = {};   // copy of batch n done (pinned slot and xdev[n&1] free again)
+  cudaEvent_t step_ev[2] = {};  // step n done
+  cudaStream_t copy_stream = nullptr;
   float* slots = nullptr;    // [R][K][2] loss, grad_sq of the step in that phase
   std::vector<float*> host_log;  // pinned chunks of LOG_CHUNK rows x K x 2
   static constexpr int LOG_CHUNK = 4096;
@@ -295,13 +299,15 @@ extern "C" int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out) {
   }
   if (rc == DSP_OK) rc = dmalloc(&e->zero_act, esz * max_act, true);
   if (rc == DSP_OK) rc = dmalloc(&e->zero_lab, sizeof(int64_t) * e->B, true);
-  if (rc == DSP_OK) rc = dmalloc(&e->xdev, sizeof(float) * (size_t)e->B * e->D);
+  for (int i = 0; i < 2 && rc == DSP_OK; ++i) rc = dmalloc(&e->xdev[i], sizeof(float) * (size_t)e->B * e->D);
   if (rc == DSP_OK) rc = dmalloc(&e->slots, sizeof(float) * (size_t)R * K * 2, true);
   for (int i = 0; i < 2 && rc == DSP_OK; ++i) {
     rc = check(cudaMallocHost((void**)&e->pin_x[i], sizeof(float) * (size_t)e->B * e->D), "cudaMallocHost");
     if (rc == DSP_OK) rc = check(cudaMallocHost((void**)&e->pin_l[i], sizeof(int64_t) * e->B), "cudaMallocHost");
     if (rc == DSP_OK) rc = check(cudaEventCreateWithFlags(&e->pin_ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    if (rc == DSP_OK) rc = check(cudaEventCreateWithFlags(&e->step_ev[i], cudaEventDisableTiming), "cudaEventCreate");
   }
+  if (rc == DSP_OK) rc = check(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   if (rc != DSP_OK) return fail(rc);
   e->phases.resize(R);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(set_error(DSP_E_CUDA, "dsp_create: device sync failed"));
@@ -375,17 +381,21 @@ extern "C" int dsp_run(dsp_engine_t* e, int n_steps, const float* x, const int64
       if (lab[b] < 0 || lab[b] >= e->cfg.num_classes)
         return set_error(DSP_E_INVALID, "dsp_run: label out of range [0, %d) at step %lld", e->cfg.num_classes,
                          (long long)n);
-    // batch n: host -> pinned slot -> device staging -> packed bf16 ring slot (block 0's input)
+    // batch n: host -> pinned slot -> device staging -> packed bf16 ring slot (block 0's
+    // input), on the copy stream so it overlaps step n-1. Safe once step n-2 is done: ring
+    // slot n mod R was last read by step n-R+m_0 (labels: n-R+cum_p[K-1]+m_{K-1}) <= n-2.
     const int pi = (int)(n & 1);
-    ENG_CUDA(cudaEventSynchronize(e->pin_ev[pi]));  // the H2D that last read this pinned slot is done
+    ENG_CUDA(cudaEventSynchronize(e->pin_ev[pi]));  // batch n-2's copy out of this pinned slot is done
     memcpy(e->pin_x[pi], x + (size_t)i * e->B * e->D, xb);
     memcpy(e->pin_l[pi], lab, lb);
     const int slot = (int)(n % e->R);
-    ENG_CUDA(cudaMemcpyAsync(e->xdev, e->pin_x[pi], xb, cudaMemcpyHostToDevice, e->stream));
-    ENG_CUDA(cudaMemcpyAsync(e->ring_lab[slot], e->pin_l[pi], lb, cudaMemcpyHostToDevice, e->stream));
-    ENG_CUDA(cudaEventRecord(e->pin_ev[pi], e->stream));
-    DSP_TRY(dsp_pack_input(e->xdev, e->ring_in[slot], e->B, e->cfg.in_c, e->cfg.in_h, e->cfg.in_w,
-                           (e->cfg.in_c + 7) / 8 * 8, e->cfg.dtype, 1, e->stream));
+    if (n >= 2) ENG_CUDA(cudaStreamWaitEvent(e->copy_stream, e->step_ev[pi], 0));  // step n-2 done
+    ENG_CUDA(cudaMemcpyAsync(e->xdev[pi], e->pin_x[pi], xb, cudaMemcpyHostToDevice, e->copy_stream));
+    ENG_CUDA(cudaMemcpyAsync(e->ring_lab[slot], e->pin_l[pi], lb, cudaMemcpyHostToDevice, e->copy_stream));
+    DSP_TRY(dsp_pack_input(e->xdev[pi], e->ring_in[slot], e->B, e->cfg.in_c, e->cfg.in_h, e->cfg.in_w,
+                           (e->cfg.in_c + 7) / 8 * 8, e->cfg.dtype, 1, e->copy_stream));
+    ENG_CUDA(cudaEventRecord(e->pin_ev[pi], e->copy_stream));
+    ENG_CUDA(cudaStreamWaitEvent(e->stream, e->pin_ev[pi], 0));
     DSP_TRY(run_step_device(e, n));
     // the step's loss / grad-norm row -> pinned host log (asynchronous)
     const int64_t row = n;
@@ -397,9 +407,11 @@ extern "C" int dsp_run(dsp_engine_t* e, int n_steps, const float* x, const int64
     float* dst = e->host_log[row / dsp_engine::LOG_CHUNK] + (row % dsp_engine::LOG_CHUNK) * e->K * 2;
     ENG_CUDA(cudaMemcpyAsync(dst, e->slots + (size_t)slot * e->K * 2, sizeof(float) * e->K * 2,
                              cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(cudaEventRecord(e->step_ev[pi], e->stream));
     e->steps = n + 1;
   }
   ENG_CUDA(cudaStreamSynchronize(e->stream));
+  ENG_CUDA(cudaStreamSynchronize(e->copy_stream));
   return DSP_OK;
 }
 
@@ -446,9 +458,11 @@ extern "C" void dsp_destroy(dsp_engine_t* e) {
   for (int64_t* p : e->ring_lab) cudaFree(p);
   cudaFree(e->zero_act);
   cudaFree(e->zero_lab);
-  cudaFree(e->xdev);
+  if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
   cudaFree(e->slots);
   for (int i = 0; i < 2; ++i) {
+    cudaFree(e->xdev[i]);
+    if (e->step_ev[i]) cudaEventDestroy(e->step_ev[i]);
     if (e->pin_x[i]) cudaFreeHost(e->pin_x[i]);
     if (e->pin_l[i]) cudaFreeHost(e->pin_l[i]);
     if (e->pin_ev[i]) cudaEventDestroy(e->pin_ev[i]);
@@ -456,5 +470,6 @@ extern "C" void dsp_destroy(dsp_engine_t* e) {
   for (float* c : e->host_log) cudaFreeHost(c);
   if (e->fork_ev) cudaEventDestroy(e->fork_ev);
   if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   delete e;
 }

@@ -56,6 +56,15 @@ class NativeEngine:
         cfg.layers = C.cast(flat, C.POINTER(L.LayerDesc))
         cfg.use_graphs = int(use_graphs)
         cfg.device = device
+        # ring depth and graph horizon exactly as csrc/engine.cu derives them (steps >= horizon
+        # replay per-phase graphs; the first replay of each of the ring phases captures it)
+        p, m = config.p, config.m
+        q = [0] + [m[k - 1] - p[k - 1] - m[k] for k in range(1, K)]
+        cum = int(sum(p[:K - 1]))
+        life = max([m[0] + 1] + [p[k] + m[k + 1] + 1 for k in range(K - 1)] + [q[k] + 1 for k in range(1, K)]
+                   + [cum + m[K - 1] + 1])
+        self.ring = life + 1
+        self.horizon = cum + max(m) + max(p) + max(q) + 1
         h = C.c_void_p()
         L.check(lib.dsp_create(C.byref(cfg), C.byref(h)))
         self.h = h
