@@ -33,6 +33,8 @@ from .blocks import (
     suggest_boundaries,
     tanh,
 )
+from .data import Dataset, TeacherSpec, batch_iter, epoch_stream, gen_teacher_dataset
+from .deviation import DeviationRow, DeviceOperators
 from .native import NativeEngine
 from .optim import LrSchedule, NonFiniteError, OptimizerState, apply_update, lr_at, sgd_step, sum_step
 from .pipeline import (
@@ -62,4 +64,5 @@ __all__ = [
     "default_queue_config", "dense", "derive_seed", "flop_balanced_boundaries", "init_params", "lr_at", "maxpool",
     "mix64", "relu", "resnet50_layers", "resnet_cifar_bottleneck_layers", "resnet_cifar_layers", "sgd_step",
     "staleness_of", "suggest_boundaries", "sum_step", "tanh", "validate_config",
+    "Dataset", "TeacherSpec", "batch_iter", "epoch_stream", "gen_teacher_dataset", "DeviationRow", "DeviceOperators",
 ]

@@ -241,9 +241,35 @@ class B200Runtime:
             self.dev[k].forward(x, y, record=False, stream=self._s(k))
         return y
 
-    def forward_record(self, k: int, x, n: int = 0) -> None:
+    def forward_record(self, k: int, x, n: int = 0, y=None) -> None:
         if self.mode != "replay":
-            self.dev[k].forward(x, None, record=True, stream=self._s(k))
+            self.dev[k].forward(x, y, record=True, stream=self._s(k))
+
+    # ---- deviation diagnostics (eager steps only) ---------------------------
+    def params_tensor(self, k: int):
+        return self.dev[k].params[: self.model.blocks[k].param_count]
+
+    def grads_tensor(self, k: int):
+        return self.dev[k].grads[: self.model.blocks[k].param_count]
+
+    def logits_buffer(self, k: int):
+        """fp32 [B][C_pad] buffer the last block's recorded forward copies its logits into."""
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.empty(self.B * _pad8(self.num_classes), dtype=self.torch.float32, device=self.device)
+
+    def vector_norm(self, t):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.linalg.vector_norm(t.float())
+
+    def xent_grad_norm(self, logits, labels):
+        """||(softmax(z) - onehot) / B|| of the recorded logits: the upstream error gradient
+        the last block differentiates (tensor.py:86-111)."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            z = logits.view(self.B, -1)[:, : self.num_classes].double()
+            g = torch.softmax(z, dim=1)
+            g[torch.arange(self.B, device=self.device), labels] -= 1.0
+            return torch.linalg.vector_norm(g / self.B)
 
     def loss(self, k: int, labels, n: int = 0):
         if self.mode != "replay":

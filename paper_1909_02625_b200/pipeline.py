@@ -245,8 +245,6 @@ class TrainEngine:
                              f"'serial'/'parallel' are the reference's CPU backends), got {backend!r}")
         if rule not in RULES:
             raise ValueError(f"unknown optimizer rule: {rule!r}")
-        if deviation_every:
-            raise NotImplementedError("deviation diagnostics are not on the B200 hot path yet (SURVEY.md §8f row 1)")
         OptimizerState(rule=rule, beta=beta, s=s)  # validates beta / s like the reference
         self.model = model
         self.config = config
@@ -317,6 +315,17 @@ class TrainEngine:
         self._outbox_act = {}
         self._outbox_grad = {}
 
+        # gradient-deviation diagnostics on the device (pipeline.py:520; deviation.py). Needs
+        # every block in this process; tracked runs take eager steps (snapshots are conditional).
+        self.tracker = None
+        if deviation_every:
+            if len(self.local) != K:
+                raise ValueError("deviation diagnostics need all blocks in one process")
+            from .deviation import DeviationTracker
+
+            self.tracker = DeviationTracker(deviation_every, model, self.batch_size, device=self.rt.device,
+                                            stream=self.rt.stream)
+
         self.opt_states = [self.rt.opt_state(k) if k in self.local else None for k in range(K)]
         self.block_steps = [0] * K
         self._block_logs = [[] for _ in range(K)]
@@ -349,7 +358,16 @@ class TrainEngine:
         if self.straggler is not None:
             self.straggler.sleep_maybe(k, n, 0)
 
+        tr = self.tracker
+        track_fresh = tr is not None and tr.wants(fresh.batch_index)
+        track_stale = tr is not None and tr.wants(stale.batch_index)
+        if track_fresh and k == 0:
+            tr.on_input(fresh.batch_index, fresh.tensor, fresh.labels)
+        if track_fresh and k < last:
+            tr.on_forward(k, fresh.batch_index, rt.params_tensor(k))
+
         loss_h = None
+        up_norm = None
         if k < last:
             h_out = rt.forward(k, fresh.tensor, n)
             pkt = ActivationPacket(fresh.batch_index, h_out, fresh.labels)
@@ -363,15 +381,26 @@ class TrainEngine:
                 raise ProtocolError(f"block {k} step {n}: gradient batch {gpkt.batch_index} "
                                     f"does not meet activation batch {stale.batch_index}")
             upstream = gpkt.tensor
+            if track_stale:
+                up_norm = rt.vector_norm(upstream)
         else:
-            rt.forward_record(k, stale.tensor, n)
+            logits = None
+            if track_stale:
+                logits = rt.logits_buffer(k)
+                rt.forward_record(k, stale.tensor, n, y=logits)
+            else:
+                rt.forward_record(k, stale.tensor, n)
             loss_h = rt.loss(k, stale.labels, n)
             upstream = None
+            if track_stale:
+                up_norm = rt.xent_grad_norm(logits, stale.labels)
 
         if self.straggler is not None:
             self.straggler.sleep_maybe(k, n, 1)
 
         grad_in = rt.backward(k, upstream, k > 0, n)
+        if track_stale:  # backward-time parameters (before the update) and the runtime gradient
+            tr.on_backward(k, stale.batch_index, rt.params_tensor(k), rt.grads_tensor(k), up_norm, n)
         if k > 0:
             gp = GradPacket(stale.batch_index, grad_in)
             if self.placement[k - 1] == self.rank:
@@ -435,7 +464,7 @@ class TrainEngine:
     def run(self, n_steps: int) -> None:
         if n_steps < 0:
             raise ValueError("n_steps must be non-negative")
-        graphs = getattr(self.rt, "use_graphs", False) and self._transport.world <= 1
+        graphs = getattr(self.rt, "use_graphs", False) and self._transport.world <= 1 and self.tracker is None
         for _ in range(n_steps):
             n = self.block_steps[self.local[0]] if self.local else 0
             if graphs and n >= self._graph_horizon():
@@ -495,10 +524,18 @@ class TrainEngine:
         merged = []
         for rows in self._block_logs:
             merged.extend(rows)
-        return TrainLog(sorted(merged, key=lambda r: (r.step, r.block)))
+        log = TrainLog(sorted(merged, key=lambda r: (r.step, r.block)))
+        if self.tracker is not None:  # pipeline.py:670-677
+            by_key = {}
+            for row in self.tracker.rows():
+                for k, step in enumerate(row.steps):
+                    by_key[(step, k)] = row.per_param[k]
+            for r in log.records:
+                r.grad_deviation = by_key.get((r.step, r.block))
+        return log
 
     def deviation_rows(self) -> list:
-        return []
+        return self.tracker.rows() if self.tracker is not None else []
 
     def realized_staleness(self) -> list[int]:
         """Fresh-vs-backward lag per block over non-warmup records (pipeline.py:682-694)."""

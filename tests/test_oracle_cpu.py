@@ -169,3 +169,26 @@ def test_live_reference_cnn_driven(stalepipe):
     finally:
         spp.block_forward, spp.block_backward = orig
     assert eng.log.checksum() == str(g["checksum"])
+
+
+def test_theory_port_matches_reference(stalepipe):
+    """theory.py (Lemma-1 bookkeeping over deviation rows) vs the reference's theory module."""
+    import paper_1909_02625_b200.theory as T
+    from paper_1909_02625_b200.deviation import DeviationRow
+    import stalepipe.theory as RT
+
+    rng = np.random.default_rng(3)
+    rows = []
+    for b in range(6):
+        diffs = list(np.abs(rng.standard_normal(3)))
+        if b == 2:
+            diffs = [0.0, 0.0, 0.0]
+        rows.append(DeviationRow(batch_index=5 * b, raw=list(np.abs(rng.standard_normal(3))), per_param=[0.0] * 3,
+                                 raw_fwd=[0.0] * 3 if b == 2 else list(np.abs(rng.standard_normal(3))), diffs=diffs,
+                                 upstream_norms=list(np.abs(rng.standard_normal(3))), steps=[b, b + 1, b + 2]))
+    assert T.estimate_constants(rows) == RT.estimate_constants(rows)
+    L, M = T.estimate_constants(rows)
+    for LL, MM in ((L, M), (0.5 * L, M), (1.0, 1.0)):
+        assert T.lemma1_report(rows, LL, MM) == RT.lemma1_report(rows, LL, MM)
+    assert T.lemma_bound_rhs(2.0, 3.0, [1.0, 0.5, 0.25]) == RT.lemma_bound_rhs(2.0, 3.0, [1.0, 0.5, 0.25])
+    assert T.lemma1_report(rows, L, M)["holds_fraction"] == 1.0
