@@ -280,7 +280,10 @@ def run_b200(args):
     model = P.build_model(layers, bounds)
     P.init_params(model, 0)
     stream = torch.cuda.current_stream(dev)
-    dev_pool = to_device_batches(host_pool, IN_SHAPE, dev, stream)
+    # device-resident pool generated on the GPU (csrc/synth.cu): bitwise the packed host pool
+    from paper_1909_02625_b200.data import device_synthetic_batches
+
+    dev_pool = device_synthetic_batches(16, args.batch, IN_SHAPE, CLASSES, seed=0, device=dev, stream=stream)
     eng = P.TrainEngine(model, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(0.1), rule="sum",
                         beta=0.9, s=1.0, weight_decay=5e-4, device=dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)

@@ -192,6 +192,12 @@ int dsp_pack_input(const float* x_dev, void* out, int batch, int c, int h, int w
                    int nchw, void* stream);
 int dsp_unpack_output(const void* in, float* out_dev, int batch, int c, int h, int w, int c_pad, int dtype,
                       int nchw, void* stream);
+/* Batch batch_no of the synthetic pool synthetic_batches(n, B, (c,h,w), num_classes, seed)
+ * (x ~ SeededRng(seed).normal, labels = floor(SeededRng(derive_seed(seed,1))
+ * .uniform * C), rng.py:47-88) generated on the device: act_out = packed NHWC activation
+ * (dtype, channels padded to c_pad), labels_out = int64 [B]; either may be NULL. */
+int dsp_synth_batch(uint64_t seed, int64_t batch_no, int batch, int c, int h, int w, int c_pad, int num_classes,
+                    int dtype, void* act_out, int64_t* labels_out, void* stream);
 const char* dsp_last_error(void);
 int dsp_abi_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */

@@ -111,6 +111,33 @@ def to_device_batches(batches, in_shape, device=None, stream=None):
     return out
 
 
+def device_synthetic_batches(n_batches: int, batch: int, in_shape, num_classes: int, seed: int = 0, device=None,
+                             stream=None):
+    """``to_device_batches(synthetic_batches(...))`` generated on the device (csrc/synth.cu): the
+    counter-based stream is evaluated per element straight into packed bf16 slots, no host
+    arrays and no H2D copies."""
+    import ctypes as C
+
+    from . import _lib as L
+    from .runtime import ptr, require_cuda, stream_ptr, torch_mod
+
+    torch = torch_mod()
+    dev = require_cuda(device)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    c, h, w = (tuple(in_shape) + (1, 1))[:3] if len(in_shape) < 3 else tuple(in_shape)
+    cp = (c + 7) // 8 * 8
+    lib = L.load()
+    out = []
+    for i in range(n_batches):
+        with torch.cuda.stream(st):
+            act = torch.empty(batch * h * w * cp, dtype=torch.bfloat16, device=dev)
+            lab = torch.empty(batch, dtype=torch.int64, device=dev)
+        L.check(lib.dsp_synth_batch(seed & ((1 << 64) - 1), i, batch, c, h, w, cp, num_classes, L.DSP_DTYPE_BF16,
+                                    ptr(act), C.cast(ptr(lab), C.POINTER(C.c_int64)), stream_ptr(st)))
+        out.append(DeviceBatch(act, lab))
+    return out
+
+
 def cycle(pool):
     while True:
         for b in pool:
