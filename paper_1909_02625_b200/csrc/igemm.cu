@@ -174,6 +174,15 @@ struct IgTma {
   // D (bf16 FPROP / DGRAD output): epilogue stages the 128 x BN tile in smem, one TMA
   // store per box of d_cols columns (rows of d_cols*2 bytes, swizzle mask d_swz)
   int on_d, d_cols, d_swz;
+  // FPROP halo tiles (stride-1 RxS convs, C <= 64, one image per tile): one stage per tile =
+  // S boxes of (hb + R - 1) input rows x W x C (one per horizontal tap offset, OOB = padding);
+  // tap (r, s) is the box-s view shifted down r rows. Weights stay resident in smem.
+  int halo;
+  int h_box;    // bytes of one A box
+  int h_nst;    // ring depth (stages = tiles in flight)
+  int h_nwb;    // resident weight boxes of 64 K x BN (SWIZZLE_128B)
+  int h_rowb;   // bytes per A row (C * 2)
+  int h_swz;    // UMMA layout type of A
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
   // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
   uint32_t fd_d[5], fd_mul[5], fd_shr[5];
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
   constexpr int BG = BN / EPC;     // MN groups in the B tile (MN-major)
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[NACC], tempty_bar[NACC];
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[NACC], tempty_bar[NACC], wbar;
   __shared__ uint32_t tmem_base_s;
   __shared__ int last_cta_s;
   __shared__ float red[4][BN][3];
@@ -290,6 +299,7 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 128);
     }
+    mbar_init(&wbar, 1);
     fence_barrier_init();
   }
   if (warp == IG_MMA_WARP) tmem_alloc(&tmem_base_s, Cfg::TMEM_COLS);
@@ -321,7 +331,29 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
   const uint32_t sA0 = smem_u32(smem);
   const uint32_t sB0 = sA0 + STAGES * A_BYTES;
 
-  if (warp < NPW) {
+  // halo layout: [h_nst stages of S boxes][resident weights]
+  const uint32_t h_stage = (uint32_t)(tm.h_box * g.S);
+  const uint32_t sW = sA0 + (uint32_t)tm.h_nst * h_stage;
+  if (warp < NPW && tm.halo) {
+    // ============================ halo producer ============================
+    if (warp == 0 && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      const int n0c = (blockIdx.x % nt) * BN;
+      mbar_arrive_expect_tx(&wbar, (uint32_t)(tm.h_nwb * BN * 128));
+      for (int j = 0; j < tm.h_nwb; ++j) tma_load_2d(sW + j * (BN * 128), &tmB, &wbar, j * KS, n0c);
+      int m0, n0, z, kb0, kb1;
+      for (int t = 0; get_unit(t, m0, n0, z, kb0, kb1); ++t) {
+        const int st = t % tm.h_nst;
+        if (t >= tm.h_nst) mbar_wait(&empty_bar[st], ((t / tm.h_nst) - 1) & 1);
+        const int img = m0 / (g.P * g.Q);
+        const int h0 = (m0 - img * g.P * g.Q) / g.Q;
+        mbar_arrive_expect_tx(&full_bar[st], h_stage);
+        for (int sx = 0; sx < g.S; ++sx)
+          tma_load_4d(sA0 + st * h_stage + sx * tm.h_box, &tmA, &full_bar[st], 0, sx - g.pad, h0 - g.pad, img);
+      }
+    }
+  } else if (warp < NPW) {
     // =============================== producers ===============================
     // (all-TMA launches: only thread 0 produces; the other producer threads go idle)
     if (gather || warp == 0) {
@@ -535,6 +567,39 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     }
     cp_async_wait<0>();
     }
+  } else if (warp == IG_MMA_WARP && tm.halo) {
+    // ============================ halo MMA issuer ============================
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, 0u, 0u, IG_BM, BN);
+      const uint64_t a_tpl = umma_sdesc(0, 16, 8 * tm.h_rowb, tm.h_swz);
+      const uint64_t b_tpl = umma_sdesc(0, 16, 1024, 2);  // [BN][128 B] SWIZZLE_128B boxes
+      const int C = g.C;
+      mbar_wait(&wbar, 0);
+      int m0, n0, z, kb0, kb1;
+      for (int i = 0; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
+        const int acc = i % NACC;
+        if (i >= NACC) mbar_wait(&tempty_bar[acc], ((i / NACC) - 1) & 1);
+        const int st = i % tm.h_nst;
+        mbar_wait(&full_bar[st], (i / tm.h_nst) & 1);
+        tc_fence_after();
+        const uint32_t td = tmem_d + acc * BN;
+        const uint32_t base = sA0 + st * h_stage;
+        bool accum = false;
+        for (int r = 0; r < g.R; ++r)
+          for (int sx = 0; sx < g.S; ++sx)
+            for (int kc = 0; kc < C; kc += MmaTraits<T>::MMA_K) {
+              const uint32_t aa = base + sx * tm.h_box + r * g.Q * tm.h_rowb + kc * 2;
+              const int k = (r * g.S + sx) * C + kc;
+              const uint32_t ba = sW + (k / KS) * (BN * 128) + (k % KS) * 2;
+              MmaTraits<T>::mma(td, a_tpl | (uint64_t)((aa >> 4) & 0x3FFF), b_tpl | (uint64_t)((ba >> 4) & 0x3FFF),
+                                idesc, accum ? 1u : 0u);
+              accum = true;
+            }
+        umma_commit(&empty_bar[st]);
+        umma_commit(&tfull_bar[acc]);
+      }
+    }
+    __syncwarp();
   } else if (warp == IG_MMA_WARP) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
@@ -927,6 +992,58 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+constexpr int IG_HALO_SMEM_MAX = 100 * 1024;  // keeps two conv CTAs per SM
+
+// FPROP halo tiles: stride-1 'same' RxS conv, C in {16, 32, 64} (one A box covers all
+// channels), output rows of 8k pixels with a 128-pixel tile = hb whole rows of one image.
+template <int BN>
+static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB,
+                      PFN_cuTensorMapEncodeTiled_v12000 enc) {
+  static const bool disabled = getenv("DSP_B200_NO_HALO") != nullptr;
+  const dsp_conv_geom_t& g = a.geom;
+  if (disabled || g.stride != 1 || g.R != g.S || g.pad != (g.R - 1) / 2 || g.R % 2 == 0) return false;
+  if (g.C != 16 && g.C != 32 && g.C != 64) return false;
+  if (g.P != g.H || g.Q != g.W || g.Q % 8 || IG_BM % g.Q) return false;
+  const int hb = IG_BM / g.Q;
+  if (hb > g.P || g.P % hb) return false;
+  if ((a.Kd % 8) || (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15)) return false;
+  const int rows = hb + g.R - 1;
+  if (rows > 256 || g.W > 256) return false;
+  const int rowb = g.C * 2;
+  const int box = rowb * g.W * rows;
+  const int nwb = (a.Kd + 63) / 64;
+  const int wbytes = nwb * BN * 128;
+  const int nst = std::min(IgCfg<BN>::STAGES, (IG_HALO_SMEM_MAX - wbytes) / (box * g.S));
+  if (nst < 2) return false;
+  const CUtensorMapSwizzle swz = g.C == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : g.C == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                             : CU_TENSOR_MAP_SWIZZLE_128B;
+  cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.nimg};
+  cuuint64_t strides[3] = {(cuuint64_t)rowb, (cuuint64_t)g.W * rowb, (cuuint64_t)g.H * g.W * rowb};
+  cuuint32_t bx[4] = {(cuuint32_t)g.C, (cuuint32_t)g.W, (cuuint32_t)rows, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.A), dims, strides, bx, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)g.K};
+  cuuint64_t bs[1] = {(cuuint64_t)a.Kd * 2};
+  cuuint32_t bb[2] = {64, (cuuint32_t)BN};
+  cuuint32_t be[2] = {1, 1};
+  if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.B), bd, bs, bb, be,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  tm.on_a = tm.on_b = 1;
+  tm.halo = 1;
+  tm.h_box = box;
+  tm.h_nst = nst;
+  tm.h_nwb = nwb;
+  tm.h_rowb = rowb;
+  tm.h_swz = g.C == 16 ? 6 : g.C == 32 ? 4 : 2;
+  return true;
+}
+
 // Decide whether this launch's A (and B) operands can be fetched with TMA and
 // build the tensor maps. A: bf16 FPROP (stride 1/2) or stride-1 DGRAD whose
 // 128-row M tile is a whole box of output pixels (OW | 128 and the rows fit
@@ -993,6 +1110,7 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
     tm.kb_imgs = imgs;
     return;
   }
+  if (MODE == DSP_IGEMM_FPROP && halo_plan<BN>(a, tm, tmA, tmB, enc)) return;
   if (MODE == DSP_IGEMM_DGRAD && g.stride != 1) return;
   if (g.stride != 1 && g.stride != 2) return;
   const int cdim = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the gathered tensor
@@ -1077,10 +1195,11 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   static int attr_state = 0;
   static int num_sms = 148;
   if (!attr_state) {
+    const int smax = std::max(Cfg::SMEM, IG_HALO_SMEM_MAX);
     cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM);
+                                         smax);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1113,10 +1232,11 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
     }
   }
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
+  const int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128 : Cfg::SMEM;
   if (tm.on_a && tm.on_b && !force4)  // nothing to gather: one producer warp
-    igemm_kernel<T, MODE, BN, 1><<<grid, IgWarps<1>::THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tmD, tm);
+    igemm_kernel<T, MODE, BN, 1><<<grid, IgWarps<1>::THREADS, smem, st>>>(a, tmA, tmB, tmD, tm);
   else
-    igemm_kernel<T, MODE, BN, 4><<<grid, IgWarps<4>::THREADS, Cfg::SMEM, st>>>(a, tmA, tmB, tmD, tm);
+    igemm_kernel<T, MODE, BN, 4><<<grid, IgWarps<4>::THREADS, smem, st>>>(a, tmA, tmB, tmD, tm);
   (void)splits;
   note_launch();
   return cudaGetLastError();

@@ -32,6 +32,12 @@ CASES = [
     (37, 1, 1, 72, 136, 1, 1, 0),       # dense layer as 1x1 conv, ragged M
     (2, 8, 8, 256, 272, 1, 1, 0),       # multiple N tiles
     (1, 4, 4, 8, 520, 3, 1, 1),         # > 2 N tiles
+    # FPROP halo tiles (one A stage per 128-pixel tile, resident weights)
+    (2, 16, 16, 32, 32, 3, 1, 1),       # C=32: SWIZZLE_64B rows, hb=8
+    (2, 32, 32, 16, 32, 3, 1, 1),       # N=32 tile
+    (1, 16, 16, 64, 64, 3, 1, 1),       # C=64: SWIZZLE_128B rows
+    (2, 16, 16, 16, 16, 5, 1, 2),       # 5x5: 4 halo rows
+    (2, 16, 16, 32, 64, 1, 1, 0),       # 1x1: a single box per tile
 ]
 
 
