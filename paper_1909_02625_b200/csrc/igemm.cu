@@ -1002,7 +1002,11 @@ static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CU
   static const bool disabled = getenv("DSP_B200_NO_HALO") != nullptr;
   const dsp_conv_geom_t& g = a.geom;
   if (disabled || g.stride != 1 || g.R != g.S || g.pad != (g.R - 1) / 2 || g.R % 2 == 0) return false;
-  if (g.C != 16 && g.C != 32 && g.C != 64) return false;
+  static const int max_c = getenv("DSP_B200_HALO_MAXC") ? atoi(getenv("DSP_B200_HALO_MAXC")) : 64;
+  // a 2-deep ring (stage 1: 42 KB) measured best in the concurrent step: 3 stages were
+  // faster alone but left less smem for the other blocks' kernels
+  static const int max_nst = getenv("DSP_B200_HALO_NST") ? atoi(getenv("DSP_B200_HALO_NST")) : 2;
+  if ((g.C != 16 && g.C != 32 && g.C != 64) || g.C > max_c) return false;
   if (g.P != g.H || g.Q != g.W || g.Q % 8 || IG_BM % g.Q) return false;
   const int hb = IG_BM / g.Q;
   if (hb > g.P || g.P % hb) return false;
@@ -1013,7 +1017,7 @@ static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CU
   const int box = rowb * g.W * rows;
   const int nwb = (a.Kd + 63) / 64;
   const int wbytes = nwb * BN * 128;
-  const int nst = std::min(IgCfg<BN>::STAGES, (IG_HALO_SMEM_MAX - wbytes) / (box * g.S));
+  const int nst = std::min(std::min(IgCfg<BN>::STAGES, max_nst), (IG_HALO_SMEM_MAX - wbytes) / (box * g.S));
   if (nst < 2) return false;
   const CUtensorMapSwizzle swz = g.C == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
                                  : g.C == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
