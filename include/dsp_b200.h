@@ -261,6 +261,13 @@ int dsp_read_log(dsp_engine_t* eng, dsp_log_record_t* recs, size_t cap, size_t* 
 int64_t dsp_steps_done(dsp_engine_t* eng);
 void dsp_destroy(dsp_engine_t* eng);
 
+/* Live kernel timing (bench.py roofline): while armed, every dsp_igemm-class launch with
+ * (mode, N, M) records events[2i] before and events[2i+1] after it on its own stream (also
+ * inside CUDA-graph capture), i = 0, 1, ... up to n_pairs; dsp_probe_reset() restarts at 0 and
+ * returns how many launches were probed. events: cudaEvent_t handles; NULL disarms. */
+int dsp_probe_arm(int mode, int n, int64_t m, void* const* events, int n_pairs);
+int dsp_probe_reset(void);
+
 /* Step-graph execution (the engine's replacement for the reference's per-step
  * Python loop, pipeline.py:416-449).  graph: a captured cudaGraph_t; flags:
  * DSP_GRAPH_NODE_PRIORITY honours each kernel node's priority (inherited from the

@@ -140,6 +140,8 @@ _SIGNATURES = {
     "dsp_graph_instantiate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "dsp_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsp_graph_destroy": (C.c_int, [C.c_void_p]),
+    "dsp_probe_arm": (C.c_int, [C.c_int, C.c_int, C.c_int64, C.POINTER(C.c_void_p), C.c_int]),
+    "dsp_probe_reset": (C.c_int, []),
     "dsp_create": (C.c_int, [C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),
     "dsp_set_params": (C.c_int, [_P, C.c_int, _P, C.c_size_t, C.c_int]),
     "dsp_get_params": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.c_size_t]),

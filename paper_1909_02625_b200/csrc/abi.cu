@@ -35,6 +35,11 @@ extern "C" const char* dsp_last_error(void) { return g_last_error; }
 extern "C" int dsp_abi_version(void) { return DSP_ABI_VERSION; }
 extern "C" int64_t dsp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+extern "C" int dsp_probe_arm(int mode, int n, int64_t m, void* const* events, int n_pairs) {
+  return probe_arm(mode, n, m, events, n_pairs);
+}
+extern "C" int dsp_probe_reset(void) { return probe_reset(); }
+
 extern "C" int dsp_graph_instantiate(void* graph, int flags, void** exec_out) {
   if (graph == nullptr || exec_out == nullptr) return set_error(DSP_E_INVALID, "dsp_graph_instantiate: null argument");
   cudaGraphExec_t exec = nullptr;

@@ -1255,7 +1255,52 @@ static cudaError_t launch_mode(const dsp_igemm_args_t& a, int splits, cudaStream
   return launch_bn<T, MODE, 256>(a, splits, st);
 }
 
+// Live-duration probe (bench.py roofline): CUDA event pairs around the launches of one shape.
+struct Probe {
+  int mode = -1, n = 0;
+  int64_t m = 0;
+  cudaEvent_t* ev = nullptr;
+  int npairs = 0, next = 0;
+};
+static Probe g_probe;
+
+static cudaError_t igemm_dispatch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st);
+
 cudaError_t igemm_launch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
+  Probe& p = g_probe;
+  if (p.ev == nullptr || mode != p.mode || a.N != p.n || a.M != p.m || p.next >= p.npairs)
+    return igemm_dispatch(mode, dtype, a, splits, st);
+  const int i = p.next++;
+  // while capturing, External makes an event-record node that fires on every replay (a plain
+  // record would only be a capture-internal dependency); the flag is illegal outside capture
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  const unsigned flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  e = cudaEventRecordWithFlags(p.ev[2 * i], st, flags);
+  if (e != cudaSuccess) return e;
+  e = igemm_dispatch(mode, dtype, a, splits, st);
+  if (e != cudaSuccess) return e;
+  return cudaEventRecordWithFlags(p.ev[2 * i + 1], st, flags);
+}
+
+int probe_arm(int mode, int n, int64_t m, void* const* events, int n_pairs) {
+  g_probe = Probe{};
+  if (events == nullptr || n_pairs <= 0) return 0;
+  g_probe.mode = mode;
+  g_probe.n = n;
+  g_probe.m = m;
+  g_probe.ev = reinterpret_cast<cudaEvent_t*>(const_cast<void**>(events));
+  g_probe.npairs = n_pairs;
+  return 0;
+}
+int probe_reset() {
+  const int k = g_probe.next;
+  g_probe.next = 0;
+  return k;
+}
+
+static cudaError_t igemm_dispatch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   if (dtype == DSP_DTYPE_BF16) {
     if (mode == DSP_IGEMM_FPROP) return launch_mode<bf16, DSP_IGEMM_FPROP>(a, splits, st);
     if (mode == DSP_IGEMM_DGRAD) return launch_mode<bf16, DSP_IGEMM_DGRAD>(a, splits, st);

@@ -12,6 +12,8 @@ namespace dsp {
 void note_launch();
 
 cudaError_t igemm_launch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st);
+int probe_arm(int mode, int n, int64_t m, void* const* events, int n_pairs);
+int probe_reset();
 
 // BatchNorm forward: reduce igemm partials [tiles][2][Cp] -> per-channel
 // stat[0]=mean, stat[1]=invstd, stat[2]=scale(gamma*invstd), stat[3]=shift(beta-mean*scale)
