@@ -112,6 +112,9 @@ typedef struct {
   int32_t bnb_count;
   int32_t bnb_c_real;
   dsp_bnb_target_t bnb[2];
+  /* DGRAD (optional): the weights transposed per tap, [Cin_p][R][S][Cout_p] bf16 -- lets
+   * stride-1 DGRAD load K-major weight boxes with TMA and use halo tiles like FPROP. */
+  const void* B_t;
 } dsp_igemm_args_t;
 
 #define DSP_IGEMM_MAX_CTAS 444

@@ -34,6 +34,7 @@ struct ConvP {
   int ci_real = 0, co_real = 0;
   int64_t w_off = 0, gamma_off = 0, beta_off = 0;  // floats, into block params
   int64_t wpack = 0;                               // elements, into packed weights
+  int64_t wpack_t = -1;                            // transposed pack [Cin_p][R][S][Cout_p] (stride-1 convs)
   size_t y = 0, stat = 0, coef = 0;                // workspace byte offsets
   int64_t M() const { return (int64_t)g.nimg * g.P * g.Q; }
   int64_t Min() const { return (int64_t)g.nimg * g.H * g.W; }
@@ -198,6 +199,7 @@ int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const voi
   a.ldd = c.g.C;
   a.residual = residual;
   a.n_valid = c.ci_real;
+  if (c.wpack_t >= 0) a.B_t = b->ws + b->packed + (size_t)c.wpack_t * b->esz;
   if (fuse != nullptr) {
     a.stats = at<float>(b, b->fpart);
     a.sem = at<int32_t>(b, b->sem);
@@ -477,6 +479,10 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
         off += co;
         c.wpack = pack_elems;
         pack_elems += (int64_t)c.g.K * k * k * c.g.C;
+        if (stride == 1) {  // DGRAD's K-major weights (TMA / halo tiles)
+          c.wpack_t = pack_elems;
+          pack_elems += (int64_t)c.g.K * k * k * c.g.C;
+        }
         l.convs.push_back(c);
         return l.convs.back().g;
       };
@@ -544,6 +550,8 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       const int sp = wgrad_splits(c, &kb, dtype);
       max_wpart = std::max<int64_t>(max_wpart, (int64_t)sp * c.g.R * c.g.S * c.g.C * c.g.K);
       b->packs.push_back({c.w_off, c.wpack, c.co_real, c.ci_real, c.g.R * c.g.S, c.g.K, c.g.C, 0});
+      if (c.wpack_t >= 0)
+        b->packs.push_back({c.w_off, c.wpack_t, c.co_real, c.ci_real, c.g.R * c.g.S, c.g.K, c.g.C, 2});
     }
     if (l.d.kind == DSP_LAYER_BASIC_UNIT || l.d.kind == DSP_LAYER_BOTTLENECK) {
       l.z1 = pl.take((size_t)l.convs[0].M() * l.convs[0].g.K * b->esz);

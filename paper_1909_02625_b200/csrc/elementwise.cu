@@ -533,13 +533,21 @@ __global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__
   const int64_t total = (int64_t)e.cop * e.rs * e.cip;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int ci = (int)(idx % e.cip);
-    const int64_t t = idx / e.cip;
-    const int tap = (int)(t % e.rs);
-    const int co = (int)(t / e.rs);
+    int ci, co, tap;
+    if (e.dense_src == 2) {  // [cip][rs][cop]
+      co = (int)(idx % e.cop);
+      const int64_t t = idx / e.cop;
+      tap = (int)(t % e.rs);
+      ci = (int)(t / e.rs);
+    } else {  // [cop][rs][cip]
+      ci = (int)(idx % e.cip);
+      const int64_t t = idx / e.cip;
+      tap = (int)(t % e.rs);
+      co = (int)(t / e.rs);
+    }
     float v = 0.f;
     if (co < e.co && ci < e.ci) {
-      v = e.dense_src ? params[e.src_off + (int64_t)ci * e.co + co]
+      v = e.dense_src == 1 ? params[e.src_off + (int64_t)ci * e.co + co]
                       : params[e.src_off + ((int64_t)co * e.rs + tap) * e.ci + ci];
     }
     packed[e.dst_off + idx] = from_f<T>(v);

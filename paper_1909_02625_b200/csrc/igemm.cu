@@ -346,8 +346,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       for (int t = 0; get_unit(t, m0, n0, z, kb0, kb1); ++t) {
         const int st = t % tm.h_nst;
         if (t >= tm.h_nst) mbar_wait(&empty_bar[st], ((t / tm.h_nst) - 1) & 1);
-        const int img = m0 / (g.P * g.Q);
-        const int h0 = (m0 - img * g.P * g.Q) / g.Q;
+        const int oh = MODE == DSP_IGEMM_FPROP ? g.P : g.H, ow = MODE == DSP_IGEMM_FPROP ? g.Q : g.W;
+        const int img = m0 / (oh * ow);
+        const int h0 = (m0 - img * oh * ow) / ow;
         mbar_arrive_expect_tx(&full_bar[st], h_stage);
         for (int sx = 0; sx < g.S; ++sx)
           tma_load_4d(sA0 + st * h_stage + sx * tm.h_box, &tmA, &full_bar[st], 0, sx - g.pad, h0 - g.pad, img);
@@ -573,7 +574,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, 0u, 0u, IG_BM, BN);
       const uint64_t a_tpl = umma_sdesc(0, 16, 8 * tm.h_rowb, tm.h_swz);
       const uint64_t b_tpl = umma_sdesc(0, 16, 1024, 2);  // [BN][128 B] SWIZZLE_128B boxes
-      const int C = g.C;
+      // FPROP: tap (r, s) = box s shifted down r rows; DGRAD (flipped taps): box S-1-s, R-1-r
+      const int C = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the A rows
+      const int ow = MODE == DSP_IGEMM_FPROP ? g.Q : g.W;
       mbar_wait(&wbar, 0);
       int m0, n0, z, kb0, kb1;
       for (int i = 0; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
@@ -588,7 +591,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
         for (int r = 0; r < g.R; ++r)
           for (int sx = 0; sx < g.S; ++sx)
             for (int kc = 0; kc < C; kc += MmaTraits<T>::MMA_K) {
-              const uint32_t aa = base + sx * tm.h_box + r * g.Q * tm.h_rowb + kc * 2;
+              const int bx = MODE == DSP_IGEMM_FPROP ? sx : g.S - 1 - sx;
+              const int ro = MODE == DSP_IGEMM_FPROP ? r : g.R - 1 - r;
+              const uint32_t aa = base + bx * tm.h_box + ro * ow * tm.h_rowb + kc * 2;
               const int k = (r * g.S + sx) * C + kc;
               const uint32_t ba = sW + (k / KS) * (BN * 128) + (k % KS) * 2;
               MmaTraits<T>::mma(td, a_tpl | (uint64_t)((aa >> 4) & 0x3FFF), b_tpl | (uint64_t)((ba >> 4) & 0x3FFF),
@@ -996,7 +1001,7 @@ constexpr int IG_HALO_SMEM_MAX = 100 * 1024;  // keeps two conv CTAs per SM
 
 // FPROP halo tiles: stride-1 'same' RxS conv, C in {16, 32, 64} (one A box covers all
 // channels), output rows of 8k pixels with a 128-pixel tile = hb whole rows of one image.
-template <int BN>
+template <int MODE, int BN>
 static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB,
                       PFN_cuTensorMapEncodeTiled_v12000 enc) {
   static const bool disabled = getenv("DSP_B200_NO_HALO") != nullptr;
@@ -1006,35 +1011,38 @@ static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CU
   // a 2-deep ring (stage 1: 42 KB) measured best in the concurrent step: 3 stages were
   // faster alone but left less smem for the other blocks' kernels
   static const int max_nst = getenv("DSP_B200_HALO_NST") ? atoi(getenv("DSP_B200_HALO_NST")) : 2;
-  if ((g.C != 16 && g.C != 32 && g.C != 64) || g.C > max_c) return false;
+  // A rows: FPROP = X pixels with C channels; DGRAD = dY pixels with K channels (weights B_t)
+  const int cch = MODE == DSP_IGEMM_FPROP ? g.C : g.K;
+  const void* bsrc = MODE == DSP_IGEMM_FPROP ? a.B : a.B_t;
+  if ((cch != 16 && cch != 32 && cch != 64) || cch > max_c || bsrc == nullptr) return false;
   if (g.P != g.H || g.Q != g.W || g.Q % 8 || IG_BM % g.Q) return false;
   const int hb = IG_BM / g.Q;
   if (hb > g.P || g.P % hb) return false;
-  if ((a.Kd % 8) || (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15)) return false;
+  if ((a.Kd % 8) || (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(bsrc) & 15)) return false;
   const int rows = hb + g.R - 1;
   if (rows > 256 || g.W > 256) return false;
-  const int rowb = g.C * 2;
+  const int rowb = cch * 2;
   const int box = rowb * g.W * rows;
   const int nwb = (a.Kd + 63) / 64;
   const int wbytes = nwb * BN * 128;
   const int nst = std::min(std::min(IgCfg<BN>::STAGES, max_nst), (IG_HALO_SMEM_MAX - wbytes) / (box * g.S));
   if (nst < 2) return false;
-  const CUtensorMapSwizzle swz = g.C == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
-                                 : g.C == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+  const CUtensorMapSwizzle swz = cch == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : cch == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                              : CU_TENSOR_MAP_SWIZZLE_128B;
-  cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.nimg};
+  cuuint64_t dims[4] = {(cuuint64_t)cch, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.nimg};
   cuuint64_t strides[3] = {(cuuint64_t)rowb, (cuuint64_t)g.W * rowb, (cuuint64_t)g.H * g.W * rowb};
-  cuuint32_t bx[4] = {(cuuint32_t)g.C, (cuuint32_t)g.W, (cuuint32_t)rows, 1};
+  cuuint32_t bx[4] = {(cuuint32_t)cch, (cuuint32_t)g.W, (cuuint32_t)rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.A), dims, strides, bx, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
-  cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)g.K};
+  cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)a.N};  // weights [N rows][Kd], K-major
   cuuint64_t bs[1] = {(cuuint64_t)a.Kd * 2};
   cuuint32_t bb[2] = {64, (cuuint32_t)BN};
   cuuint32_t be[2] = {1, 1};
-  if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.B), bd, bs, bb, be,
+  if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(bsrc), bd, bs, bb, be,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
@@ -1044,7 +1052,7 @@ static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CU
   tm.h_nst = nst;
   tm.h_nwb = nwb;
   tm.h_rowb = rowb;
-  tm.h_swz = g.C == 16 ? 6 : g.C == 32 ? 4 : 2;
+  tm.h_swz = cch == 16 ? 6 : cch == 32 ? 4 : 2;
   return true;
 }
 
@@ -1114,7 +1122,7 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
     tm.kb_imgs = imgs;
     return;
   }
-  if (MODE == DSP_IGEMM_FPROP && halo_plan<BN>(a, tm, tmA, tmB, enc)) return;
+  if (MODE != DSP_IGEMM_WGRAD && halo_plan<MODE, BN>(a, tm, tmA, tmB, enc)) return;
   if (MODE == DSP_IGEMM_DGRAD && g.stride != 1) return;
   if (g.stride != 1 && g.stride != 2) return;
   const int cdim = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the gathered tensor

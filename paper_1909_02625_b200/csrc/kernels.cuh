@@ -78,8 +78,8 @@ cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, i
 struct PackEntry {
   int64_t src_off;   // into params (floats)
   int64_t dst_off;   // into the packed buffer (elements)
-  int32_t co, ci, rs, cop, cip, dense_src;
-};
+  int32_t co, ci, rs, cop, cip, dense_src;  // dense_src: 0 conv [cop][rs][cip], 1 dense, 2 conv transposed
+};                                           //   per tap [cip][rs][cop] (DGRAD K-major weights)
 cudaError_t pack_weights(int dtype, const float* params, void* packed, const PackEntry* entries_dev, int n_entries,
                          int max_elems, cudaStream_t st);
 

@@ -48,7 +48,7 @@ def _geom(nimg, H, W, C_, K, R, stride, pad):
 
 
 def _run(mode, dtype, g, M, N, Kd, A, B, D, splits=1, kb=1, stats=None, residual=None, bias=None, ldd=None,
-         out_f32=0, stat_out=None, gamma=None, beta=None, sem=None, n_valid=0):
+         out_f32=0, stat_out=None, gamma=None, beta=None, sem=None, n_valid=0, B_t=None):
     a = L.IgemmArgs()
     a.geom = g
     a.M, a.N, a.Kd = M, N, Kd
@@ -60,7 +60,7 @@ def _run(mode, dtype, g, M, N, Kd, A, B, D, splits=1, kb=1, stats=None, residual
     a.stats = stats.data_ptr() if stats is not None else None
     a.kb_per_split = kb
     a.n_valid = n_valid
-    for name, t in (("stat_out", stat_out), ("gamma", gamma), ("beta", beta), ("sem", sem)):
+    for name, t in (("stat_out", stat_out), ("gamma", gamma), ("beta", beta), ("sem", sem), ("B_t", B_t)):
         setattr(a, name, t.data_ptr() if t is not None else None)
     L.check(L.load().dsp_igemm(mode, dtype, C.byref(a), splits, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
@@ -125,14 +125,18 @@ def test_fprop(case, dt):
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16])
+@pytest.mark.parametrize("transposed", [False, True])
 @pytest.mark.parametrize("case", CASES)
-def test_dgrad(case, dt):
+def test_dgrad(case, dt, transposed):
+    """transposed: also pass the per-tap transposed weights B_t [C][R][S][K] -- stride-1 'same'
+    convs with K in {16, 32, 64} then take the halo path (TMA dY boxes + resident weights)."""
     nimg, H, W, Cc, K, R, stride, pad = case
     g, P, Q, dcode, x, w, dy = _setup(case, dt)
     rtol, atol = _tol(dt)
     dx = torch.empty(nimg, H, W, Cc, device="cuda", dtype=dt)
     res = torch.randn(nimg, H, W, Cc, device="cuda").to(dt)
-    _run(L.DSP_IGEMM_DGRAD, dcode, g, nimg * H * W, Cc, R * R * K, dy, w, dx, residual=res)
+    w_t = w.permute(3, 1, 2, 0).contiguous() if transposed else None
+    _run(L.DSP_IGEMM_DGRAD, dcode, g, nimg * H * W, Cc, R * R * K, dy, w, dx, residual=res, B_t=w_t)
     refdx = torch.nn.grad.conv2d_input((nimg, Cc, H, W), w.float().permute(0, 3, 1, 2),
                                        dy.float().permute(0, 3, 1, 2), stride=stride,
                                        padding=pad).permute(0, 2, 3, 1)
