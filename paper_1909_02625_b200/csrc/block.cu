@@ -304,7 +304,11 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
 }
 
 // u: gradient w.r.t. the layer output; x: the layer input; dx may be null.
-int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* dx, cudaStream_t st) {
+// below: the top BatchNorm(s) of the layer under this one, whose backward statistics the
+// final DGRAD (producing dx = that layer's upstream) accumulates; top_done: this layer's top
+// BN statistics were produced that way by the layer above (only the apply pass is left).
+int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* dx, cudaStream_t st,
+                   const BnbFuse* below = nullptr, bool top_done = false) {
   const int dt = b->dtype;
   switch (l.d.kind) {
     case DSP_LAYER_DENSE: {
@@ -345,9 +349,12 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
     case DSP_LAYER_CONV_BN_RELU: {
       const ConvP& c = l.convs[0];
       void* dy = b->ws + b->S[0];
-      DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
+      if (top_done)
+        DSP_TRY(bn_backward_apply(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
+      else
+        DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
       DSP_TRY(conv_wgrad(b, c, x, dy, st));
-      if (dx) DSP_TRY(conv_dgrad(b, c, dy, dx, nullptr, st));
+      if (dx) DSP_TRY(conv_dgrad(b, c, dy, dx, nullptr, st, below));
       return DSP_OK;
     }
     case DSP_LAYER_BASIC_UNIT:
@@ -361,7 +368,10 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
       const ConvP& cl = l.convs[nmain - 1];
       const ConvP* cs = l.proj ? &l.convs[nmain] : nullptr;
       // top BN(s): g = u * (out > 0); dy_last -> S0, dy_sc -> S1 (proj) or g -> S1 (identity)
-      DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st));
+      if (top_done)
+        DSP_TRY(bn_backward_apply(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st));
+      else
+        DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st));
       // walk the main path down
       for (int i = nmain - 1; i >= 0; --i) {
         const ConvP& c = l.convs[i];
@@ -381,7 +391,7 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
         if (dx) DSP_TRY(conv_dgrad(b, *cs, S1, S3, nullptr, st));
         res = S3;
       }
-      if (dx) DSP_TRY(conv_dgrad(b, l.convs[0], S0, dx, res, st));
+      if (dx) DSP_TRY(conv_dgrad(b, l.convs[0], S0, dx, res, st, below));
       return DSP_OK;
     }
   }
@@ -662,11 +672,26 @@ extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* gr
   if (!u) return set_error(DSP_E_INVALID, "dsp_block_backward: null upstream");
   const int n = (int)b->L.size();
   DSP_CUDA(cudaMemsetAsync(b->grads, 0, sizeof(float) * b->param_count, st));
+  auto has_top_bn = [](const LayerP& l) {
+    return l.d.kind == DSP_LAYER_CONV_BN_RELU || l.d.kind == DSP_LAYER_BASIC_UNIT ||
+           l.d.kind == DSP_LAYER_BOTTLENECK;
+  };
+  bool top_done = false;
   for (int i = n - 1; i >= 0; --i) {
     LayerP& l = b->L[i];
     const void* x = i == 0 ? b->rec_x : (const void*)(b->ws + b->L[i - 1].out);
     void* dx = i == 0 ? grad_in : (void*)(b->ws + b->G[i & 1]);
-    DSP_TRY(layer_backward(b, l, x, u, dx, st));
+    // the layer below's top BN statistics ride on this layer's final DGRAD (g = dx * (x > 0))
+    BnbFuse fz{};
+    const BnbFuse* below = nullptr;
+    if (i > 0 && dx != nullptr && has_top_bn(l) && has_top_bn(b->L[i - 1])) {
+      const LayerP& lb = b->L[i - 1];
+      const int nmain = lb.d.kind == DSP_LAYER_BOTTLENECK ? 3 : lb.d.kind == DSP_LAYER_BASIC_UNIT ? 2 : 1;
+      fz = BnbFuse{x, &lb.convs[nmain - 1], lb.proj ? &lb.convs[nmain] : nullptr};
+      below = &fz;
+    }
+    DSP_TRY(layer_backward(b, l, x, u, dx, st, below, top_done));
+    top_done = below != nullptr;
     u = dx;
   }
   return DSP_OK;
