@@ -146,6 +146,12 @@ class B200Runtime:
             return act, lab
         if x.shape[0] != self.B:
             raise ValueError(f"batch of {x.shape[0]} rows, engine sized for {self.B}")
+        width = int(np.prod(x.shape[1:]))
+        shape0 = self.model.blocks[0].in_shape
+        if width != int(np.prod(shape0)):
+            from .blocks import ShapeError
+
+            raise ShapeError(f"batch width {width} does not match the model input {tuple(shape0)}")
         lab_h = np.asarray(labels, dtype=np.int64)
         if lab_h.shape != (self.B,):
             raise ValueError(f"labels must have shape ({self.B},), got {lab_h.shape}")

@@ -87,6 +87,11 @@ class NativeEngine:
         """len(x) DSP steps on host batches x [n, B, C*H*W] (float32) and labels [n, B] (int64)."""
         x = np.ascontiguousarray(x, dtype=np.float32).reshape(len(x), self.B, -1)
         labels = np.ascontiguousarray(labels, dtype=np.int64).reshape(len(x), self.B)
+        D = int(np.prod(self.model.blocks[0].in_shape))
+        if x.shape[2] != D:
+            from .blocks import ShapeError
+
+            raise ShapeError(f"batch width {x.shape[2]} does not match the model input {self.model.blocks[0].in_shape}")
         L.check(self.lib.dsp_run(self.h, len(x), x.ctypes.data_as(C.POINTER(C.c_float)),
                                  labels.ctypes.data_as(C.POINTER(C.c_int64))))
 
