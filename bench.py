@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--k", type=int, default=0, help="DSP blocks (default 4, or 8 when --gpus 8)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cuts", default="", help="block boundaries (layer indices), default FLOP-balanced")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -63,7 +64,10 @@ def workload(args):
 
     K = blocks_for(args)
     layers = P.resnet_cifar_layers(DEPTH, CLASSES)
-    bounds = P.flop_balanced_boundaries(layers, K) if K > 1 else []
+    if getattr(args, "cuts", ""):
+        bounds = [int(v) for v in args.cuts.split(",")]
+    else:
+        bounds = P.flop_balanced_boundaries(layers, K) if K > 1 else []
     cfg = P.default_queue_config(K)
     return layers, bounds, cfg
 

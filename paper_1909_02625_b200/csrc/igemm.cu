@@ -37,6 +37,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -345,7 +346,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       int m0, n0, z, kb0, kb1;
       for (int t = 0; get_unit(t, m0, n0, z, kb0, kb1); ++t) {
         const int st = t % tm.h_nst;
+        IG_TRACE(2 * t, t < 32);
         if (t >= tm.h_nst) mbar_wait(&empty_bar[st], ((t / tm.h_nst) - 1) & 1);
+        IG_TRACE(2 * t + 1, t < 32);
         const int oh = MODE == DSP_IGEMM_FPROP ? g.P : g.H, ow = MODE == DSP_IGEMM_FPROP ? g.Q : g.W;
         const int img = m0 / (oh * ow);
         const int h0 = (m0 - img * oh * ow) / ow;
@@ -577,31 +580,65 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       // FPROP: tap (r, s) = box s shifted down r rows; DGRAD (flipped taps): box S-1-s, R-1-r
       const int C = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the A rows
       const int ow = MODE == DSP_IGEMM_FPROP ? g.Q : g.W;
+      const uint32_t row_step = (uint32_t)(ow * tm.h_rowb);
+      const bool unrolled = g.R == 3 && g.S == 3;
       mbar_wait(&wbar, 0);
       int m0, n0, z, kb0, kb1;
       for (int i = 0; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
         const int acc = i % NACC;
         if (i >= NACC) mbar_wait(&tempty_bar[acc], ((i / NACC) - 1) & 1);
         const int st = i % tm.h_nst;
+        IG_TRACE(128 + i, i < 16);
         mbar_wait(&full_bar[st], (i / tm.h_nst) & 1);
+        IG_TRACE(64 + 2 * i, i < 32);
         tc_fence_after();
         const uint32_t td = tmem_d + acc * BN;
         const uint32_t base = sA0 + st * h_stage;
-        bool accum = false;
-        for (int r = 0; r < g.R; ++r)
-          for (int sx = 0; sx < g.S; ++sx)
-            for (int kc = 0; kc < C; kc += MmaTraits<T>::MMA_K) {
-              const int bx = MODE == DSP_IGEMM_FPROP ? sx : g.S - 1 - sx;
-              const int ro = MODE == DSP_IGEMM_FPROP ? r : g.R - 1 - r;
-              const uint32_t aa = base + bx * tm.h_box + ro * ow * tm.h_rowb + kc * 2;
-              const int k = (r * g.S + sx) * C + kc;
+        // per-tile MMA sequence: 3x3 taps fully unrolled per channel count (compile-time tap and
+        // K offsets; only the stage base and two runtime strides remain), generic loop otherwise
+        auto issue = [&](auto cch) {
+          constexpr int CC = decltype(cch)::value;
+#pragma unroll
+          for (int t = 0; t < 9; ++t) {
+            const int r = t / 3, sx = t % 3;
+            const int ro = MODE == DSP_IGEMM_FPROP ? r : 2 - r;
+            const int bx = MODE == DSP_IGEMM_FPROP ? sx : 2 - sx;
+            const uint32_t arow = base + bx * tm.h_box + ro * row_step;
+#pragma unroll
+            for (int kc = 0; kc < CC; kc += MmaTraits<T>::MMA_K) {
+              const int k = t * CC + kc;
+              const uint32_t aa = arow + kc * 2;
               const uint32_t ba = sW + (k / KS) * (BN * 128) + (k % KS) * 2;
               MmaTraits<T>::mma(td, a_tpl | (uint64_t)((aa >> 4) & 0x3FFF), b_tpl | (uint64_t)((ba >> 4) & 0x3FFF),
-                                idesc, accum ? 1u : 0u);
-              accum = true;
+                                idesc, k > 0 ? 1u : 0u);
             }
+          }
+        };
+        if (unrolled && C == 16) {
+          issue(std::integral_constant<int, 16>{});
+        } else if (unrolled && C == 32) {
+          issue(std::integral_constant<int, 32>{});
+        } else if (unrolled && C == 64) {
+          issue(std::integral_constant<int, 64>{});
+        } else {
+          uint32_t k = 0;
+          for (int r = 0; r < g.R; ++r) {
+            const int ro = MODE == DSP_IGEMM_FPROP ? r : g.R - 1 - r;
+            for (int sx = 0; sx < g.S; ++sx) {
+              const int bx = MODE == DSP_IGEMM_FPROP ? sx : g.S - 1 - sx;
+              const uint32_t arow = base + bx * tm.h_box + ro * row_step;
+              for (int kc = 0; kc < C; kc += MmaTraits<T>::MMA_K, k += MmaTraits<T>::MMA_K) {
+                const uint32_t aa = arow + kc * 2;
+                const uint32_t ba = sW + (k / KS) * (BN * 128) + (k % KS) * 2;
+                MmaTraits<T>::mma(td, a_tpl | (uint64_t)((aa >> 4) & 0x3FFF),
+                                  b_tpl | (uint64_t)((ba >> 4) & 0x3FFF), idesc, k > 0 ? 1u : 0u);
+              }
+            }
+          }
+        }
         umma_commit(&empty_bar[st]);
         umma_commit(&tfull_bar[acc]);
+        IG_TRACE(65 + 2 * i, i < 32);
       }
     }
     __syncwarp();
