@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "paper_1909_02625_b200 kernels target sm_100a only"
@@ -84,6 +85,15 @@ __device__ __forceinline__ double part_sums_get(const double* fin4, int NS, int 
 }
 // widest column window part_sums_load can cover with NTH threads
 __host__ __device__ constexpr int part_sums_window(int NTH, int NS) { return NS <= 2 ? 2 * NTH : NTH; }
+
+// Programmatic dependent launch. Kernels are launched with programmatic stream serialization
+// (launch_k below) so a kernel's launch and prologue overlap its predecessor's teardown; every
+// kernel calls pdl_wait() before its first global-memory access (reads and writes: the
+// predecessor may still be reading). No kernel triggers early (pdl_trigger): successors are
+// released as the predecessor's CTAs exit -- early triggers let waiting CTAs occupy SM slots
+// the concurrent block streams need (measured, igemm.cu).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
@@ -319,5 +329,31 @@ template <>
 __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+// Kernel launch with programmatic stream serialization (see pdl_wait); DSP_B200_PDL=0 turns it
+// off (plain stream order). Captured into CUDA graphs as programmatic edges.
+inline bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("DSP_B200_PDL");
+    return (e == nullptr || e[0] != '0') ? 1 : 0;
+  }();
+  return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 }  // namespace dsp

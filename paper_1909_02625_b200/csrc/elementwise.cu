@@ -57,6 +57,7 @@ cudaError_t dispatch_dtype(int dtype, F&& f) {
 // ------------------------------------------------------------------ BatchNorm forward
 __global__ void bn_finalize_k(const float* __restrict__ part, int tiles, int Cp, int c_real, double count,
                               const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ stat) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ double s1[128], s2[128];
   const int c = blockIdx.x;
   double a = 0.0, b = 0.0;
@@ -97,6 +98,7 @@ template <typename T>
 __global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
                            int64_t nvec, int Cp, int relu) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e0 = v * VE;
@@ -142,6 +144,7 @@ template <typename T>
 __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                 const float* __restrict__ stat, float* __restrict__ part, int64_t M, int Cp,
                                 int rows_per_chunk, const BnBwdFin fin) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   __shared__ float red[kThreads][2 * VE];
   const int G = Cp / VE;
@@ -233,6 +236,7 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
 __global__ void bn_bwd_finalize_k(const float* __restrict__ part, int chunks, int Cp, int c_real, double count,
                                   const float* __restrict__ gamma, const float* __restrict__ stat,
                                   float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ coef) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ double s1[128], s2[128];
   const int c = blockIdx.x;
   double a = 0.0, b = 0.0;
@@ -268,6 +272,7 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
                                int64_t nvec, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e0 = v * VE;
@@ -309,6 +314,7 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
 // ------------------------------------------------------------------ activations / pooling
 template <typename T>
 __global__ void act_fwd_k(int tanh_kind, const T* __restrict__ x, T* __restrict__ out, int64_t nvec) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
     float a[VE];
@@ -322,6 +328,7 @@ __global__ void act_fwd_k(int tanh_kind, const T* __restrict__ x, T* __restrict_
 template <typename T>
 __global__ void act_bwd_k(int tanh_kind, const T* __restrict__ x, const T* __restrict__ u, T* __restrict__ dx,
                           int64_t nvec) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
     float a[VE], g[VE];
@@ -342,6 +349,7 @@ __global__ void act_bwd_k(int tanh_kind, const T* __restrict__ x, const T* __res
 
 template <typename T>
 __global__ void avgpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int B, int HW, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int G = Cp / VE;
   const int64_t nthr = (int64_t)B * G;
@@ -365,6 +373,7 @@ __global__ void avgpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int 
 
 template <typename T>
 __global__ void avgpool_bwd_k(const T* __restrict__ u, T* __restrict__ dx, int B, int HW, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int64_t nvec = (int64_t)B * HW * Cp / VE;
   const float inv = 1.f / (float)HW;
@@ -383,6 +392,7 @@ __global__ void avgpool_bwd_k(const T* __restrict__ u, T* __restrict__ dx, int B
 template <typename T>
 __global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int32_t* __restrict__ arg, int B, int H,
                               int W, int P, int Q, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const int64_t n = (int64_t)B * P * Q * Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cp);
@@ -414,6 +424,7 @@ __global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int3
 template <typename T>
 __global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict__ arg, T* __restrict__ dx, int B,
                               int H, int W, int P, int Q, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const int64_t n = (int64_t)B * H * W * Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cp);
@@ -445,6 +456,7 @@ __global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict
 template <typename T>
 __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, int C, const int64_t* __restrict__ labels,
                                T* __restrict__ dlogits, float* __restrict__ loss) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   extern __shared__ float row_loss[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -482,6 +494,7 @@ __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, 
 __global__ void __launch_bounds__(256) wgrad_reduce_k(const float* __restrict__ part, int splits, int Mw, int N,
                                                      int RS, int Cp, int ci_real, int co_real, int dense_layout,
                                                      float* __restrict__ grad) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   // CTA = 32 consecutive partial elements (coalesced 128 B per split row) x 8 warps; warp w
   // sums the contiguous split range [w*S/8, (w+1)*S/8), 8 loads in flight, then warp 0 adds
   // the 8 warp sums in order (deterministic). Small CTAs on purpose: the step runs the K
@@ -529,6 +542,7 @@ __global__ void __launch_bounds__(256) wgrad_reduce_k(const float* __restrict__ 
 template <typename T>
 __global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__ packed,
                                const PackEntry* __restrict__ ents, int n_entries) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const PackEntry e = ents[blockIdx.y];
   const int64_t total = (int64_t)e.cop * e.rs * e.cip;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -558,6 +572,7 @@ __global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__
 template <int RULE, bool WD>
 __global__ void update_f32_k(int64_t n, float* __restrict__ x, const float* __restrict__ grad, float* __restrict__ ys,
                              float lr, float slr, float beta, float wd, float* __restrict__ part) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ float red[kThreads];
   float sq = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -587,6 +602,7 @@ template <int RULE, bool WD>
 __global__ void update_f64_k(int64_t n, double* __restrict__ x, const double* __restrict__ grad,
                              double* __restrict__ ys, double* __restrict__ yout, double lr, double slr, double beta,
                              double wd, double* __restrict__ part) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ double red[kThreads];
   double sq = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -614,6 +630,7 @@ __global__ void update_f64_k(int64_t n, double* __restrict__ x, const double* __
 }
 
 __global__ void sumsq_k(int64_t n, const float* __restrict__ v, float* __restrict__ part) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ float red[kThreads];
   float sq = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -629,6 +646,7 @@ __global__ void sumsq_k(int64_t n, const float* __restrict__ v, float* __restric
 
 template <typename S, typename O>
 __global__ void sum_partials_k(const S* __restrict__ part, int n, O* __restrict__ out) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ double red[kThreads];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += kThreads) s += (double)part[i];
@@ -645,6 +663,7 @@ __global__ void sum_partials_k(const S* __restrict__ part, int n, O* __restrict_
 template <typename T>
 __global__ void pack_input_k(const float* __restrict__ x, T* __restrict__ out, int B, int C, int H, int W, int Cp,
                              int nchw) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const int64_t n = (int64_t)B * H * W * Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cp);
@@ -660,6 +679,7 @@ __global__ void pack_input_k(const float* __restrict__ x, T* __restrict__ out, i
 template <typename T>
 __global__ void unpack_output_k(const T* __restrict__ in, float* __restrict__ out, int B, int C, int H, int W, int Cp,
                                 int nchw) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const int64_t n = (int64_t)B * C * H * W;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t b, c, hw;
@@ -683,7 +703,7 @@ __global__ void unpack_output_k(const T* __restrict__ in, float* __restrict__ ou
 // ================================================================== launch wrappers
 cudaError_t bn_finalize(const float* part, int tiles, int Cp, int c_real, int64_t count, const float* gamma,
                         const float* beta, float* stat, cudaStream_t st) {
-  bn_finalize_k<<<Cp, 128, 0, st>>>(part, tiles, Cp, c_real, (double)count, gamma, beta, stat);
+  launch_k(bn_finalize_k, Cp, 128, 0, st, part, tiles, Cp, c_real, (double)count, gamma, beta, stat);
   return note_launch(), cudaGetLastError();
 }
 
@@ -692,7 +712,7 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
-    bn_apply_k<T><<<grid_for(nvec), kThreads, 0, st>>>((const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
+    launch_k(bn_apply_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
                                                       nvec, Cp, relu);
     return note_launch(), cudaGetLastError();
   });
@@ -719,7 +739,7 @@ cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const v
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
-    bn_bwd_reduce_k<T><<<chunks, kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
+    launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
                                                     rows, BnBwdFin{});
     return note_launch(), cudaGetLastError();
   });
@@ -734,7 +754,7 @@ cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const vo
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
-    bn_bwd_reduce_k<T><<<chunks, kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
+    launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
                                                     rows, fin);
     return note_launch(), cudaGetLastError();
   });
@@ -742,7 +762,7 @@ cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const vo
 
 cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, int64_t count, const float* gamma,
                             const float* stat, float* dgamma, float* dbeta, float* coef, cudaStream_t st) {
-  bn_bwd_finalize_k<<<Cp, 128, 0, st>>>(part, chunks, Cp, c_real, (double)count, gamma, stat, dgamma, dbeta, coef);
+  launch_k(bn_bwd_finalize_k, Cp, 128, 0, st, part, chunks, Cp, c_real, (double)count, gamma, stat, dgamma, dbeta, coef);
   return note_launch(), cudaGetLastError();
 }
 
@@ -752,7 +772,7 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
-    bn_bwd_apply_k<T><<<grid_for(nvec), kThreads, 0, st>>>((const T*)gsrc, (const T*)mask, (const T*)y, stat, coef,
+    launch_k(bn_bwd_apply_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef,
                                                            (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b,
                                                            (T*)g_out, nvec, Cp);
     return note_launch(), cudaGetLastError();
@@ -763,7 +783,7 @@ cudaError_t act_forward(int dtype, int tanh_kind, const void* x, void* out, int6
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = n / V16<T>::N;
-    act_fwd_k<T><<<grid_for(nvec), kThreads, 0, st>>>(tanh_kind, (const T*)x, (T*)out, nvec);
+    launch_k(act_fwd_k<T>, grid_for(nvec), kThreads, 0, st, tanh_kind, (const T*)x, (T*)out, nvec);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -772,7 +792,7 @@ cudaError_t act_backward(int dtype, int tanh_kind, const void* x, const void* u,
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = n / V16<T>::N;
-    act_bwd_k<T><<<grid_for(nvec), kThreads, 0, st>>>(tanh_kind, (const T*)x, (const T*)u, (T*)dx, nvec);
+    launch_k(act_bwd_k<T>, grid_for(nvec), kThreads, 0, st, tanh_kind, (const T*)x, (const T*)u, (T*)dx, nvec);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -780,7 +800,7 @@ cudaError_t act_backward(int dtype, int tanh_kind, const void* x, const void* u,
 cudaError_t avgpool_forward(int dtype, const void* x, void* out, int B, int HW, int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    avgpool_fwd_k<T><<<grid_for((int64_t)B * Cp / V16<T>::N), kThreads, 0, st>>>((const T*)x, (T*)out, B, HW, Cp);
+    launch_k(avgpool_fwd_k<T>, grid_for((int64_t)B * Cp / V16<T>::N), kThreads, 0, st, (const T*)x, (T*)out, B, HW, Cp);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -788,7 +808,7 @@ cudaError_t avgpool_forward(int dtype, const void* x, void* out, int B, int HW, 
 cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    avgpool_bwd_k<T><<<grid_for((int64_t)B * HW * Cp / V16<T>::N), kThreads, 0, st>>>((const T*)u, (T*)dx, B, HW, Cp);
+    launch_k(avgpool_bwd_k<T>, grid_for((int64_t)B * HW * Cp / V16<T>::N), kThreads, 0, st, (const T*)u, (T*)dx, B, HW, Cp);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -797,7 +817,7 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, i
                             int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    maxpool_fwd_k<T><<<grid_for((int64_t)B * P * Q * Cp), kThreads, 0, st>>>((const T*)x, (T*)out, arg, B, H, W, P, Q,
+    launch_k(maxpool_fwd_k<T>, grid_for((int64_t)B * P * Q * Cp), kThreads, 0, st, (const T*)x, (T*)out, arg, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
   });
@@ -807,7 +827,7 @@ cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void*
                              int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    maxpool_bwd_k<T><<<grid_for((int64_t)B * H * W * Cp), kThreads, 0, st>>>((const T*)u, arg, (T*)dx, B, H, W, P, Q,
+    launch_k(maxpool_bwd_k<T>, grid_for((int64_t)B * H * W * Cp), kThreads, 0, st, (const T*)u, arg, (T*)dx, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
   });
@@ -817,7 +837,7 @@ cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, c
                          float* loss, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    softmax_xent_k<T><<<1, 512, B * sizeof(float), st>>>(logits, ld, B, C, labels, (T*)dlogits, loss);
+    launch_k(softmax_xent_k<T>, 1, 512, B * sizeof(float), st, logits, ld, B, C, labels, (T*)dlogits, loss);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -825,7 +845,7 @@ cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, c
 cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
                          int dense_layout, float* grad, cudaStream_t st) {
   const int64_t total = (int64_t)Mw * N;
-  wgrad_reduce_k<<<(unsigned)((total + 31) / 32), 256, 0, st>>>(part, splits, Mw, N, RS, Cp, ci_real, co_real,
+  launch_k(wgrad_reduce_k, (unsigned)((total + 31) / 32), 256, 0, st, part, splits, Mw, N, RS, Cp, ci_real, co_real,
                                                                   dense_layout, grad);
   return note_launch(), cudaGetLastError();
 }
@@ -836,7 +856,7 @@ cudaError_t pack_weights(int dtype, const float* params, void* packed, const Pac
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     dim3 grid(grid_for(max_elems, kThreads, 256), n_entries);
-    pack_weights_k<T><<<grid, kThreads, 0, st>>>(params, (T*)packed, entries_dev, n_entries);
+    launch_k(pack_weights_k<T>, grid, kThreads, 0, st, params, (T*)packed, entries_dev, n_entries);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -848,11 +868,11 @@ cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* 
   const int g = update_grid(n);
   const bool w = wd != 0.f;
   if (rule == DSP_RULE_SGD) {
-    if (w) update_f32_k<DSP_RULE_SGD, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
-    else update_f32_k<DSP_RULE_SGD, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
+    if (w) launch_k(update_f32_k<DSP_RULE_SGD, true>, g, kThreads, 0, st, n, x, grad, ys, lr, slr, beta, wd, part);
+    else launch_k(update_f32_k<DSP_RULE_SGD, false>, g, kThreads, 0, st, n, x, grad, ys, lr, slr, beta, wd, part);
   } else {
-    if (w) update_f32_k<DSP_RULE_SUM, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
-    else update_f32_k<DSP_RULE_SUM, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, lr, slr, beta, wd, part);
+    if (w) launch_k(update_f32_k<DSP_RULE_SUM, true>, g, kThreads, 0, st, n, x, grad, ys, lr, slr, beta, wd, part);
+    else launch_k(update_f32_k<DSP_RULE_SUM, false>, g, kThreads, 0, st, n, x, grad, ys, lr, slr, beta, wd, part);
   }
   return note_launch(), cudaGetLastError();
 }
@@ -862,27 +882,27 @@ cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, doubl
   const int g = update_grid(n);
   const bool w = wd != 0.0;
   if (rule == DSP_RULE_SGD) {
-    if (w) update_f64_k<DSP_RULE_SGD, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
-    else update_f64_k<DSP_RULE_SGD, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
+    if (w) launch_k(update_f64_k<DSP_RULE_SGD, true>, g, kThreads, 0, st, n, x, grad, ys, y, lr, slr, beta, wd, part);
+    else launch_k(update_f64_k<DSP_RULE_SGD, false>, g, kThreads, 0, st, n, x, grad, ys, y, lr, slr, beta, wd, part);
   } else {
-    if (w) update_f64_k<DSP_RULE_SUM, true><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
-    else update_f64_k<DSP_RULE_SUM, false><<<g, kThreads, 0, st>>>(n, x, grad, ys, y, lr, slr, beta, wd, part);
+    if (w) launch_k(update_f64_k<DSP_RULE_SUM, true>, g, kThreads, 0, st, n, x, grad, ys, y, lr, slr, beta, wd, part);
+    else launch_k(update_f64_k<DSP_RULE_SUM, false>, g, kThreads, 0, st, n, x, grad, ys, y, lr, slr, beta, wd, part);
   }
   return note_launch(), cudaGetLastError();
 }
 
 cudaError_t sumsq_f32(int64_t n, const float* v, float* part, cudaStream_t st) {
-  sumsq_k<<<update_grid(n), kThreads, 0, st>>>(n, v, part);
+  launch_k(sumsq_k, update_grid(n), kThreads, 0, st, n, v, part);
   return note_launch(), cudaGetLastError();
 }
 
 cudaError_t sum_partials_f32(const float* part, int n, float* out, cudaStream_t st) {
-  sum_partials_k<float, float><<<1, kThreads, 0, st>>>(part, n, out);
+  launch_k(sum_partials_k<float, float>, 1, kThreads, 0, st, part, n, out);
   return note_launch(), cudaGetLastError();
 }
 
 cudaError_t sum_partials_f64(const double* part, int n, double* out, cudaStream_t st) {
-  sum_partials_k<double, double><<<1, kThreads, 0, st>>>(part, n, out);
+  launch_k(sum_partials_k<double, double>, 1, kThreads, 0, st, part, n, out);
   return note_launch(), cudaGetLastError();
 }
 
@@ -890,7 +910,7 @@ cudaError_t pack_input(const float* x, void* out, int B, int C, int H, int W, in
                        cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    pack_input_k<T><<<grid_for((int64_t)B * H * W * Cp), kThreads, 0, st>>>(x, (T*)out, B, C, H, W, Cp, nchw);
+    launch_k(pack_input_k<T>, grid_for((int64_t)B * H * W * Cp), kThreads, 0, st, x, (T*)out, B, C, H, W, Cp, nchw);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -899,7 +919,7 @@ cudaError_t unpack_output(const void* in, float* out, int B, int C, int H, int W
                           cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    unpack_output_k<T><<<grid_for((int64_t)B * C * H * W), kThreads, 0, st>>>((const T*)in, out, B, C, H, W, Cp, nchw);
+    launch_k(unpack_output_k<T>, grid_for((int64_t)B * C * H * W), kThreads, 0, st, (const T*)in, out, B, C, H, W, Cp, nchw);
     return note_launch(), cudaGetLastError();
   });
 }

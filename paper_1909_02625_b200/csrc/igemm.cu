@@ -304,6 +304,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     fence_barrier_init();
   }
   if (warp == IG_MMA_WARP) tmem_alloc(&tmem_base_s, Cfg::TMEM_COLS);
+  // programmatic dependent launch: everything above overlapped the predecessor's tail; no
+  // global memory is touched before it has completed
+  pdl_wait();
   if (want_stats && warp >= IG_EPI_WARP0) {
     for (int c = lane; c < BN; c += 32) red[warp & 3][c][0] = red[warp & 3][c][1] = red[warp & 3][c][2] = 0.f;
     if (bnb && warp == IG_EPI_WARP0) {
@@ -908,6 +911,14 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     }
   }
 
+  // No early trigger by default: successors launch as our CTAs exit (programmatic launch still
+  // overlaps their launch + prologue with our teardown). Triggering here, before the BN-finalize
+  // tail, measured 10% slower in the concurrent step: waiting successor CTAs hold SM slots the
+  // other block streams need (73.1k vs 63.5k samples/s; no PDL at all: 70.5k).
+#ifdef IG_PDL_TRIGGER
+  pdl_trigger();
+#endif
+
   // ---------------- fused BatchNorm finalize by the last CTA ----------------
   if (ctat != nullptr) {
     __syncthreads();
@@ -1283,9 +1294,9 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
   const int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128 : Cfg::SMEM;
   if (tm.on_a && tm.on_b && !force4)  // nothing to gather: one producer warp
-    igemm_kernel<T, MODE, BN, 1><<<grid, IgWarps<1>::THREADS, smem, st>>>(a, tmA, tmB, tmD, tm);
+    launch_k(igemm_kernel<T, MODE, BN, 1>, grid, IgWarps<1>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
   else
-    igemm_kernel<T, MODE, BN, 4><<<grid, IgWarps<4>::THREADS, smem, st>>>(a, tmA, tmB, tmD, tm);
+    launch_k(igemm_kernel<T, MODE, BN, 4>, grid, IgWarps<4>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
   (void)splits;
   note_launch();
   return cudaGetLastError();

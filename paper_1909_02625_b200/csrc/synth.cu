@@ -35,6 +35,7 @@ __device__ __forceinline__ double u53(uint64_t z) { return (double)(z >> 11) * 0
 
 template <typename T>
 __global__ void synth_x_k(uint64_t seed, uint64_t base, int B, int C, int H, int W, int Cp, T* __restrict__ out) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const int64_t n = (int64_t)B * H * W * Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cp);
@@ -59,6 +60,7 @@ __global__ void synth_x_k(uint64_t seed, uint64_t base, int B, int C, int H, int
 }
 
 __global__ void synth_labels_k(uint64_t seed, uint64_t base, int B, int C, int64_t* __restrict__ out) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const double u = u53(splitmix(seed, base + (uint64_t)b));
@@ -90,17 +92,17 @@ extern "C" int dsp_synth_batch(uint64_t seed, int64_t batch_no, int batch, int c
     const int64_t n = (int64_t)batch * h * w * c_pad;
     const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
     if (dtype == DSP_DTYPE_BF16)
-      synth_x_k<bf16><<<grid, 256, 0, st>>>(seed, (uint64_t)batch_no * draws_per_batch, batch, c, h, w, c_pad,
+      launch_k(synth_x_k<bf16>, grid, 256, 0, st, seed, (uint64_t)batch_no * draws_per_batch, batch, c, h, w, c_pad,
                                            (bf16*)act_out);
     else
-      synth_x_k<float><<<grid, 256, 0, st>>>(seed, (uint64_t)batch_no * draws_per_batch, batch, c, h, w, c_pad,
+      launch_k(synth_x_k<float>, grid, 256, 0, st, seed, (uint64_t)batch_no * draws_per_batch, batch, c, h, w, c_pad,
                                             (float*)act_out);
     note_launch();
     DSP_CUDA(cudaGetLastError());
   }
   if (labels_out) {
     const uint64_t lseed = mix64_host(seed + kGolden * 2ull);  // derive_seed(seed, 1) (rng.py:38-44)
-    synth_labels_k<<<(batch + 255) / 256, 256, 0, st>>>(lseed, (uint64_t)batch_no * batch, batch, num_classes,
+    launch_k(synth_labels_k, (batch + 255) / 256, 256, 0, st, lseed, (uint64_t)batch_no * batch, batch, num_classes,
                                                         labels_out);
     note_launch();
     DSP_CUDA(cudaGetLastError());
