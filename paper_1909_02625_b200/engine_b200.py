@@ -111,6 +111,7 @@ class B200Runtime:
         self._cur_stream = self.stream
         prio = block_priorities(model, self.local)
         self._block_streams = {k: torch.cuda.Stream(self.device, priority=prio[k]) for k in self.local}
+        self.eager_concurrent = True  # eager steps: local blocks on their own streams too
         self.replayed_kernels = 0  # library kernels executed through graph replays
 
     def kernels_executed(self) -> int:
@@ -129,8 +130,28 @@ class B200Runtime:
         return act_elems(self.B, self.model.blocks[k].in_shape)
 
     def _s(self, k):
-        """Stream for block k's work: its own forked stream while capturing a step graph."""
-        return self._block_streams[k] if self.mode == "capture" else self.stream
+        """Stream for block k's work: its own forked stream while capturing a step graph, and in
+        eager steps too (eager_concurrent) so the local blocks of a step run concurrently."""
+        if self.mode == "capture" or (self.mode == "eager" and self.eager_concurrent):
+            return self._block_streams[k]
+        return self.stream
+
+    def fork_blocks(self) -> None:
+        """Eager step start: every block stream waits for the main stream (inputs staged, the
+        previous step and its exchange done)."""
+        if self.mode != "eager" or not self.eager_concurrent:
+            return
+        ev = self.torch.cuda.Event()
+        ev.record(self.stream)
+        for k in self.local:
+            self._block_streams[k].wait_event(ev)
+
+    def join_blocks(self) -> None:
+        """Eager step end: the main stream waits for every block stream (before the exchange)."""
+        if self.mode != "eager" or not self.eager_concurrent:
+            return
+        for k in self.local:
+            self.stream.wait_stream(self._block_streams[k])
 
     def make_input(self, x, labels, n: int = 0):
         from .data import DeviceBatch
@@ -140,7 +161,7 @@ class B200Runtime:
         act, lab = self.ring_in[slot], self.ring_lab[slot]
         if isinstance(x, DeviceBatch):
             if self.mode == "eager":
-                self._copy_device_batch(x, slot)
+                self._copy_device_batch(x, slot, self._s(0))
             else:  # graph steps copy the batch in right before the launch
                 self._pending_input = (x, slot)
             return act, lab
@@ -161,7 +182,7 @@ class B200Runtime:
         # Graph steps defer all of it to just before the launch (no syncs in capture).
         if self.mode == "eager":
             self._stage_host_input(x, lab_h, slot)
-            self._issue_host_input(slot)
+            self._issue_host_input(slot, self._s(0))
         else:
             self._pending_input = ("host", slot, x, lab_h)
         return act, lab
@@ -180,22 +201,22 @@ class B200Runtime:
         xs.numpy()[...] = x
         self._pinned[("l", slot)].numpy()[...] = lab_h
 
-    def _copy_device_batch(self, db, slot):
-        with self.torch.cuda.stream(self.stream):
+    def _copy_device_batch(self, db, slot, stream):
+        with self.torch.cuda.stream(stream):
             self.ring_in[slot].copy_(db.act, non_blocking=True)
             self.ring_lab[slot].copy_(db.labels, non_blocking=True)
 
-    def _issue_host_input(self, slot):
+    def _issue_host_input(self, slot, stream):
         torch = self.torch
         xs, ls, xd = self._pinned[("x", slot)], self._pinned[("l", slot)], self._pinned[("xd", slot)]
         c, h, w = self.model.blocks[0].in_shape
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(stream):
             xd.copy_(xs.view(-1), non_blocking=True)
             self.ring_lab[slot].copy_(ls, non_blocking=True)
         L.check(L.load().dsp_pack_input(ptr(xd), ptr(self.ring_in[slot]), self.B, c, h, w, _pad8(c),
-                                        L.DSP_DTYPE_BF16, 1, stream_ptr(self.stream)))
+                                        L.DSP_DTYPE_BF16, 1, stream_ptr(stream)))
         ev = self._pinned.get(("ev", slot)) or torch.cuda.Event()
-        ev.record(self.stream)
+        ev.record(stream)
         self._pinned[("ev", slot)] = ev
 
     def zero_act(self, k: int):
@@ -360,12 +381,12 @@ class B200Runtime:
         self._pending_input = None
         if pend is None:
             return
-        if pend[0] == "host":
+        if pend[0] == "host":  # graph steps: staged on the main stream the graph launch follows
             _, slot, x, lab_h = pend
             self._stage_host_input(x, lab_h, slot)
-            self._issue_host_input(slot)
+            self._issue_host_input(slot, self.stream)
         else:
-            self._copy_device_batch(pend[0], pend[1])
+            self._copy_device_batch(pend[0], pend[1], self.stream)
 
     def _post_step(self, n: int) -> None:
         """Copy phase slots of step n into the device log (eager steps write slots too)."""

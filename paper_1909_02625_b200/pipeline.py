@@ -325,6 +325,7 @@ class TrainEngine:
 
             self.tracker = DeviationTracker(deviation_every, model, self.batch_size, device=self.rt.device,
                                             stream=self.rt.stream)
+            self.rt.eager_concurrent = False  # snapshots are taken on the main stream
 
         self.opt_states = [self.rt.opt_state(k) if k in self.local else None for k in range(K)]
         self.block_steps = [0] * K
@@ -476,8 +477,14 @@ class TrainEngine:
                     end(n)
 
     def _issue_step(self) -> None:
+        fork = getattr(self.rt, "fork_blocks", None)
+        if fork is not None:
+            fork()
         for k in self.local:
             self._iterate_block(k)
+        join = getattr(self.rt, "join_blocks", None)
+        if join is not None:
+            join()
         self._exchange()
 
     def _graph_horizon(self) -> int:
