@@ -201,6 +201,9 @@ int dsp_unpack_output(const void* in, float* out_dev, int batch, int c, int h, i
  * (dtype, channels padded to c_pad), labels_out = int64 [B]; either may be NULL. */
 int dsp_synth_batch(uint64_t seed, int64_t batch_no, int batch, int c, int h, int w, int c_pad, int num_classes,
                     int dtype, void* act_out, int64_t* labels_out, void* stream);
+/* Straggler injection: a one-thread kernel that keeps the stream busy
+ * for ns nanoseconds (the device counterpart of the reference's RuntimeStraggler sleeps). */
+int dsp_device_sleep(int64_t ns, void* stream);
 const char* dsp_last_error(void);
 int dsp_abi_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */

@@ -41,6 +41,7 @@ from .pipeline import (
     ActivationPacket,
     ConfigError,
     DeadlockError,
+    DeviceStraggler,
     GradPacket,
     LogRecord,
     PipelineConfig,
@@ -64,5 +65,5 @@ __all__ = [
     "default_queue_config", "dense", "derive_seed", "flop_balanced_boundaries", "init_params", "lr_at", "maxpool",
     "mix64", "relu", "resnet50_layers", "resnet_cifar_bottleneck_layers", "resnet_cifar_layers", "sgd_step",
     "staleness_of", "suggest_boundaries", "sum_step", "tanh", "validate_config",
-    "Dataset", "TeacherSpec", "batch_iter", "epoch_stream", "gen_teacher_dataset", "DeviationRow", "DeviceOperators",
+    "Dataset", "TeacherSpec", "batch_iter", "epoch_stream", "gen_teacher_dataset", "DeviationRow", "DeviceOperators", "DeviceStraggler",
 ]

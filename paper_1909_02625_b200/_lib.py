@@ -153,6 +153,7 @@ _SIGNATURES = {
     "dsp_read_log": (C.c_int, [_P, C.POINTER(LogRecordC), C.c_size_t, C.POINTER(C.c_size_t)]),
     "dsp_steps_done": (C.c_int64, [_P]),
     "dsp_destroy": (None, [_P]),
+    "dsp_device_sleep": (C.c_int, [C.c_int64, _P]),
     "dsp_synth_batch": (C.c_int, [C.c_uint64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_int, _P, C.POINTER(C.c_int64), _P]),
 }

@@ -68,6 +68,13 @@ __global__ void synth_labels_k(uint64_t seed, uint64_t base, int B, int C, int64
   out[b] = l < C - 1 ? l : C - 1;
 }
 
+// Straggler injection: one thread spins on %globaltimer for ns nanoseconds on the stream.
+__global__ void device_sleep_k(int64_t ns) {
+  pdl_wait();
+  const uint64_t t0 = globaltimer_ns();
+  while ((int64_t)(globaltimer_ns() - t0) < ns) __nanosleep(256);
+}
+
 uint64_t mix64_host(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -107,5 +114,13 @@ extern "C" int dsp_synth_batch(uint64_t seed, int64_t batch_no, int batch, int c
     note_launch();
     DSP_CUDA(cudaGetLastError());
   }
+  return DSP_OK;
+}
+
+extern "C" int dsp_device_sleep(int64_t ns, void* stream) {
+  if (ns < 0) return set_error(DSP_E_INVALID, "dsp_device_sleep: negative duration");
+  if (ns == 0) return DSP_OK;
+  DSP_CUDA(launch_k(device_sleep_k, 1, 1, 0, (cudaStream_t)stream, ns));
+  note_launch();
   return DSP_OK;
 }

@@ -136,6 +136,10 @@ class B200Runtime:
             return self._block_streams[k]
         return self.stream
 
+    def device_sleep(self, k: int, seconds: float) -> None:
+        """Straggler delay on block k's stream (DeviceStraggler)."""
+        L.check(L.load().dsp_device_sleep(int(seconds * 1e9), stream_ptr(self._s(k))))
+
     def fork_blocks(self) -> None:
         """Eager step start: every block stream waits for the main stream (inputs staged, the
         previous step and its exchange done)."""

@@ -216,6 +216,25 @@ class RuntimeStraggler:
             time.sleep(self.delay_s)
 
 
+@dataclass
+class DeviceStraggler(RuntimeStraggler):
+    """RuntimeStraggler's seeded decisions, with the delay injected on the block's device stream
+    (dsp_device_sleep) -- it slows the GPU work itself, like a straggling worker, and never changes
+    values. Runs with eager steps: the per-step decisions vary."""
+
+    def hits(self, block: int, step: int, phase: int) -> bool:
+        z = mix64(self.seed ^ mix64((block + 1) * 0x9E37 + step * 2 + phase))
+        return (z >> 11) * 2.0**-53 < self.prob
+
+    def sleep_maybe(self, block: int, step: int, phase: int, rt=None) -> None:
+        if not self.hits(block, step, phase):
+            return
+        if rt is None:
+            time.sleep(self.delay_s)
+        else:
+            rt.device_sleep(block, self.delay_s)
+
+
 def default_placement(k: int, world: int) -> list[int]:
     """Contiguous blocks per rank: K blocks over `world` ranks (one block per GPU when K == world)."""
     if world <= 1:
@@ -356,7 +375,9 @@ class TrainEngine:
         self.in_queues[k].put(fresh)
         stale = self.in_queues[k].get()
 
-        if self.straggler is not None:
+        if isinstance(self.straggler, DeviceStraggler):
+            self.straggler.sleep_maybe(k, n, 0, rt)
+        elif self.straggler is not None:
             self.straggler.sleep_maybe(k, n, 0)
 
         tr = self.tracker
@@ -396,7 +417,9 @@ class TrainEngine:
             if track_stale:
                 up_norm = rt.xent_grad_norm(logits, stale.labels)
 
-        if self.straggler is not None:
+        if isinstance(self.straggler, DeviceStraggler):
+            self.straggler.sleep_maybe(k, n, 1, rt)
+        elif self.straggler is not None:
             self.straggler.sleep_maybe(k, n, 1)
 
         grad_in = rt.backward(k, upstream, k > 0, n)
@@ -465,7 +488,8 @@ class TrainEngine:
     def run(self, n_steps: int) -> None:
         if n_steps < 0:
             raise ValueError("n_steps must be non-negative")
-        graphs = getattr(self.rt, "use_graphs", False) and self._transport.world <= 1 and self.tracker is None
+        graphs = (getattr(self.rt, "use_graphs", False) and self._transport.world <= 1 and self.tracker is None
+                  and not isinstance(self.straggler, DeviceStraggler))
         for _ in range(n_steps):
             n = self.block_steps[self.local[0]] if self.local else 0
             if graphs and n >= self._graph_horizon():
@@ -568,7 +592,7 @@ def model_forward(model: Model, x: np.ndarray) -> np.ndarray:
 
 __all__ = [
     "ActivationPacket", "ConfigError", "DeadlockError", "GradPacket", "LogRecord", "PipelineConfig",
-    "ProtocolError", "RuntimeStraggler", "ShapeError", "StalenessProfile", "TrainEngine", "TrainLog",
+    "ProtocolError", "RuntimeStraggler", "DeviceStraggler", "ShapeError", "StalenessProfile", "TrainEngine", "TrainLog",
     "WARMUP_POLICIES", "default_placement", "default_queue_config", "model_forward", "staleness_of",
     "validate_config",
 ]

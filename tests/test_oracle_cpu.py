@@ -192,3 +192,26 @@ def test_theory_port_matches_reference(stalepipe):
         assert T.lemma1_report(rows, LL, MM) == RT.lemma1_report(rows, LL, MM)
     assert T.lemma_bound_rhs(2.0, 3.0, [1.0, 0.5, 0.25]) == RT.lemma_bound_rhs(2.0, 3.0, [1.0, 0.5, 0.25])
     assert T.lemma1_report(rows, L, M)["holds_fraction"] == 1.0
+
+
+def test_des_restatement_matches_reference(stalepipe):
+    """calibrate.simulate_dsp / simulate_bp vs the reference's simulate.py on the same costs."""
+    import importlib
+
+    from paper_1909_02625_b200 import calibrate as CAL
+
+    S = importlib.import_module("stalepipe.simulate")
+    import paper_1909_02625_b200 as P
+
+    f, b = (1.0, 2.5, 0.7, 1.3), (2.0, 3.1, 1.9, 2.2)
+    for p, m in (((1, 1, 1, 0), (6, 4, 2, 0)), ((2, 1, 1, 0), (7, 4, 2, 0))):
+        cfg_ref = stalepipe.validate_config(p, m)
+        ref, _ = S.simulate("dsp", S.CostModel(f, b, transfer_cost=0.05), 40, cfg_ref)
+        mine = CAL.simulate_dsp(f, b, P.validate_config(p, m), 40, link=0.05)
+        assert mine["makespan"] == ref.makespan and mine["steady_interval"] == ref.steady_interval
+        strag = S.StragglerModel(prob=0.3, rho=0.5, seed=4)
+        ref2, _ = S.simulate("dsp", S.CostModel(f, b), 40, cfg_ref, strag)
+        mult = CAL.straggler_multipliers(4, 40, 0.3, 0.5, seed=4)
+        assert CAL.simulate_dsp(f, b, P.validate_config(p, m), 40, mult=mult)["makespan"] == ref2.makespan
+        ref3, _ = S.simulate("sync_bp", S.CostModel(f, b), 40, None, strag)
+        assert CAL.simulate_bp(f, b, 40, mult=mult)["makespan"] == ref3.makespan
