@@ -83,14 +83,17 @@ constexpr bool kTrace = false;
 
 template <int BN>
 struct IgCfg {
-  static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 3);
+  static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 4);
   static constexpr int RING = STAGES * (IG_BM * 128 + BN * 128);
 #ifdef IG_TMA_STORE
   static constexpr int OUT_BYTES = IG_BM * BN * 2;  // bf16 output tile staged for the TMA store
 #else
   static constexpr int OUT_BYTES = 0;
 #endif
-  static constexpr int SMEM = RING + OUT_BYTES;
+  // wide tiles: per-epilogue-warp double-buffered 32-row x 16-column bf16 staging slabs for
+  // TMA stores (8 warps x 2 x 1 KB)
+  static constexpr int DW_BYTES = BN >= 128 ? 8 * 2 * 1024 : 0;
+  static constexpr int SMEM = RING + OUT_BYTES + DW_BYTES;
   static constexpr int NACC = BN <= 128 ? 4 : 2;  // TMEM accumulators: MMA runs NACC-1 tiles ahead
   static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
   static constexpr int BY_SMEM = SMEM <= 70 * 1024 ? 3 : SMEM <= 100 * 1024 ? 2 : 1;
@@ -102,7 +105,8 @@ struct IgCfg {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <int NT>
+__device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
 // Column sums of a 32-row x 16-column register tile (one row per lane) with 16
 // shuffles: halve the column set at each butterfly step. Lane l ends holding the
@@ -184,6 +188,12 @@ struct IgTma {
   int h_nwb;    // resident weight boxes of 64 K x BN (SWIZZLE_128B)
   int h_rowb;   // bytes per A row (C * 2)
   int h_swz;    // UMMA layout type of A
+  // im2col-mode A (any output width; FPROP stride 1/2, stride-1 DGRAD on dY with the per-tap
+  // transposed weights B_t, WGRAD): one box of 128 (WGRAD: 64) consecutive output pixels x 64
+  // channels per (tap, channel chunk); the tap is the instruction's im2col offset
+  int i2c;
+  int d_warp;   // wide-tile epilogue: per-warp 32 x 16 slabs staged in smem, TMA-stored (box {16, 32})
+  int i2c_pad;  // start coordinate of output pixel (p, q) = (p * st - i2c_pad, q * st - i2c_pad)
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
   // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
   uint32_t fd_d[5], fd_mul[5], fd_shr[5];
@@ -205,25 +215,30 @@ static void fastdiv_host(uint32_t d, uint32_t& mul, uint32_t& shr) {
 // threads), 1 when every operand comes through TMA (one lane issues the boxes).
 // Registers are budgeted as if REG_BLOCKS CTAs shared an SM, leaving room for the other
 // block streams' kernels beside a conv CTA (<= 75 regs at 288 threads, <= 68 at 192).
-template <int NPW>
+template <int NPW, int BN>
 struct IgWarps {
-  static constexpr int THREADS = (NPW + 5) * 32;
+  // 8 epilogue warps (two per TMEM lane quadrant, each half the columns) for the wide tiles of
+  // the tensor-bound shapes, whose epilogue would otherwise bound small-Kd (1x1) convs
+  static constexpr int NEPI = BN >= 128 ? 8 : 4;
+  static constexpr int THREADS = (NPW + 1 + NEPI) * 32;
   static constexpr int MMA_WARP = NPW;
   static constexpr int EPI_WARP0 = NPW + 1;
-  static constexpr int REG_BLOCKS = NPW == 4 ? IG_REG_BLOCKS : IG_REG_BLOCKS + 2;
+  static constexpr int REG_BLOCKS = BN >= 128 ? 1 : (NPW == 4 ? IG_REG_BLOCKS : IG_REG_BLOCKS + 2);
 };
 
 template <typename T, int MODE, int BN, int NPW>
-__global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM
-                                                             ? IgWarps<NPW>::REG_BLOCKS
+__global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM
+                                                             ? IgWarps<NPW, BN>::REG_BLOCKS
                                                              : IgCfg<BN>::CTAS_PER_SM)
     igemm_kernel(const dsp_igemm_args_t a, const __grid_constant__ CUtensorMap tmA,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmD,
                  const IgTma tm) {
   using Cfg = IgCfg<BN>;
-  constexpr int IG_THREADS = IgWarps<NPW>::THREADS;
-  constexpr int IG_MMA_WARP = IgWarps<NPW>::MMA_WARP;
-  constexpr int IG_EPI_WARP0 = IgWarps<NPW>::EPI_WARP0;
+  constexpr int IG_THREADS = IgWarps<NPW, BN>::THREADS;
+  constexpr int IG_MMA_WARP = IgWarps<NPW, BN>::MMA_WARP;
+  constexpr int IG_EPI_WARP0 = IgWarps<NPW, BN>::EPI_WARP0;
+  constexpr int NEPI = IgWarps<NPW, BN>::NEPI;
+  constexpr int EPI_T = NEPI * 32;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NACC = Cfg::NACC;
   constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     }
     for (int s = 0; s < NACC; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], EPI_T);
     }
     mbar_init(&wbar, 1);
     fence_barrier_init();
@@ -381,8 +396,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     int gcount = 0;
     int m0, n0, z, kb0, kb1;
     for (int j = 0; get_unit(j, m0, n0, z, kb0, kb1); ++j) {
-      const int t_n0 = m0 / out_hw;              // TMA tile origin: image, output row
+      const int t_n0 = m0 / out_hw;              // TMA tile origin: image, output row, column
       const int t_h0 = (m0 - t_n0 * out_hw) / out_w;
+      const int t_q0 = m0 - t_n0 * out_hw - t_h0 * out_w;
       // per-tile A-row precompute
       int a_h[8], a_w[8], a_img[8];
       int wg_r = 0, wg_s = 0, wg_c = 0;
@@ -434,7 +450,49 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
           continue;
         }
         // ---------------- A operand ----------------
-        if (tm.on_a && MODE == DSP_IGEMM_WGRAD) {
+        if (tm.i2c && MODE == DSP_IGEMM_WGRAD) {
+          // k-block = 64 output pixels from kb*KS on (crossing rows / images); A boxes = one per
+          // 64-channel M group (tap, c0) as im2col offsets; B = dY [pixels][K] 2-D boxes
+          const int nbox_a = IG_BM / tm.cbox, nbox_b = BN / tm.cbox_b;
+          if (warp == 0) {
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(nbox_a * tm.box_a + nbox_b * tm.box_b));
+            __syncwarp();
+            if (lane < nbox_a) {
+              int rem, kq;
+              const int kn = fd_pix.divmod(kb * KS, rem);
+              const int kh = fd_row.divmod(rem, kq);
+              const int mm = m0 + lane * tm.cbox;
+              int c0 = 0, rr = 0, ss2 = 0;
+              if (mm < M) {
+                const int tap = fd_ch.divmod(mm, c0);
+                rr = fd_s.divmod(tap, ss2);
+              }
+              // rows past R*S*C read channels >= C: zero filled (their D rows are never stored)
+              tma_load_im2col_4d(sA + lane * tm.box_a, &tmA, &full_bar[s], mm < M ? c0 : g.C,
+                                 kq * g.stride - tm.i2c_pad, kh * g.stride - tm.i2c_pad, kn, (uint16_t)ss2,
+                                 (uint16_t)rr);
+            } else if (lane >= 32 - nbox_b) {
+              const int jb = lane - (32 - nbox_b);
+              tma_load_2d(sB + jb * tm.box_b, &tmB, &full_bar[s], n0 + jb * tm.cbox_b, kb * KS);
+            }
+          }
+        } else if (tm.i2c) {
+          // one im2col box (128 output pixels x 64 channels of one tap) + one weight box
+          if (warp == 0 && lane == 0) {
+            mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(tm.box_a + tm.box_b));
+            const int k0 = kb * KS;
+            int c0, ss2;
+            const int tap = fd_ch.divmod(k0, c0);
+            const int rr = fd_s.divmod(tap, ss2);
+            const int st2 = MODE == DSP_IGEMM_FPROP ? g.stride : 1;
+            // DGRAD = conv of dY with the flipped kernel: weight tap (r, s) meets offset (R-1-r, S-1-s)
+            const int ow = MODE == DSP_IGEMM_FPROP ? ss2 : g.S - 1 - ss2;
+            const int oh = MODE == DSP_IGEMM_FPROP ? rr : g.R - 1 - rr;
+            tma_load_im2col_4d(sA, &tmA, &full_bar[s], c0, t_q0 * st2 - tm.i2c_pad, t_h0 * st2 - tm.i2c_pad, t_n0,
+                               (uint16_t)ow, (uint16_t)oh);
+            tma_load_2d(sB, &tmB, &full_bar[s], k0, n0);
+          }
+        } else if (tm.on_a && MODE == DSP_IGEMM_WGRAD) {
           // WGRAD: k-block = 64 output pixels; A box j = tap-shifted X pixels x cbox
           // channels of MN range [m0 + j*cbox, +cbox); B box j = dY pixels x cbox_b
           const int nbox_a = IG_BM / tm.cbox, nbox_b = BN / tm.cbox_b;
@@ -648,7 +706,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
   } else if (warp == IG_MMA_WARP) {
     // =============================== MMA issuer ===============================
     if (lane == 0) {
-      const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, A_MN ? 1u : 0u, B_MN ? 1u : 0u, IG_BM, BN);
+      // im2col DGRAD reads the transposed weights B_t [C][R][S][K]: K-major like FPROP
+      const bool b_mn = B_MN && !(tm.i2c && MODE == DSP_IGEMM_DGRAD);
+      const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, A_MN ? 1u : 0u, b_mn ? 1u : 0u, IG_BM, BN);
       constexpr int NKK = KS / MmaTraits<T>::MMA_K;
       // descriptor templates (start address 0) and per-MMA byte offsets, hoisted
       // out of the loop: the issuing thread only adds the stage base.
@@ -730,9 +790,15 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     // =============================== epilogue ===============================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;
-    const int et = tid - IG_EPI_WARP0 * 32;  // 0..127
+    const int et = tid - IG_EPI_WARP0 * 32;  // 0..EPI_T-1
+    const int half = (warp - IG_EPI_WARP0) >> 2;  // column half (8 epilogue warps)
     const bool tma_out = Cfg::OUT_BYTES > 0 && MODE != DSP_IGEMM_WGRAD && sizeof(T) == 2 && tm.on_d;
     const uint32_t sOut = sA0 + Cfg::RING;  // 1024-aligned staging tile, boxes of 128 x d_cols
+    // per-warp slab staging (wide tiles): slab = 32 rows x 32 B, two per warp
+    const bool dw = Cfg::DW_BYTES > 0 && NEPI == 8 && MODE != DSP_IGEMM_WGRAD && sizeof(T) == 2 && tm.d_warp &&
+                    !(a.out_f32 & 1);
+    const uint32_t sDW = sA0 + Cfg::RING + Cfg::OUT_BYTES + (uint32_t)(warp - IG_EPI_WARP0) * 2048;
+    int dwc = 0;  // slabs this warp has staged
     int i = 0;
     int m0, n0, z, kb0, kb1;
     for (; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
@@ -742,15 +808,28 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
       tc_fence_after();
       if (tma_out && i > 0) {  // the previous tile's store must have read the staging tile
         if (et == 0) bulk_wait_read0();
-        epi_barrier();
+        epi_barrier<EPI_T>();
       }
       const int m = m0 + row;
       const bool mok = m < M;
       const uint32_t tl = tmem_d + acc * BN + ((uint32_t)(q * 32) << 16);
+      // each warp: CPW 16-column chunks of its half; wide tiles load 32 TMEM columns per wait
+      constexpr int CPW = BN / 16 / (NEPI / 4);
+      constexpr int LDW = (BN >= 128 && CPW % 2 == 0) ? 2 : 1;
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 16; ++cc) {
+      for (int c2 = 0; c2 < CPW; c2 += LDW) {
+        float vb[16 * LDW];
+        if constexpr (LDW == 2) {
+          tmem_ld32(tl + (half * CPW + c2) * 16, vb);
+        } else {
+          tmem_ld16(tl + (half * CPW + c2) * 16, vb);
+        }
+#pragma unroll
+        for (int h = 0; h < LDW; ++h) {
+        const int cc = half * CPW + c2 + h;
         float v[16];
-        tmem_ld16(tl + cc * 16, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = vb[h * 16 + e];
         const int nb = n0 + cc * 16;
         if (MODE == DSP_IGEMM_WGRAD) {
           float* out = reinterpret_cast<float*>(a.D) + (size_t)z * M * N + (size_t)m * N;
@@ -799,6 +878,60 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
               for (int e = 0; e < 16; ++e)
                 if (nb + e < N) out[nb + e] = v[e];
             }
+          } else if (dw) {
+            // stage this warp's 32 x 16 slab (row = lane) in smem, then store it row-contiguously:
+            // lane = (row l >> 1 (+16), 16-byte half l & 1), so each warp store writes 16 whole
+            // 32-byte sectors instead of 32 half sectors in 32 rows
+            const uint32_t buf = sDW + (uint32_t)(dwc & 1) * 1024;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = to_f<T>(from_f<T>(v[e]));
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              uint4 raw;
+              T* e8 = reinterpret_cast<T*>(&raw);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) e8[e] = from_f<T>(v[hh * 8 + e]);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 32 + hh * 16), "r"(raw.x),
+                           "r"(raw.y), "r"(raw.z), "r"(raw.w)
+                           : "memory");
+            }
+            __syncwarp();
+            {
+              const int rvalid = M - (m0 + q * 32);
+#pragma unroll
+              for (int k2 = 0; k2 < 2; ++k2) {
+                const int r = (lane >> 1) + 16 * k2;
+                uint4 raw;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                             : "r"(buf + r * 32 + (lane & 1) * 16));
+                if (r < rvalid && nb < N)  // N % 16 == 0: a slab is wholly inside or outside
+                  *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(m0 + q * 32 + r) * a.ldd + nb +
+                                            (lane & 1) * 8) = raw;
+              }
+            }
+            if (want_stats && MODE == DSP_IGEMM_FPROP) {
+              // column sums from the staged slab: lane = (column l & 15, row parity l >> 4)
+              const int col = lane & 15;
+              float s1 = 0.f, s2 = 0.f;
+              const int rvalid = M - (m0 + q * 32);  // rows of this slab inside M
+#pragma unroll
+              for (int r2 = 0; r2 < 16; ++r2) {
+                const int r = (lane >> 4) + 2 * r2;
+                uint16_t raw16;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=h"(raw16) : "r"(buf + r * 32 + col * 2));
+                const float y = r < rvalid ? __bfloat162float(__ushort_as_bfloat16(raw16)) : 0.f;
+                s1 += y;
+                s2 = fmaf(y, y, s2);
+              }
+              s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+              s2 += __shfl_xor_sync(0xffffffffu, s2, 16);
+              if (lane < 16) {
+                red[q][cc * 16 + col][0] += s1;
+                red[q][cc * 16 + col][1] += s2;
+              }
+            }
+            ++dwc;
           } else if (tma_out) {
             // round to bf16 (BN statistics describe the stored tensor) and stage two 16-byte
             // chunks of this row in the TMA swizzle pattern (conflict-free across lanes)
@@ -840,7 +973,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
               }
             }
           }
-          if (want_stats && MODE == DSP_IGEMM_FPROP) {
+          if (want_stats && MODE == DSP_IGEMM_FPROP && dw) {
+            // accumulated from the staged slab above
+          } else if (want_stats && MODE == DSP_IGEMM_FPROP) {
             float sq[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -883,12 +1018,13 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
             }
           }
         }
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (tma_out) {  // whole tile staged: one thread stores it (rows >= M / cols >= N are clipped)
         fence_proxy_async_smem();
-        epi_barrier();
+        epi_barrier<EPI_T>();
         if (et == 0) {
           for (int b = 0; b * tm.d_cols < BN; ++b)
             tma_store_2d(&tmD, sOut + b * (IG_BM * tm.d_cols * 2), n0 + b * tm.d_cols, m0);
@@ -899,9 +1035,9 @@ __global__ void __launch_bounds__(IgWarps<NPW>::THREADS, IgWarps<NPW>::REG_BLOCK
     }
     if (tma_out && et == 0) bulk_wait0();
     if (want_stats) {
-      epi_barrier();
+      epi_barrier<EPI_T>();
       const int n0c = (blockIdx.x % nt) * BN;
-      for (int c = et; c < BN; c += 128) {
+      for (int c = et; c < BN; c += EPI_T) {
         const int n = n0c + c;
         if (n < N) {
           for (int k = 0; k < NS; ++k)
@@ -1045,7 +1181,102 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+static PFN_cuTensorMapEncodeIm2col_v12000 im2col_encoder() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  }
+  return fn;
+}
+
 constexpr int IG_HALO_SMEM_MAX = 100 * 1024;  // keeps two conv CTAs per SM
+
+// im2col-mode A operand (any output width, 64-channel multiples): FPROP (stride 1/2) on X,
+// stride-1 DGRAD on dY with the transposed weights B_t (flipped-kernel conv, padding R-1-pad),
+// WGRAD on X (64-pixel k-blocks) with dY as a plain [pixels][K] matrix. The tensor map's
+// bounding box per image is [-pad, dim + pad - (R-1)) in W and H, walked with the conv stride,
+// so the n-th pixel of a box is output pixel m0 + n whatever the rows / images it crosses.
+template <int MODE, int BN>
+static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB,
+                     PFN_cuTensorMapEncodeTiled_v12000 enc) {
+  static const bool disabled = getenv("DSP_B200_NO_IM2COL") != nullptr;
+  PFN_cuTensorMapEncodeIm2col_v12000 enc2 = im2col_encoder();
+  const dsp_conv_geom_t& g = a.geom;
+  if (disabled || enc2 == nullptr || g.R != g.S) return false;
+  const int st = MODE == DSP_IGEMM_DGRAD ? 1 : g.stride;
+  if (MODE == DSP_IGEMM_DGRAD && (g.stride != 1 || a.B_t == nullptr)) return false;
+  if (st != 1 && st != 2) return false;
+  const int cdim = MODE == DSP_IGEMM_DGRAD ? g.K : g.C;  // channels of the im2col'd tensor
+  if (cdim % 64) return false;
+  const int pad = MODE == DSP_IGEMM_DGRAD ? g.R - 1 - g.pad : g.pad;
+  if (pad < 0 || pad > 64 || g.R > 64) return false;
+  const int ih = MODE == DSP_IGEMM_DGRAD ? g.P : g.H, iw = MODE == DSP_IGEMM_DGRAD ? g.Q : g.W;
+  const int oh = MODE == DSP_IGEMM_DGRAD ? g.H : g.P, ow = MODE == DSP_IGEMM_DGRAD ? g.W : g.Q;
+  const int lo = -pad, hi = pad - (g.R - 1);
+  // positions walked per row / column must be exactly the output extent
+  if ((iw + hi - lo + st - 1) / st != ow || (ih + hi - lo + st - 1) / st != oh) return false;
+  const void* asrc = a.A;
+  const void* bsrc = MODE == DSP_IGEMM_DGRAD ? a.B_t : a.B;
+  if ((reinterpret_cast<uintptr_t>(asrc) & 15) || (reinterpret_cast<uintptr_t>(bsrc) & 15)) return false;
+  const int ppc = MODE == DSP_IGEMM_WGRAD ? 64 : IG_BM;
+  cuuint64_t dims[4] = {(cuuint64_t)cdim, (cuuint64_t)iw, (cuuint64_t)ih, (cuuint64_t)g.nimg};
+  cuuint64_t strides[3] = {(cuuint64_t)cdim * 2, (cuuint64_t)iw * cdim * 2, (cuuint64_t)ih * iw * cdim * 2};
+  int lower[2] = {lo, lo}, upper[2] = {hi, hi};
+  cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+  if (enc2(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(asrc), dims, strides, lower, upper, 64,
+           (cuuint32_t)ppc, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (MODE == DSP_IGEMM_WGRAD) {
+    const int cb = std::min(std::min(g.K, 64), BN);
+    if ((cb != 16 && cb != 32 && cb != 64) || g.K % cb || BN % cb) return false;
+    const int64_t npix = (int64_t)g.nimg * g.P * g.Q;
+    cuuint64_t bd[2] = {(cuuint64_t)g.K, (cuuint64_t)npix};  // dY [pixels][K]
+    cuuint64_t bs[1] = {(cuuint64_t)g.K * 2};
+    cuuint32_t bb[2] = {(cuuint32_t)cb, 64};
+    cuuint32_t be[2] = {1, 1};
+    const CUtensorMapSwizzle swz = cb == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                   : cb == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
+    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.B), bd, bs, bb, be,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    tm.on_a = tm.on_b = 1;
+    tm.i2c = 1;
+    tm.i2c_pad = pad;
+    tm.cbox = 64;
+    tm.box_a = 64 * 64 * 2;
+    tm.swz_a = 2;
+    tm.cbox_b = cb;
+    tm.box_b = 64 * cb * 2;
+    tm.swz_b = cb == 16 ? 6 : cb == 32 ? 4 : 2;
+    return true;
+  }
+  if (a.Kd % 64) return false;
+  cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)a.N};  // FPROP W [Cout][Kd]; DGRAD B_t [C][Kd]
+  cuuint64_t bs[1] = {(cuuint64_t)a.Kd * 2};
+  cuuint32_t bb[2] = {64, (cuuint32_t)BN};
+  cuuint32_t be[2] = {1, 1};
+  if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(bsrc), bd, bs, bb, be,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  tm.on_a = tm.on_b = 1;
+  tm.i2c = 1;
+  tm.i2c_pad = pad;
+  tm.cbox = 64;
+  tm.box_a = IG_BM * 128;
+  tm.swz_a = 2;
+  tm.box_b = BN * 128;
+  return true;
+}
 
 // FPROP halo tiles: stride-1 'same' RxS conv, C in {16, 32, 64} (one A box covers all
 // channels), output rows of 8k pixels with a 128-pixel tile = hb whole rows of one image.
@@ -1104,19 +1335,9 @@ static bool halo_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CU
   return true;
 }
 
-// Decide whether this launch's A (and B) operands can be fetched with TMA and
-// build the tensor maps. A: bf16 FPROP (stride 1/2) or stride-1 DGRAD whose
-// 128-row M tile is a whole box of output pixels (OW | 128 and the rows fit
-// the image, or whole images). B: FPROP weights [Cout_p][Kd].
-template <typename T, int MODE, int BN>
-static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB) {
-  tm = IgTma{};
-  memset(&tmA, 0, sizeof(tmA));
-  memset(&tmB, 0, sizeof(tmB));
-  static const bool disabled = getenv("DSP_B200_NO_TMA") != nullptr;
-  if (disabled || sizeof(T) != 2) return;
-  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-  if (enc == nullptr) return;
+template <int BN>
+static void tma_plan_wgrad_tiled(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB,
+                                 PFN_cuTensorMapEncodeTiled_v12000 enc) {
   const dsp_conv_geom_t& g = a.geom;
   auto swz_of = [](int cbox, int& umma) {
     umma = cbox == 8 ? 0 : cbox == 16 ? 6 : cbox == 32 ? 4 : 2;
@@ -1125,7 +1346,7 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
            : cbox == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                         : CU_TENSOR_MAP_SWIZZLE_128B;
   };
-  if (MODE == DSP_IGEMM_WGRAD) {
+  {
     // k-block = 64 output pixels = Q x rows x imgs; A = X boxes per (tap, channel chunk), B = dY boxes
     if (g.stride != 1 && g.stride != 2) return;
     const int ca = std::min(g.C, 64), cb = std::min(std::min(g.K, 64), BN);
@@ -1170,7 +1391,12 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
     tm.kb_imgs = imgs;
     return;
   }
-  if (MODE != DSP_IGEMM_WGRAD && halo_plan<MODE, BN>(a, tm, tmA, tmB, enc)) return;
+}
+
+template <int MODE, int BN>
+static void tma_plan_tiled(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB,
+                           PFN_cuTensorMapEncodeTiled_v12000 enc) {
+  const dsp_conv_geom_t& g = a.geom;
   if (MODE == DSP_IGEMM_DGRAD && g.stride != 1) return;
   if (g.stride != 1 && g.stride != 2) return;
   const int cdim = MODE == DSP_IGEMM_FPROP ? g.C : g.K;  // channels of the gathered tensor
@@ -1221,6 +1447,34 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   }
 }
 
+// Decide whether this launch's A (and B) operands can be fetched with TMA and build the
+// tensor maps: FPROP / DGRAD halo tiles, else tiled boxes when a 128-row M tile is whole output
+// rows (OW | 128) or images, else im2col mode (64-channel multiples); WGRAD tiled, else im2col.
+template <typename T, int MODE, int BN>
+static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUtensorMap& tmB) {
+  tm = IgTma{};
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  static const bool disabled = getenv("DSP_B200_NO_TMA") != nullptr;
+  if (disabled || sizeof(T) != 2) return;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (enc == nullptr) return;
+  if (MODE == DSP_IGEMM_WGRAD) {
+    tma_plan_wgrad_tiled<BN>(a, tm, tmA, tmB, enc);
+  } else if (!halo_plan<MODE, BN>(a, tm, tmA, tmB, enc)) {
+    tma_plan_tiled<MODE, BN>(a, tm, tmA, tmB, enc);
+  }
+  if (!(tm.on_a && tm.on_b)) {
+    IgTma t2{};
+    CUtensorMap a2, b2;
+    if (i2c_plan<MODE, BN>(a, t2, a2, b2, enc)) {
+      tm = t2;
+      tmA = a2;
+      tmB = b2;
+    }
+  }
+}
+
 // D through TMA stores: bf16 FPROP / DGRAD outputs with 16-byte aligned rows.
 template <typename T, int MODE, int BN>
 static void tma_out_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
@@ -1247,6 +1501,19 @@ static void tma_out_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD)
   tm.on_d = 1;
   tm.d_cols = cols;
   tm.d_swz = cols == 16 ? 1 : cols == 32 ? 3 : 7;
+}
+
+// Wide-tile epilogue stores (BN >= 128, bf16 FPROP / DGRAD): each epilogue warp stages
+// 32-row x 16-column slabs of the tile in smem and stores them row-contiguously (whole 32-byte
+// sectors per lane pair instead of 32 row-strided 16-byte stores per warp instruction).
+template <typename T, int MODE, int BN>
+static void dwarp_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
+  static const bool disabled = getenv("DSP_B200_NO_DWARP") != nullptr;
+  if (disabled || tm.halo || IgCfg<BN>::DW_BYTES == 0 || MODE == DSP_IGEMM_WGRAD || sizeof(T) != 2 || (a.out_f32 & 1))
+    return;
+  if ((reinterpret_cast<uintptr_t>(a.D) & 15) || (a.ldd % 8) || a.N % 16 || a.ldd < a.N) return;
+  (void)tmD;
+  tm.d_warp = 1;
 }
 
 template <typename T, int MODE, int BN>
@@ -1281,6 +1548,7 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   CUtensorMap tmA, tmB, tmD;
   tma_plan<T, MODE, BN>(a, tm, tmA, tmB);
   tma_out_plan<T, MODE, BN>(a, tm, tmD);
+  if (!tm.on_d) dwarp_plan<T, MODE, BN>(a, tm, tmD);
   {
     const dsp_conv_geom_t& g = a.geom;
     const uint32_t divs[5] = {(uint32_t)(MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q),
@@ -1294,9 +1562,9 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
   const int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128 : Cfg::SMEM;
   if (tm.on_a && tm.on_b && !force4)  // nothing to gather: one producer warp
-    launch_k(igemm_kernel<T, MODE, BN, 1>, grid, IgWarps<1>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
+    launch_k(igemm_kernel<T, MODE, BN, 1>, grid, IgWarps<1, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
   else
-    launch_k(igemm_kernel<T, MODE, BN, 4>, grid, IgWarps<4>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
+    launch_k(igemm_kernel<T, MODE, BN, 4>, grid, IgWarps<4, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
   (void)splits;
   note_launch();
   return cudaGetLastError();

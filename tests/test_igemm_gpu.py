@@ -38,6 +38,12 @@ CASES = [
     (1, 16, 16, 64, 64, 3, 1, 1),       # C=64: SWIZZLE_128B rows
     (2, 16, 16, 16, 16, 5, 1, 2),       # 5x5: 4 halo rows
     (2, 16, 16, 32, 64, 1, 1, 0),       # 1x1: a single box per tile
+    # im2col-mode TMA (output width does not divide 128: tiles cross rows and images)
+    (2, 14, 14, 64, 128, 3, 1, 1),
+    (3, 7, 7, 128, 256, 3, 1, 1),       # BN=256, ragged last tile
+    (2, 28, 28, 64, 128, 3, 2, 1),      # stride 2
+    (2, 12, 12, 128, 64, 1, 2, 0),      # 1x1 stride-2 projection
+    (1, 20, 20, 64, 320, 1, 1, 0),      # two n-tiles of 256
 ]
 
 
