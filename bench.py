@@ -38,6 +38,26 @@ DEPTH = 56
 CLASSES = 10
 IN_SHAPE = (3, 32, 32)
 
+# --model: BASELINE.json configs this bench can run (configs[1] is the default bench line;
+# configs[2] asks for Adam, which the reference rejects -- optim.py:70-71 -- so it is not offered)
+MODELS = {
+    "resnet56": dict(cfg=1, depth=56, classes=10, in_shape=(3, 32, 32), batch=128,
+                     desc="ResNet-56 DSP K={K}, synthetic CIFAR-10-shaped 32x32x3, batch {B}"),
+    "resnet164": dict(cfg=3, depth=164, classes=100, in_shape=(3, 32, 32), batch=256,
+                      desc="ResNet-164 (bottleneck) DSP K={K}, synthetic CIFAR-100-shaped 32x32x3, batch {B}"),
+    "resnet50": dict(cfg=4, depth=50, classes=1000, in_shape=(3, 224, 224), batch=256,
+                     desc="ResNet-50 DSP K={K}, synthetic ImageNet-shaped 224x224x3, batch {B}, bf16 tensor-core convs"),
+}
+
+
+def select_model(args):
+    """Point the module-level workload constants at --model (default: configs[1], ResNet-56)."""
+    global DEPTH, CLASSES, IN_SHAPE
+    m = MODELS[args.model]
+    DEPTH, CLASSES, IN_SHAPE = m["depth"], m["classes"], m["in_shape"]
+    if not args.batch:
+        args.batch = m["batch"]
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -45,7 +65,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--batch", type=int, default=0, help="default: the config's batch (128 / 256)")
+    ap.add_argument("--model", default="resnet56", choices=sorted(MODELS))
     ap.add_argument("--k", type=int, default=0, help="DSP blocks (default 4, or 8 when --gpus 8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cuts", default="", help="block boundaries (layer indices), default FLOP-balanced")
@@ -63,7 +84,12 @@ def workload(args):
     import paper_1909_02625_b200 as P
 
     K = blocks_for(args)
-    layers = P.resnet_cifar_layers(DEPTH, CLASSES)
+    if args.model == "resnet50":
+        layers = P.resnet50_layers(CLASSES, IN_SHAPE)
+    elif args.model == "resnet164":
+        layers = P.resnet_cifar_bottleneck_layers(DEPTH, CLASSES)
+    else:
+        layers = P.resnet_cifar_layers(DEPTH, CLASSES)
     if getattr(args, "cuts", ""):
         bounds = [int(v) for v in args.cuts.split(",")]
     else:
@@ -73,8 +99,9 @@ def workload(args):
 
 
 def config_dict(args, K, world):
-    return {"workload": f"ResNet-{DEPTH} DSP K={K}, synthetic CIFAR-10-shaped 32x32x3, batch {args.batch}",
-            "model": f"resnet{DEPTH}-cifar", "global_batch": args.batch, "k_blocks": K,
+    m = MODELS[args.model]
+    return {"workload": m["desc"].format(K=K, B=args.batch), "baseline_config": m["cfg"],
+            "model": args.model if args.model == "resnet50" else f"{args.model}-cifar", "global_batch": args.batch, "k_blocks": K,
             "queues": "p_k=1, m_k=2(K-1-k)", "optimizer": "SUM momentum beta=0.9 s=1, lr 0.1, wd 5e-4",
             "parallelism": f"dsp-pipeline k{K} over {world} gpu(s)",
             "l2": "L2 flushed (256 MiB write) between timed steps; step working set > L2"}
@@ -169,12 +196,13 @@ def run_reference(args):
     if rank != 0:
         return 0
     K = blocks_for(args)
-    sub = min(args.batch, 32)
+    big = IN_SHAPE[1] > 32
+    sub = min(args.batch, 2 if big else 32)
     steps = max(1, args.steps)
-    warm = max(1, min(args.warmup, 3))
-    # bound the run to a few minutes: ~2.7 s per K=4 step at batch 32 on 8 cores
+    warm = max(1, min(args.warmup, 1 if big else 3))
+    # bound the run to a few minutes: ~2.7 s per ResNet-56 K=4 step at batch 32 on 8 cores
     budget_s = 150.0
-    est = 0.085 * sub
+    est = sub * {"resnet56": 0.085, "resnet164": 0.17, "resnet50": 3.0}.get(args.model, 0.1)
     if (steps + warm) * est > budget_s:
         steps = max(1, int(budget_s / est) - warm)
     v, dt, cpu_s = cpu_oracle_steps(args, steps, warm, sub)
@@ -204,7 +232,20 @@ def ncu_traffic():
         return None
 
 
-def kernel_roofline(torch, peaks, batch, live_us):
+def roofline_spec(model: str, batch: int) -> dict:
+    """The dominant conv of the model's step and how its roofline is read:
+    CIFAR stage-1 3x3 convs are HBM/latency-bound (bytes), ResNet-50's stage-3 3x3 is
+    tensor-bound (FLOPs)."""
+    if model == "resnet50":
+        H, C_, K = 14, 256, 256
+        return dict(nimg=batch, H=H, C=C_, K=K, bound="tensor", M=batch * H * H, Kd=9 * C_,
+                    kernel=f"igemm_kernel<bf16,FPROP,256> im2col (ResNet-50 stage-3 conv3x3 256->256 + BN stats, B={batch})")
+    H, C_, K = 32, 16, 16
+    return dict(nimg=batch, H=H, C=C_, K=K, bound="hbm", M=batch * H * H, Kd=9 * C_,
+                kernel=f"igemm_kernel<bf16,FPROP,16> halo (stage-1 conv3x3 16->16 + BN stats, B={batch})")
+
+
+def kernel_roofline(torch, peaks, batch, live_us, spec=None):
     """achieved = algorithmic bytes / the dominant kernel's average launch duration measured
     live in the timed steps (event pairs around each launch on its block stream, concurrent
     with the other blocks). Also timed alone on rotating buffers larger than L2 ("isolated")."""
@@ -214,8 +255,8 @@ def kernel_roofline(torch, peaks, batch, live_us):
 
     lib = L.load()
     st = torch.cuda.current_stream()
-    # stage-1 3x3 16->16 conv of ResNet-56 at B=128: the most frequent shape of the step
-    nimg, H, W, Cc, K = batch, 32, 32, 16, 16
+    spec = spec or roofline_spec("resnet56", batch)
+    nimg, H, W, Cc, K = spec["nimg"], spec["H"], spec["H"], spec["C"], spec["K"]
     M = nimg * H * W
     nbuf = max(2, int(2 * L2_BYTES // (M * Cc * 2)) + 1)
     xs = [torch.randn(M * Cc, device="cuda").bfloat16() for _ in range(nbuf)]
@@ -247,15 +288,27 @@ def kernel_roofline(torch, peaks, batch, live_us):
     t_iso = e0.elapsed_time(e1) / 1000.0 / reps
     algo = M * Cc * 2 + M * K * 2 + K * 9 * Cc * 2 + tiles * 2 * K * 4
     t = (sum(live_us) / len(live_us) / 1e6) if live_us else t_iso
+    timing = ((f"live: mean of {len(live_us)} launches in timed steps of the same workload (event pairs on "
+               "the block stream, concurrent with the other blocks; a probe pass after the value steps)")
+              if live_us else "isolated (probe found no launch)")
+    if spec["bound"] == "tensor":
+        flops = 2.0 * M * K * 9 * Cc
+        peak_key = "bf16_tflops_sustained" if ("bf16_tflops_sustained" in peaks and live_us) else "bf16_tflops"
+        peak = peaks.get(peak_key, peaks.get("bf16_tflops", 2250.0))
+        achieved = flops / t / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "kernel": spec["kernel"], "algorithmic_flops_per_launch": flops,
+                "launch_us": t * 1e6, "timing": timing, "isolated_launch_us": t_iso * 1e6,
+                "isolated_achieved": flops / t_iso / 1e12,
+                "isolated_frac": flops / t_iso / 1e12 / peaks.get("bf16_tflops", 2250.0),
+                "peak_source": f"MEASURED_PEAKS.json {peak_key}" if peak_key in peaks else "fallback 2250 TFLOP/s"}
     peak_key = "hbm_gbs_sustained" if ("hbm_gbs_sustained" in peaks and live_us) else "hbm_gbs"
     peak = peaks.get(peak_key, peaks.get("hbm_gbs", 6650.0))
     achieved = algo / t / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(), "kernel": "igemm_kernel<bf16,FPROP,16> (ResNet-56 stage-1 conv3x3 16->16 + BN stats, B=128)",
+            "traffic": ncu_traffic() if spec["M"] == 128 * 32 * 32 else None, "kernel": spec["kernel"],
             "algorithmic_bytes_per_launch": algo, "launch_us": t * 1e6,
-            "timing": (f"live: mean of {len(live_us)} launches in timed steps of the same workload (event pairs on "
-                       "the block stream, concurrent with the other blocks; a probe pass after the value steps)")
-                      if live_us else "isolated (probe found no launch)",
+            "timing": timing,
             "isolated_launch_us": t_iso * 1e6, "isolated_achieved": algo / t_iso / 1e9,
             "isolated_frac": algo / t_iso / 1e9 / peaks.get("hbm_gbs", 6650.0),
             "peak_source": f"MEASURED_PEAKS.json {peak_key}" if peak_key in peaks else "fallback 6650 GB/s"}
@@ -288,14 +341,15 @@ def run_b200(args):
     except Exception:
         pass
 
-    host_pool = synthetic_batches(16, args.batch, IN_SHAPE, CLASSES, seed=0)
+    npool = 16 if IN_SHAPE[1] <= 32 else 4  # ImageNet-shaped batches: 154 MB each on the host
+    host_pool = synthetic_batches(npool, args.batch, IN_SHAPE, CLASSES, seed=0)
     model = P.build_model(layers, bounds)
     P.init_params(model, 0)
     stream = torch.cuda.current_stream(dev)
     # device-resident pool generated on the GPU (csrc/synth.cu): bitwise the packed host pool
     from paper_1909_02625_b200.data import device_synthetic_batches
 
-    dev_pool = device_synthetic_batches(16, args.batch, IN_SHAPE, CLASSES, seed=0, device=dev, stream=stream)
+    dev_pool = device_synthetic_batches(npool, args.batch, IN_SHAPE, CLASSES, seed=0, device=dev, stream=stream)
     eng = P.TrainEngine(model, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(0.1), rule="sum",
                         beta=0.9, s=1.0, weight_decay=5e-4, device=dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
@@ -314,7 +368,7 @@ def run_b200(args):
         ev.record(stream)  # materialise the handles
     torch.cuda.synchronize()
     handles = (C.c_void_p * (2 * probe_pairs))(*[C.c_void_p(ev.cuda_event) for ev in probe_ev])
-    roof_m = args.batch * 32 * 32
+    spec = roofline_spec(args.model, args.batch)
 
     # warm up through the zero-prefill horizon and one capture of every step-graph phase
     warm = max(3, args.warmup, eng._graph_horizon() + getattr(eng.rt, "R", 0) + 1)
@@ -339,7 +393,7 @@ def run_b200(args):
     # the probe's event nodes never touch the timed steps above.
     live_us = []
     if world == 1:
-        lib.dsp_probe_arm(L.DSP_IGEMM_FPROP, 16, roof_m, handles, probe_pairs)
+        lib.dsp_probe_arm(L.DSP_IGEMM_FPROP | (spec["Kd"] << 8), spec["K"], spec["M"], handles, probe_pairs)
         for g in eng.rt.graphs.values():
             lib.dsp_graph_destroy(g[3])
         eng.rt.graphs.clear()
@@ -420,14 +474,16 @@ def run_b200(args):
                "d2h_bytes_per_step": d2h, "timing": how}
         del eng2, model2
 
-    roof = kernel_roofline(torch, peaks, args.batch, live_us) if rank == 0 else None
+    roof = kernel_roofline(torch, peaks, args.batch, live_us, spec) if rank == 0 else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            v, dt, cpu_s = cpu_oracle_steps(args, 3, 1, 32)
+            sub = 32 if IN_SHAPE[1] <= 32 else 2
+            v, dt, cpu_s = cpu_oracle_steps(args, 3 if sub > 2 else 1, 1, sub)
             cpu = {"value": v, "unit": UNIT, "cores": threads_used(), "kind": "port",
                    "sample": f"oracle/dsp_ref.py float64 DSP step (CPU restatement of the reference), ResNet-{DEPTH} "
-                             f"K={K}, 3 timed steps of a 32-sample sub-batch after 1 warmup ({dt:.1f} s)"}
+                             f"K={K}, {3 if sub > 2 else 1} timed step(s) of a {sub}-sample sub-batch after 1 warmup "
+                             f"({dt:.1f} s)"}
         except Exception as exc:  # the baseline must never sink the bench line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc!r}"}
     if rank == 0:
@@ -445,6 +501,7 @@ def run_b200(args):
 
 def main():
     args = parse()
+    select_model(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

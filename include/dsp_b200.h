@@ -270,7 +270,8 @@ void dsp_destroy(dsp_engine_t* eng);
 /* Live kernel timing (bench.py roofline): while armed, every dsp_igemm-class launch with
  * (mode, N, M) records events[2i] before and events[2i+1] after it on its own stream (also
  * inside CUDA-graph capture), i = 0, 1, ... up to n_pairs; dsp_probe_reset() restarts at 0 and
- * returns how many launches were probed. events: cudaEvent_t handles; NULL disarms. */
+ * returns how many launches were probed. events: cudaEvent_t handles; NULL disarms. mode: a
+ * DSP_IGEMM_* value in bits 0-7; bits 8+ (if nonzero) also require the launch's Kd to equal them. */
 int dsp_probe_arm(int mode, int n, int64_t m, void* const* events, int n_pairs);
 int dsp_probe_reset(void);
 

@@ -47,6 +47,22 @@ __device__ __forceinline__ void st16(T* p, const float (&v)[V16<T>::N]) {
   *reinterpret_cast<uint4*>(p) = raw;
 }
 
+// raw 16-byte load (converted later, so a thread can keep several loads in flight)
+template <typename T>
+__device__ __forceinline__ uint4 ldraw(const T* p) {
+  return *reinterpret_cast<const uint4*>(p);
+}
+template <typename T>
+__device__ __forceinline__ void cvt16(const uint4& raw, float (&v)[V16<T>::N]) {
+  const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+  for (int i = 0; i < V16<T>::N; ++i) v[i] = to_f<T>(e[i]);
+}
+
+// vectors per thread per grid-stride pass: tensors larger than one full-occupancy wave
+// (148 SMs x 2048 threads) keep UNR 16-byte loads per operand in flight per thread
+constexpr int kWave = 148 * 2048;
+
 template <typename F>
 cudaError_t dispatch_dtype(int dtype, F&& f) {
   if (dtype == DSP_DTYPE_BF16) return f(bf16{});
@@ -94,36 +110,76 @@ __global__ void bn_finalize_k(const float* __restrict__ part, int tiles, int Cp,
   }
 }
 
-template <typename T>
+template <typename T, int UNR>
 __global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
                            int64_t nvec, int Cp, int relu) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = v * VE;
-    const int c0 = (int)(e0 % Cp);
-    float a[VE];
-    ld16(y + e0, a);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // when the channel-vector count divides the block, every vector a thread visits has the
+  // same channels: scale / shift live in registers (no per-vector 64-bit modulo or loads)
+  const int CV = Cp / VE;
+  const bool fixc = (blockDim.x % CV) == 0;
+  float sc[VE], sh[VE], sc2[VE], sh2[VE];
+  if (fixc) {
+    const int c0 = (threadIdx.x % CV) * VE;
 #pragma unroll
-    for (int i = 0; i < VE; ++i) a[i] = a[i] * stat[2 * Cp + c0 + i] + stat[3 * Cp + c0 + i];
-    if (res != nullptr) {
-      float r[VE];
-      ld16(res + e0, r);
-#pragma unroll
-      for (int i = 0; i < VE; ++i) a[i] += r[i];
+    for (int i = 0; i < VE; ++i) {
+      sc[i] = stat[2 * Cp + c0 + i];
+      sh[i] = stat[3 * Cp + c0 + i];
+      sc2[i] = y2 != nullptr ? stat2[2 * Cp + c0 + i] : 0.f;
+      sh2[i] = y2 != nullptr ? stat2[3 * Cp + c0 + i] : 0.f;
     }
-    if (y2 != nullptr) {
-      float r[VE];
-      ld16(y2 + e0, r);
+  }
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * UNR) {
+    uint4 ry[UNR], rr[UNR], r2[UNR];
 #pragma unroll
-      for (int i = 0; i < VE; ++i) a[i] += r[i] * stat2[2 * Cp + c0 + i] + stat2[3 * Cp + c0 + i];
+    for (int u = 0; u < UNR; ++u) {  // every load of the pass first
+      const int64_t v = v0 + u * stride;
+      if (v < nvec) {
+        ry[u] = ldraw(y + v * VE);
+        if (res != nullptr) rr[u] = ldraw(res + v * VE);
+        if (y2 != nullptr) r2[u] = ldraw(y2 + v * VE);
+      }
     }
-    if (relu) {
 #pragma unroll
-      for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v >= nvec) break;
+      const int64_t e0 = v * VE;
+      if (!fixc) {
+        const int c0 = (int)(e0 % Cp);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+          sc[i] = stat[2 * Cp + c0 + i];
+          sh[i] = stat[3 * Cp + c0 + i];
+          sc2[i] = y2 != nullptr ? stat2[2 * Cp + c0 + i] : 0.f;
+          sh2[i] = y2 != nullptr ? stat2[3 * Cp + c0 + i] : 0.f;
+        }
+      }
+      float a[VE];
+      cvt16<T>(ry[u], a);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] = a[i] * sc[i] + sh[i];
+      if (res != nullptr) {
+        float r[VE];
+        cvt16<T>(rr[u], r);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) a[i] += r[i];
+      }
+      if (y2 != nullptr) {
+        float r[VE];
+        cvt16<T>(r2[u], r);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) a[i] += r[i] * sc2[i] + sh2[i];
+      }
+      if (relu) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
+      }
+      st16(out + e0, a);
     }
-    st16(out + e0, a);
   }
 }
 
@@ -266,7 +322,7 @@ __global__ void bn_bwd_finalize_k(const float* __restrict__ part, int chunks, in
   }
 }
 
-template <typename T>
+template <typename T, int UNR>
 __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
@@ -274,39 +330,70 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
                                int64_t nvec, int Cp) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = v * VE;
-    const int c0 = (int)(e0 % Cp);
-    float g[VE];
-    ld16(gsrc + e0, g);
-    if (mask != nullptr) {
-      float mk[VE];
-      ld16(mask + e0, mk);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // per-channel BN-backward coefficients of the main target, in registers when the
+  // channel-vector count divides the block (see bn_apply_k):
+  //   dy = c0 * (g - c1 - (y - mean) * (invstd * c2))
+  const int CV = Cp / VE;
+  const bool fixc = (blockDim.x % CV) == 0;
+  float k0[VE], k1[VE], km[VE], kq[VE];
+  auto coeffs = [&](int c0) {
 #pragma unroll
-      for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
+    for (int i = 0; i < VE; ++i) {
+      const int c = c0 + i;
+      k0[i] = coef[c];
+      k1[i] = coef[Cp + c];
+      km[i] = stat[c];
+      kq[i] = stat[Cp + c] * coef[2 * Cp + c];
     }
-    if (gout != nullptr) st16(gout + e0, g);
-    {
-      float yy[VE], o[VE];
-      ld16(y + e0, yy);
+  };
+  if (fixc) coeffs((threadIdx.x % CV) * VE);
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * UNR) {
+    uint4 rg[UNR], rm[UNR], ry[UNR], rb[UNR];
 #pragma unroll
-      for (int i = 0; i < VE; ++i) {
-        const int c = c0 + i;
-        const float xh = (yy[i] - stat[c]) * stat[Cp + c];
-        o[i] = coef[c] * (g[i] - coef[Cp + c] - xh * coef[2 * Cp + c]);
+    for (int u = 0; u < UNR; ++u) {  // every load of the pass first
+      const int64_t v = v0 + u * stride;
+      if (v < nvec) {
+        rg[u] = ldraw(gsrc + v * VE);
+        if (mask != nullptr) rm[u] = ldraw(mask + v * VE);
+        ry[u] = ldraw(y + v * VE);
+        if (dyb != nullptr) rb[u] = ldraw(yb + v * VE);
       }
-      st16(dy + e0, o);
     }
-    if (dyb != nullptr) {
-      float yy[VE], o[VE];
-      ld16(yb + e0, yy);
 #pragma unroll
-      for (int i = 0; i < VE; ++i) {
-        const int c = c0 + i;
-        const float xh = (yy[i] - statb[c]) * statb[Cp + c];
-        o[i] = coefb[c] * (g[i] - coefb[Cp + c] - xh * coefb[2 * Cp + c]);
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v >= nvec) break;
+      const int64_t e0 = v * VE;
+      const int c0 = fixc ? (int)(threadIdx.x % CV) * VE : (int)(e0 % Cp);
+      if (!fixc) coeffs(c0);
+      float g[VE];
+      cvt16<T>(rg[u], g);
+      if (mask != nullptr) {
+        float mk[VE];
+        cvt16<T>(rm[u], mk);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
       }
-      st16(dyb + e0, o);
+      if (gout != nullptr) st16(gout + e0, g);
+      {
+        float yy[VE], o[VE];
+        cvt16<T>(ry[u], yy);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) o[i] = k0[i] * (g[i] - k1[i] - (yy[i] - km[i]) * kq[i]);
+        st16(dy + e0, o);
+      }
+      if (dyb != nullptr) {
+        float yy[VE], o[VE];
+        cvt16<T>(rb[u], yy);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+          const int c = c0 + i;
+          const float xh = (yy[i] - statb[c]) * statb[Cp + c];
+          o[i] = coefb[c] * (g[i] - coefb[Cp + c] - xh * coefb[2 * Cp + c]);
+        }
+        st16(dyb + e0, o);
+      }
     }
   }
 }
@@ -389,35 +476,54 @@ __global__ void avgpool_bwd_k(const T* __restrict__ u, T* __restrict__ dx, int B
   }
 }
 
+// 3x3 / stride-2 / pad-1 max pooling, one thread per 16-byte channel vector of an output pixel;
+// arg = winning tap (0-8, first maximum in tap order) per element, int32.
 template <typename T>
 __global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int32_t* __restrict__ arg, int B, int H,
                               int W, int P, int Q, int Cp) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
-  const int64_t n = (int64_t)B * P * Q * Cp;
+  constexpr int VE = V16<T>::N;
+  const int CV = Cp / VE;
+  const int64_t n = (int64_t)B * P * Q * CV;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % Cp);
-    int64_t t = i / Cp;
+    const int cv = (int)(i % CV);
+    int64_t t = i / CV;
     const int q = (int)(t % Q);
     t /= Q;
     const int p = (int)(t % P);
     const int b = (int)(t / P);
-    float best = -INFINITY;
-    int ba = 0;
-    for (int r = 0; r < 3; ++r) {
-      const int h = 2 * p - 1 + r;
-      for (int s = 0; s < 3; ++s) {
-        const int w = 2 * q - 1 + s;
-        if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) {
-          const float v = to_f<T>(x[(((int64_t)b * H + h) * W + w) * Cp + c]);
-          if (v > best) {
-            best = v;
-            ba = r * 3 + s;
+    uint4 raw[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {  // all nine taps in flight
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W)
+        raw[k] = ldraw(x + (((int64_t)b * H + h) * W + w) * Cp + cv * VE);
+    }
+    float best[VE];
+    int ba[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      best[e] = -INFINITY;
+      ba[e] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) {
+        float v[VE];
+        cvt16<T>(raw[k], v);
+#pragma unroll
+        for (int e = 0; e < VE; ++e)
+          if (v[e] > best[e]) {
+            best[e] = v[e];
+            ba[e] = k;
           }
-        }
       }
     }
-    out[i] = from_f<T>(best);
-    arg[i] = ba;
+    st16(out + i * VE, best);
+    int4* ap = reinterpret_cast<int4*>(arg + i * VE);
+#pragma unroll
+    for (int e = 0; e < VE; e += 4) ap[e / 4] = make_int4(ba[e], ba[e + 1], ba[e + 2], ba[e + 3]);
   }
 }
 
@@ -425,30 +531,43 @@ template <typename T>
 __global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict__ arg, T* __restrict__ dx, int B,
                               int H, int W, int P, int Q, int Cp) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
-  const int64_t n = (int64_t)B * H * W * Cp;
+  constexpr int VE = V16<T>::N;
+  const int CV = Cp / VE;
+  const int64_t n = (int64_t)B * H * W * CV;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % Cp);
-    int64_t t = i / Cp;
+    const int cv = (int)(i % CV);
+    int64_t t = i / CV;
     const int w = (int)(t % W);
     t /= W;
     const int h = (int)(t % H);
     const int b = (int)(t / H);
-    float acc = 0.f;
+    float acc[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) acc[e] = 0.f;
+#pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int pp = h + 1 - r;
-      if (pp < 0 || (pp & 1)) continue;
-      const int p = pp >> 1;
-      if (p >= P) continue;
-      for (int s = 0; s < 3; ++s) {
-        const int qq = w + 1 - s;
-        if (qq < 0 || (qq & 1)) continue;
-        const int q = qq >> 1;
-        if (q >= Q) continue;
-        const int64_t o = (((int64_t)b * P + p) * Q + q) * Cp + c;
-        if (arg[o] == r * 3 + s) acc += to_f<T>(u[o]);
+      if (pp < 0 || (pp & 1) || (pp >> 1) >= P) continue;
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) {
+        const int qq = w + 1 - s2;
+        if (qq < 0 || (qq & 1) || (qq >> 1) >= Q) continue;
+        const int64_t o = (((int64_t)b * P + (pp >> 1)) * Q + (qq >> 1)) * Cp + cv * VE;
+        float uv[VE];
+        cvt16<T>(ldraw(u + o), uv);
+        const int4* ap = reinterpret_cast<const int4*>(arg + o);
+#pragma unroll
+        for (int e = 0; e < VE; e += 4) {
+          const int4 a4 = ap[e / 4];
+          const int k = r * 3 + s2;
+          if (a4.x == k) acc[e] += uv[e];
+          if (a4.y == k) acc[e + 1] += uv[e + 1];
+          if (a4.z == k) acc[e + 2] += uv[e + 2];
+          if (a4.w == k) acc[e + 3] += uv[e + 3];
+        }
       }
     }
-    dx[i] = from_f<T>(acc);
+    st16(dx + i * VE, acc);
   }
 }
 
@@ -712,8 +831,12 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
-    launch_k(bn_apply_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
-                                                      nvec, Cp, relu);
+    if (nvec > kWave)
+      launch_k(bn_apply_k<T, 4>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2,
+               (T*)out, nvec, Cp, relu);
+    else
+      launch_k(bn_apply_k<T, 1>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2,
+               (T*)out, nvec, Cp, relu);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -772,9 +895,12 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
-    launch_k(bn_bwd_apply_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef,
-                                                           (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b,
-                                                           (T*)g_out, nvec, Cp);
+    if (nvec > kWave)
+      launch_k(bn_bwd_apply_k<T, 2>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat,
+               coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
+    else
+      launch_k(bn_bwd_apply_k<T, 1>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat,
+               coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -817,7 +943,8 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, i
                             int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    launch_k(maxpool_fwd_k<T>, grid_for((int64_t)B * P * Q * Cp), kThreads, 0, st, (const T*)x, (T*)out, arg, B, H, W, P, Q,
+    if (Cp % V16<T>::N) return cudaErrorInvalidValue;
+    launch_k(maxpool_fwd_k<T>, grid_for((int64_t)B * P * Q * Cp / V16<T>::N), kThreads, 0, st, (const T*)x, (T*)out, arg, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
   });
@@ -827,7 +954,8 @@ cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void*
                              int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    launch_k(maxpool_bwd_k<T>, grid_for((int64_t)B * H * W * Cp), kThreads, 0, st, (const T*)u, arg, (T*)dx, B, H, W, P, Q,
+    if (Cp % V16<T>::N) return cudaErrorInvalidValue;
+    launch_k(maxpool_bwd_k<T>, grid_for((int64_t)B * H * W * Cp / V16<T>::N), kThreads, 0, st, (const T*)u, arg, (T*)dx, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
   });

@@ -1592,7 +1592,9 @@ static cudaError_t igemm_dispatch(int mode, int dtype, const dsp_igemm_args_t& a
 
 cudaError_t igemm_launch(int mode, int dtype, const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   Probe& p = g_probe;
-  if (p.ev == nullptr || mode != p.mode || a.N != p.n || a.M != p.m || p.next >= p.npairs)
+  // probe key: mode (low 8 bits of p.mode), N, M and, when bits 8+ are set, Kd
+  if (p.ev == nullptr || mode != (p.mode & 0xff) || a.N != p.n || a.M != p.m || p.next >= p.npairs ||
+      ((p.mode >> 8) != 0 && a.Kd != (p.mode >> 8)))
     return igemm_dispatch(mode, dtype, a, splits, st);
   const int i = p.next++;
   // while capturing, External makes an event-record node that fires on every replay (a plain
