@@ -192,6 +192,7 @@ struct IgTma {
   // transposed weights B_t, WGRAD): one box of 128 (WGRAD: 64) consecutive output pixels x 64
   // channels per (tap, channel chunk); the tap is the instruction's im2col offset
   int i2c;
+  int a2d;      // im2col plan of a 1x1 stride-1 conv: A is a plain [pixels][C] matrix (2-D tiled boxes)
   int d_warp;   // wide-tile epilogue: per-warp 32 x 16 slabs staged in smem, TMA-stored (box {16, 32})
   int i2c_pad;  // start coordinate of output pixel (p, q) = (p * st - i2c_pad, q * st - i2c_pad)
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
@@ -468,29 +469,43 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
                 rr = fd_s.divmod(tap, ss2);
               }
               // rows past R*S*C read channels >= C: zero filled (their D rows are never stored)
-              tma_load_im2col_4d(sA + lane * tm.box_a, &tmA, &full_bar[s], mm < M ? c0 : g.C,
-                                 kq * g.stride - tm.i2c_pad, kh * g.stride - tm.i2c_pad, kn, (uint16_t)ss2,
-                                 (uint16_t)rr);
+              if (tm.a2d)
+                tma_load_2d(sA + lane * tm.box_a, &tmA, &full_bar[s], mm < M ? c0 : g.C, kb * KS);
+              else
+                tma_load_im2col_4d(sA + lane * tm.box_a, &tmA, &full_bar[s], mm < M ? c0 : g.C,
+                                   kq * g.stride - tm.i2c_pad, kh * g.stride - tm.i2c_pad, kn, (uint16_t)ss2,
+                                   (uint16_t)rr);
             } else if (lane >= 32 - nbox_b) {
               const int jb = lane - (32 - nbox_b);
               tma_load_2d(sB + jb * tm.box_b, &tmB, &full_bar[s], n0 + jb * tm.cbox_b, kb * KS);
             }
           }
         } else if (tm.i2c) {
-          // one im2col box (128 output pixels x 64 channels of one tap) + one weight box
-          if (warp == 0 && lane == 0) {
-            mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(tm.box_a + tm.box_b));
-            const int k0 = kb * KS;
-            int c0, ss2;
-            const int tap = fd_ch.divmod(k0, c0);
-            const int rr = fd_s.divmod(tap, ss2);
-            const int st2 = MODE == DSP_IGEMM_FPROP ? g.stride : 1;
-            // DGRAD = conv of dY with the flipped kernel: weight tap (r, s) meets offset (R-1-r, S-1-s)
-            const int ow = MODE == DSP_IGEMM_FPROP ? ss2 : g.S - 1 - ss2;
-            const int oh = MODE == DSP_IGEMM_FPROP ? rr : g.R - 1 - rr;
-            tma_load_im2col_4d(sA, &tmA, &full_bar[s], c0, t_q0 * st2 - tm.i2c_pad, t_h0 * st2 - tm.i2c_pad, t_n0,
-                               (uint16_t)ow, (uint16_t)oh);
-            tma_load_2d(sB, &tmB, &full_bar[s], k0, n0);
+          // one im2col box per (tap, cbox-channel chunk) of the stage (128 output pixels each),
+          // one lane per box, plus the weight box; K beyond Kd reads channel cdim (zero fill)
+          if (warp == 0) {
+            const int nbox = KS / tm.cbox;
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(nbox * tm.box_a + tm.box_b));
+            __syncwarp();
+            if (lane < nbox) {
+              const int k0 = kb * KS + lane * tm.cbox;
+              const int cdim = MODE == DSP_IGEMM_FPROP ? g.C : g.K;
+              int c0 = cdim, ss2 = 0, rr = 0;
+              if (k0 < Kd) {
+                const int tap = fd_ch.divmod(k0, c0);
+                rr = fd_s.divmod(tap, ss2);
+              }
+              const int st2 = MODE == DSP_IGEMM_FPROP ? g.stride : 1;
+              // DGRAD = conv of dY with the flipped kernel: weight tap (r, s) meets offset (R-1-r, S-1-s)
+              const int ow = MODE == DSP_IGEMM_FPROP ? ss2 : g.S - 1 - ss2;
+              const int oh = MODE == DSP_IGEMM_FPROP ? rr : g.R - 1 - rr;
+              if (tm.a2d)
+                tma_load_2d(sA + lane * tm.box_a, &tmA, &full_bar[s], c0, m0);
+              else
+                tma_load_im2col_4d(sA + lane * tm.box_a, &tmA, &full_bar[s], c0, t_q0 * st2 - tm.i2c_pad,
+                                   t_h0 * st2 - tm.i2c_pad, t_n0, (uint16_t)ow, (uint16_t)oh);
+            }
+            if (lane == 31) tma_load_2d(sB, &tmB, &full_bar[s], kb * KS, n0);
           }
         } else if (tm.on_a && MODE == DSP_IGEMM_WGRAD) {
           // WGRAD: k-block = 64 output pixels; A box j = tap-shifted X pixels x cbox
@@ -1213,7 +1228,13 @@ static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   if (MODE == DSP_IGEMM_DGRAD && (g.stride != 1 || a.B_t == nullptr)) return false;
   if (st != 1 && st != 2) return false;
   const int cdim = MODE == DSP_IGEMM_DGRAD ? g.K : g.C;  // channels of the im2col'd tensor
-  if (cdim % 64) return false;
+  const int cbox = std::min(cdim, 64);  // channels per A box (one tap each)
+  if ((cbox != 8 && cbox != 16 && cbox != 32 && cbox != 64) || cdim % cbox) return false;
+  const CUtensorMapSwizzle swz = cbox == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                 : cbox == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : cbox == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
+  const int uswz = cbox == 8 ? 0 : cbox == 16 ? 6 : cbox == 32 ? 4 : 2;
   const int pad = MODE == DSP_IGEMM_DGRAD ? g.R - 1 - g.pad : g.pad;
   if (pad < 0 || pad > 64 || g.R > 64) return false;
   const int ih = MODE == DSP_IGEMM_DGRAD ? g.P : g.H, iw = MODE == DSP_IGEMM_DGRAD ? g.Q : g.W;
@@ -1225,14 +1246,29 @@ static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   const void* bsrc = MODE == DSP_IGEMM_DGRAD ? a.B_t : a.B;
   if ((reinterpret_cast<uintptr_t>(asrc) & 15) || (reinterpret_cast<uintptr_t>(bsrc) & 15)) return false;
   const int ppc = MODE == DSP_IGEMM_WGRAD ? 64 : IG_BM;
-  cuuint64_t dims[4] = {(cuuint64_t)cdim, (cuuint64_t)iw, (cuuint64_t)ih, (cuuint64_t)g.nimg};
-  cuuint64_t strides[3] = {(cuuint64_t)cdim * 2, (cuuint64_t)iw * cdim * 2, (cuuint64_t)ih * iw * cdim * 2};
-  int lower[2] = {lo, lo}, upper[2] = {hi, hi};
-  cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
-  if (enc2(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(asrc), dims, strides, lower, upper, 64,
-           (cuuint32_t)ppc, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
+  // 1x1 stride-1: output pixel m reads input pixel m, so A is a plain [pixels][channels] matrix
+  static const bool no_a2d = getenv("DSP_B200_NO_A2D") != nullptr;
+  const bool a2d = !no_a2d && g.R == 1 && st == 1 && pad == 0;
+  if (a2d) {
+    cuuint64_t dims[2] = {(cuuint64_t)cdim, (cuuint64_t)g.nimg * ih * iw};
+    cuuint64_t strides[1] = {(cuuint64_t)cdim * 2};
+    cuuint32_t box[2] = {(cuuint32_t)cbox, (cuuint32_t)ppc};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(asrc), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  } else {
+    cuuint64_t dims[4] = {(cuuint64_t)cdim, (cuuint64_t)iw, (cuuint64_t)ih, (cuuint64_t)g.nimg};
+    cuuint64_t strides[3] = {(cuuint64_t)cdim * 2, (cuuint64_t)iw * cdim * 2, (cuuint64_t)ih * iw * cdim * 2};
+    int lower[2] = {lo, lo}, upper[2] = {hi, hi};
+    cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+    if (enc2(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(asrc), dims, strides, lower, upper, cbox,
+             (cuuint32_t)ppc, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  tm.a2d = a2d ? 1 : 0;
   if (MODE == DSP_IGEMM_WGRAD) {
     const int cb = std::min(std::min(g.K, 64), BN);
     if ((cb != 16 && cb != 32 && cb != 64) || g.K % cb || BN % cb) return false;
@@ -1251,15 +1287,15 @@ static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
     tm.on_a = tm.on_b = 1;
     tm.i2c = 1;
     tm.i2c_pad = pad;
-    tm.cbox = 64;
-    tm.box_a = 64 * 64 * 2;
-    tm.swz_a = 2;
+    tm.cbox = cbox;
+    tm.box_a = 64 * cbox * 2;
+    tm.swz_a = uswz;
     tm.cbox_b = cb;
     tm.box_b = 64 * cb * 2;
     tm.swz_b = cb == 16 ? 6 : cb == 32 ? 4 : 2;
     return true;
   }
-  if (a.Kd % 64) return false;
+  if (a.Kd % 8) return false;
   cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)a.N};  // FPROP W [Cout][Kd]; DGRAD B_t [C][Kd]
   cuuint64_t bs[1] = {(cuuint64_t)a.Kd * 2};
   cuuint32_t bb[2] = {64, (cuuint32_t)BN};
@@ -1271,9 +1307,9 @@ static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   tm.on_a = tm.on_b = 1;
   tm.i2c = 1;
   tm.i2c_pad = pad;
-  tm.cbox = 64;
-  tm.box_a = IG_BM * 128;
-  tm.swz_a = 2;
+  tm.cbox = cbox;
+  tm.box_a = IG_BM * cbox * 2;
+  tm.swz_a = uswz;
   tm.box_b = BN * 128;
   return true;
 }

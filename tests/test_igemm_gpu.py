@@ -44,6 +44,10 @@ CASES = [
     (2, 28, 28, 64, 128, 3, 2, 1),      # stride 2
     (2, 12, 12, 128, 64, 1, 2, 0),      # 1x1 stride-2 projection
     (1, 20, 20, 64, 320, 1, 1, 0),      # two n-tiles of 256
+    (2, 14, 14, 128, 256, 1, 1, 0),     # 1x1 stride 1: A as a plain 2-D [pixels][C] TMA map
+    (3, 7, 7, 64, 64, 1, 1, 0),         # ... ragged M
+    (2, 20, 20, 8, 64, 7, 2, 3),        # ResNet-50 stem shape: 8-channel im2col boxes, Kd = 392
+    (2, 14, 14, 16, 32, 3, 1, 1),       # 16 / 32-channel im2col boxes (SW32 / SW64)
 ]
 
 
