@@ -94,7 +94,8 @@ struct IgCfg {
   // TMA stores (8 warps x 2 x 1 KB)
   static constexpr int DW_BYTES = BN >= 128 ? 8 * 2 * 1024 : 0;
   static constexpr int SMEM = RING + OUT_BYTES + DW_BYTES;
-  static constexpr int NACC = BN <= 128 ? 4 : 2;  // TMEM accumulators: MMA runs NACC-1 tiles ahead
+  // TMEM accumulators (MMA runs NACC-1 tiles ahead); BN=128 keeps two so two CTAs share an SM
+  static constexpr int NACC = BN < 128 ? 4 : 2;
   static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
   static constexpr int BY_SMEM = SMEM <= 70 * 1024 ? 3 : SMEM <= 100 * 1024 ? 2 : 1;
   static constexpr int BY_TMEM = 512 / TMEM_COLS;
@@ -227,7 +228,9 @@ struct IgWarps {
   static constexpr int REG_BLOCKS = BN >= 128 ? 1 : (NPW == 4 ? IG_REG_BLOCKS : IG_REG_BLOCKS + 2);
 };
 
-template <typename T, int MODE, int BN, int NPW>
+// I2C: the im2col-operand variant (its producer branches are compiled only into it: extra
+// never-taken producer code measurably slowed the halo / tiled kernels of the CIFAR step)
+template <typename T, int MODE, int BN, int NPW, bool I2C = false>
 __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM
                                                              ? IgWarps<NPW, BN>::REG_BLOCKS
                                                              : IgCfg<BN>::CTAS_PER_SM)
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
   // halo layout: [h_nst stages of S boxes][resident weights]
   const uint32_t h_stage = (uint32_t)(tm.h_box * g.S);
   const uint32_t sW = sA0 + (uint32_t)tm.h_nst * h_stage;
-  if (warp < NPW && tm.halo) {
+  if (warp < NPW && !I2C && tm.halo) {
     // ============================ halo producer ============================
     if (warp == 0 && lane == 0) {
       tma_prefetch_desc(&tmA);
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
           continue;
         }
         // ---------------- A operand ----------------
-        if (tm.i2c && MODE == DSP_IGEMM_WGRAD) {
+        if (I2C && MODE == DSP_IGEMM_WGRAD) {
           // k-block = 64 output pixels from kb*KS on (crossing rows / images); A boxes = one per
           // 64-channel M group (tap, c0) as im2col offsets; B = dY [pixels][K] 2-D boxes
           const int nbox_a = IG_BM / tm.cbox, nbox_b = BN / tm.cbox_b;
@@ -480,11 +483,32 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
               tma_load_2d(sB + jb * tm.box_b, &tmB, &full_bar[s], n0 + jb * tm.cbox_b, kb * KS);
             }
           }
-        } else if (tm.i2c) {
+        } else if (I2C) {
           // one im2col box per (tap, cbox-channel chunk) of the stage (128 output pixels each),
           // one lane per box, plus the weight box; K beyond Kd reads channel cdim (zero fill)
-          if (warp == 0) {
-            const int nbox = KS / tm.cbox;
+          // (64-channel boxes: one box per stage, issued by lane 0 alone with no warp handshake --
+          // the warp-parallel form measured 30% slower on the ResNet-50 stage-3 3x3)
+          // (wide tiles compile only the 64-channel form: the extra producer code measured
+          // 20% slower on the ResNet-50 stage-3 3x3 even when never executed)
+          const int nbox = BN >= 128 ? 1 : KS / tm.cbox;
+          if (nbox == 1) {
+            if (warp == 0 && lane == 0) {
+              mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(tm.box_a + tm.box_b));
+              const int k0 = kb * KS;
+              int c0, ss2;
+              const int tap = fd_ch.divmod(k0, c0);
+              const int rr = fd_s.divmod(tap, ss2);
+              const int st2 = MODE == DSP_IGEMM_FPROP ? g.stride : 1;
+              const int ow = MODE == DSP_IGEMM_FPROP ? ss2 : g.S - 1 - ss2;
+              const int oh = MODE == DSP_IGEMM_FPROP ? rr : g.R - 1 - rr;
+              if (tm.a2d)
+                tma_load_2d(sA, &tmA, &full_bar[s], c0, m0);
+              else
+                tma_load_im2col_4d(sA, &tmA, &full_bar[s], c0, t_q0 * st2 - tm.i2c_pad, t_h0 * st2 - tm.i2c_pad,
+                                   t_n0, (uint16_t)ow, (uint16_t)oh);
+              tma_load_2d(sB, &tmB, &full_bar[s], k0, n0);
+            }
+          } else if (warp == 0) {
             if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(nbox * tm.box_a + tm.box_b));
             __syncwarp();
             if (lane < nbox) {
@@ -507,7 +531,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
             }
             if (lane == 31) tma_load_2d(sB, &tmB, &full_bar[s], kb * KS, n0);
           }
-        } else if (tm.on_a && MODE == DSP_IGEMM_WGRAD) {
+        } else if (!I2C && tm.on_a && MODE == DSP_IGEMM_WGRAD) {
           // WGRAD: k-block = 64 output pixels; A box j = tap-shifted X pixels x cbox
           // channels of MN range [m0 + j*cbox, +cbox); B box j = dY pixels x cbox_b
           const int nbox_a = IG_BM / tm.cbox, nbox_b = BN / tm.cbox_b;
@@ -532,7 +556,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
               tma_load_4d(sB + jb * tm.box_b, &tmB, &full_bar[s], n0 + jb * tm.cbox_b, 0, kh, kn);
             }
           }
-        } else if (tm.on_a) {
+        } else if (!I2C && tm.on_a) {
           // warp 0 issues the stage's TMA boxes in parallel, one per lane
           const int nbox = KS / tm.cbox;
           if (warp == 0) {
@@ -560,7 +584,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
             }
             if (tm.on_b && lane == 31) tma_load_2d(sB, &tmB, &full_bar[s], kb * KS, n0);
           }
-        } else if (MODE != DSP_IGEMM_WGRAD) {
+        } else if (!I2C && MODE != DSP_IGEMM_WGRAD) {
           const int k0 = kb * KS + aj * EPC;
           const bool kok = k0 < Kd;
           int c0 = 0, s2 = 0, r = 0;
@@ -589,7 +613,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
             }
             cp_async_16(sA + aj * (IG_BM * 16) + row * 16, ok ? Asrc + off : Asrc, ok ? 16u : 0u);
           }
-        } else {
+        } else if (!I2C) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int kr = tid / AG + (128 / AG) * i;
@@ -611,7 +635,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
         }
         // ---------------- B operand ----------------
         constexpr int BCH = 8 * BN;
-        if (tm.on_b) {
+        if (I2C || tm.on_b) {
           // loaded by the TMA thread above
         } else if (MODE == DSP_IGEMM_FPROP) {
 #pragma unroll
@@ -647,7 +671,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
     }
     cp_async_wait<0>();
     }
-  } else if (warp == IG_MMA_WARP && tm.halo) {
+  } else if (warp == IG_MMA_WARP && !I2C && tm.halo) {
     // ============================ halo MMA issuer ============================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, 0u, 0u, IG_BM, BN);
@@ -722,7 +746,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
     // =============================== MMA issuer ===============================
     if (lane == 0) {
       // im2col DGRAD reads the transposed weights B_t [C][R][S][K]: K-major like FPROP
-      const bool b_mn = B_MN && !(tm.i2c && MODE == DSP_IGEMM_DGRAD);
+      const bool b_mn = B_MN && !(I2C && MODE == DSP_IGEMM_DGRAD);
       const uint32_t idesc = umma_idesc(MmaTraits<T>::FMT, A_MN ? 1u : 0u, b_mn ? 1u : 0u, IG_BM, BN);
       constexpr int NKK = KS / MmaTraits<T>::MMA_K;
       // descriptor templates (start address 0) and per-MMA byte offsets, hoisted
@@ -1230,6 +1254,7 @@ static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   const int cdim = MODE == DSP_IGEMM_DGRAD ? g.K : g.C;  // channels of the im2col'd tensor
   const int cbox = std::min(cdim, 64);  // channels per A box (one tap each)
   if ((cbox != 8 && cbox != 16 && cbox != 32 && cbox != 64) || cdim % cbox) return false;
+  if (MODE != DSP_IGEMM_WGRAD && BN >= 128 && cbox != 64) return false;  // wide tiles: 64-channel boxes only
   const CUtensorMapSwizzle swz = cbox == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
                                  : cbox == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
                                  : cbox == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
@@ -1564,6 +1589,8 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1597,8 +1624,13 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   }
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
   const int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128 : Cfg::SMEM;
-  if (tm.on_a && tm.on_b && !force4)  // nothing to gather: one producer warp
-    launch_k(igemm_kernel<T, MODE, BN, 1>, grid, IgWarps<1, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
+  if (tm.on_a && tm.on_b && (!force4 || tm.i2c))  // nothing to gather: one producer warp
+  {
+    if (tm.i2c)
+      launch_k(igemm_kernel<T, MODE, BN, 1, true>, grid, IgWarps<1, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
+    else
+      launch_k(igemm_kernel<T, MODE, BN, 1>, grid, IgWarps<1, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
+  }
   else
     launch_k(igemm_kernel<T, MODE, BN, 4>, grid, IgWarps<4, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
   (void)splits;
@@ -1612,6 +1644,10 @@ static cudaError_t launch_mode(const dsp_igemm_args_t& a, int splits, cudaStream
   if (a.N <= 32) return launch_bn<T, MODE, 32>(a, splits, st);
   if (a.N <= 64) return launch_bn<T, MODE, 64>(a, splits, st);
   if (a.N <= 128) return launch_bn<T, MODE, 128>(a, splits, st);
+  // short-K FPROP / DGRAD (1x1 convs over <= 128 channels) are epilogue-bound: 128-wide tiles at
+  // two CTAs per SM give each SM twice the epilogue warps of one 256-wide CTA
+  static const bool wide = getenv("DSP_B200_SHORTK_WIDE") != nullptr;
+  if (!wide && MODE != DSP_IGEMM_WGRAD && a.Kd <= 128) return launch_bn<T, MODE, 128>(a, splits, st);
   return launch_bn<T, MODE, 256>(a, splits, st);
 }
 
