@@ -92,11 +92,12 @@ typedef struct {
                               (sum, sum of squares of the stored values) */
   int32_t kb_per_split;    /* WGRAD split-K: K blocks per split */
   int32_t n_valid;         /* FPROP/DGRAD: columns >= n_valid are stored as 0 (0 = all N valid) */
-  /* FPROP fused BatchNorm finalize (optional, needs stats): the last CTA to
-   * finish reduces the per-CTA partials in fixed order and writes
-   * stat_out[4][N] = mean, invstd, gamma*invstd, beta - mean*gamma*invstd
-   * (columns >= n_valid get zeros).  sem: a device int that is 0 on entry
-   * (the kernel leaves it 0 again). */
+  /* FPROP fused BatchNorm finalize (optional, needs stats): per n-tile of the
+   * launch, the last CTA owning it reduces that tile's per-CTA partials in fixed
+   * order and writes stat_out[4][N] = mean, invstd, gamma*invstd,
+   * beta - mean*gamma*invstd for its columns (columns >= n_valid get zeros).
+   * sem: device ints, one per n-tile (ceil(N / 128) suffice, 64 max), 0 on entry
+   * (the kernel leaves them 0 again). */
   float* stat_out;
   const float* gamma;
   const float* beta;

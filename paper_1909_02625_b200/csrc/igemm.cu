@@ -1101,7 +1101,12 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
   }
   const bool fuse_fin = want_stats && a.sem != nullptr && (bnb || a.stat_out != nullptr);
   if (fuse_fin) {
-    if (last_cta_ticket(a.sem, (int)gridDim.x, &last_cta_s, (a.out_f32 >> 8) & 3)) {
+    // one ticket per n-tile (sem[t], t = blockIdx.x % nt): the last of the G/nt CTAs owning
+    // n-tile t finalizes its BN columns, so wide outputs finalize on nt CTAs in parallel
+    const int t_own = (int)(blockIdx.x % nt);
+    int* const sem_t = a.sem + t_own;
+    if (last_cta_ticket(sem_t, (int)gridDim.x / nt, &last_cta_s, (a.out_f32 >> 8) & 3)) {
+      const int cbeg = t_own * BN, cend = min(N, cbeg + BN);
       if (kTrace && a.trace != nullptr && tid == 0) a.trace[186] = (int64_t)globaltimer_ns();
       const int nvalid = a.n_valid > 0 ? a.n_valid : N;
       const double count = (double)M;
@@ -1142,11 +1147,11 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
         double* fin4 = reinterpret_cast<double*>(smem);  // operand ring is idle by now
         constexpr int NTH = IG_THREADS >= 256 ? 256 : 128;  // threads of the load phase
         const int win = part_sums_window(NTH, NS);
-        for (int w0 = 0; w0 < N; w0 += win) {
-          const int cols = min(win, N - w0);
+        for (int w0 = cbeg; w0 < cend; w0 += win) {
+          const int cols = min(win, cend - w0);
           part_sums_load<4, NTH>(a.stats, G, N, NS, w0, cols, BN, nt, fin4);
           __syncthreads();
-          if (kTrace && a.trace != nullptr && tid == 0 && w0 == 0) a.trace[187] = (int64_t)globaltimer_ns();
+          if (kTrace && a.trace != nullptr && tid == 0 && w0 == cbeg) a.trace[187] = (int64_t)globaltimer_ns();
           for (int cc = tid; cc < cols; cc += IG_THREADS) {
             const double s1 = part_sums_get<NTH>(fin4, NS, cols, cc, 0);
             const double s2 = part_sums_get<NTH>(fin4, NS, cols, cc, 1);
@@ -1162,8 +1167,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
       } else if (MODE == DSP_IGEMM_FPROP) {
         double(*fin)[2] = reinterpret_cast<double(*)[2]>(smem);
         constexpr int NTH = IG_THREADS >= 256 ? 256 : 128;
-        for (int cb = 0; cb < N; cb += NTH) {
-          const int cols = min(NTH, N - cb);
+        for (int cb = cbeg; cb < cend; cb += NTH) {
+          const int cols = min(NTH, cend - cb);
           const int parts = NTH / cols;
           if (tid < parts * cols) {
             const int c = cb + tid % cols, p = tid / cols;
@@ -1188,7 +1193,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::R
           __syncthreads();
         }
       }
-      if (tid == 0) *a.sem = 0;
+      if (tid == 0) *sem_t = 0;
       if (kTrace && a.trace != nullptr && tid == 0) a.trace[188] = (int64_t)globaltimer_ns();
     }
   }
