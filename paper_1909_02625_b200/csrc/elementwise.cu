@@ -143,6 +143,7 @@ __global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ st
         if (y2 != nullptr) r2[u] = ldraw(y2 + v * VE);
       }
     }
+
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int64_t v = v0 + u * stride;
@@ -360,6 +361,7 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
         if (dyb != nullptr) rb[u] = ldraw(yb + v * VE);
       }
     }
+
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int64_t v = v0 + u * stride;
@@ -394,6 +396,87 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
         }
         st16(dyb + e0, o);
       }
+    }
+  }
+}
+
+// Tensors within one wave (CIFAR shapes, one vector per thread): the plain form -- per-vector
+// coefficient loads overlap the data load's latency, which the register-resident form above
+// (coefficients first) cannot (measured 1.5% slower on the ResNet-56 step).
+template <typename T>
+__global__ void bn_apply_small_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
+                           const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
+                           int64_t nvec, int Cp, int relu) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  constexpr int VE = V16<T>::N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = v * VE;
+    const int c0 = (int)(e0 % Cp);
+    float a[VE];
+    ld16(y + e0, a);
+#pragma unroll
+    for (int i = 0; i < VE; ++i) a[i] = a[i] * stat[2 * Cp + c0 + i] + stat[3 * Cp + c0 + i];
+    if (res != nullptr) {
+      float r[VE];
+      ld16(res + e0, r);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] += r[i];
+    }
+    if (y2 != nullptr) {
+      float r[VE];
+      ld16(y2 + e0, r);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] += r[i] * stat2[2 * Cp + c0 + i] + stat2[3 * Cp + c0 + i];
+    }
+    if (relu) {
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
+    }
+    st16(out + e0, a);
+  }
+}
+
+template <typename T>
+__global__ void bn_bwd_apply_small_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+                               const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
+                               const T* __restrict__ yb, const float* __restrict__ statb,
+                               const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
+                               int64_t nvec, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  constexpr int VE = V16<T>::N;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = v * VE;
+    const int c0 = (int)(e0 % Cp);
+    float g[VE];
+    ld16(gsrc + e0, g);
+    if (mask != nullptr) {
+      float mk[VE];
+      ld16(mask + e0, mk);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
+    }
+    if (gout != nullptr) st16(gout + e0, g);
+    {
+      float yy[VE], o[VE];
+      ld16(y + e0, yy);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) {
+        const int c = c0 + i;
+        const float xh = (yy[i] - stat[c]) * stat[Cp + c];
+        o[i] = coef[c] * (g[i] - coef[Cp + c] - xh * coef[2 * Cp + c]);
+      }
+      st16(dy + e0, o);
+    }
+    if (dyb != nullptr) {
+      float yy[VE], o[VE];
+      ld16(yb + e0, yy);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) {
+        const int c = c0 + i;
+        const float xh = (yy[i] - statb[c]) * statb[Cp + c];
+        o[i] = coefb[c] * (g[i] - coefb[Cp + c] - xh * coefb[2 * Cp + c]);
+      }
+      st16(dyb + e0, o);
     }
   }
 }
@@ -835,8 +918,8 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
       launch_k(bn_apply_k<T, 4>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2,
                (T*)out, nvec, Cp, relu);
     else
-      launch_k(bn_apply_k<T, 1>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2,
-               (T*)out, nvec, Cp, relu);
+      launch_k(bn_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2,
+               stat2, (T*)out, nvec, Cp, relu);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -899,8 +982,8 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
       launch_k(bn_bwd_apply_k<T, 2>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat,
                coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
     else
-      launch_k(bn_bwd_apply_k<T, 1>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat,
-               coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
+      launch_k(bn_bwd_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y,
+               stat, coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
     return note_launch(), cudaGetLastError();
   });
 }

@@ -1530,6 +1530,7 @@ static void tma_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   } else if (!halo_plan<MODE, BN>(a, tm, tmA, tmB, enc)) {
     tma_plan_tiled<MODE, BN>(a, tm, tmA, tmB, enc);
   }
+  // im2col wherever an operand would otherwise be gathered
   if (!(tm.on_a && tm.on_b)) {
     IgTma t2{};
     CUtensorMap a2, b2;
