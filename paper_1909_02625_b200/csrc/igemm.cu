@@ -81,9 +81,11 @@ constexpr bool kTrace = true;
 constexpr bool kTrace = false;
 #endif
 
-template <int BN>
+// DEEP: the im2col kernel variant (ImageNet-sized launches that own the GPU) keeps a 4-stage
+// ring at every width <= 64; the CIFAR variants stay shallow so concurrent block streams fit
+template <int BN, bool DEEP = false>
 struct IgCfg {
-  static constexpr int STAGES = BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 4);
+  static constexpr int STAGES = (DEEP && BN <= 64) ? 4 : BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 4);
   static constexpr int RING = STAGES * (IG_BM * 128 + BN * 128);
 #ifdef IG_TMA_STORE
   static constexpr int OUT_BYTES = IG_BM * BN * 2;  // bf16 output tile staged for the TMA store
@@ -231,13 +233,13 @@ struct IgWarps {
 // I2C: the im2col-operand variant (its producer branches are compiled only into it: extra
 // never-taken producer code measurably slowed the halo / tiled kernels of the CIFAR step)
 template <typename T, int MODE, int BN, int NPW, bool I2C = false>
-__global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::REG_BLOCKS > IgCfg<BN>::CTAS_PER_SM
+__global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::REG_BLOCKS > IgCfg<BN, I2C>::CTAS_PER_SM
                                                              ? IgWarps<NPW, BN>::REG_BLOCKS
-                                                             : IgCfg<BN>::CTAS_PER_SM)
+                                                             : IgCfg<BN, I2C>::CTAS_PER_SM)
     igemm_kernel(const dsp_igemm_args_t a, const __grid_constant__ CUtensorMap tmA,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmD,
                  const IgTma tm) {
-  using Cfg = IgCfg<BN>;
+  using Cfg = IgCfg<BN, I2C>;
   constexpr int IG_THREADS = IgWarps<NPW, BN>::THREADS;
   constexpr int IG_MMA_WARP = IgWarps<NPW, BN>::MMA_WARP;
   constexpr int IG_EPI_WARP0 = IgWarps<NPW, BN>::EPI_WARP0;
@@ -1589,7 +1591,7 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   static int attr_state = 0;
   static int num_sms = 148;
   if (!attr_state) {
-    const int smax = std::max(Cfg::SMEM, IG_HALO_SMEM_MAX);
+    const int smax = std::max(std::max(Cfg::SMEM, IgCfg<BN, true>::SMEM), IG_HALO_SMEM_MAX);
     cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smax);
     if (e != cudaSuccess) return e;
@@ -1608,6 +1610,7 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   const int ns = MODE == DSP_IGEMM_WGRAD ? (nkb + a.kb_per_split - 1) / a.kb_per_split : 1;
   const int units = ((a.M + IG_BM - 1) / IG_BM) * ((a.N + BN - 1) / BN) * ns;
   static const int cap = getenv("DSP_B200_GRID_CAP") ? atoi(getenv("DSP_B200_GRID_CAP")) : DSP_IGEMM_MAX_CTAS;
+  static_assert(IgCfg<BN, true>::CTAS_PER_SM == Cfg::CTAS_PER_SM, "grid sizing assumes equal residency");
   int grid = std::min(units, std::min(cap, num_sms * Cfg::CTAS_PER_SM));
   if (MODE != DSP_IGEMM_WGRAD) {  // each CTA owns one n-tile: grid must be a multiple of nt
     const int nt = (a.N + BN - 1) / BN;
@@ -1629,7 +1632,8 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
     }
   }
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
-  const int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128 : Cfg::SMEM;
+  const int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128
+                           : (tm.i2c ? IgCfg<BN, true>::SMEM : Cfg::SMEM);
   if (tm.on_a && tm.on_b && (!force4 || tm.i2c))  // nothing to gather: one producer warp
   {
     if (tm.i2c)
