@@ -85,7 +85,8 @@ constexpr bool kTrace = false;
 // ring at every width <= 64; the CIFAR variants stay shallow so concurrent block streams fit
 template <int BN, bool DEEP = false>
 struct IgCfg {
-  static constexpr int STAGES = (DEEP && BN <= 64) ? 4 : BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 4);
+  static constexpr int STAGES = (DEEP && BN <= 32) ? 4 : (DEEP && BN == 64) ? 3
+                                : BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 4);
   static constexpr int RING = STAGES * (IG_BM * 128 + BN * 128);
 #ifdef IG_TMA_STORE
   static constexpr int OUT_BYTES = IG_BM * BN * 2;  // bf16 output tile staged for the TMA store
@@ -94,7 +95,7 @@ struct IgCfg {
 #endif
   // wide tiles: per-epilogue-warp double-buffered 32-row x 16-column bf16 staging slabs for
   // TMA stores (8 warps x 2 x 1 KB)
-  static constexpr int DW_BYTES = BN >= 128 ? 8 * 2 * 1024 : 0;
+  static constexpr int DW_BYTES = (BN >= 128 || (DEEP && BN == 64)) ? 8 * 2 * 1024 : 0;
   static constexpr int SMEM = RING + OUT_BYTES + DW_BYTES;
   // TMEM accumulators (MMA runs NACC-1 tiles ahead); BN=128 keeps two so two CTAs share an SM
   static constexpr int NACC = BN < 128 ? 4 : 2;
@@ -219,31 +220,32 @@ static void fastdiv_host(uint32_t d, uint32_t& mul, uint32_t& shr) {
 // threads), 1 when every operand comes through TMA (one lane issues the boxes).
 // Registers are budgeted as if REG_BLOCKS CTAs shared an SM, leaving room for the other
 // block streams' kernels beside a conv CTA (<= 75 regs at 288 threads, <= 68 at 192).
-template <int NPW, int BN>
+template <int NPW, int BN, bool I2C = false>
 struct IgWarps {
+  static constexpr bool WIDE = BN >= 128 || (I2C && BN == 64);
   // 8 epilogue warps (two per TMEM lane quadrant, each half the columns) for the wide tiles of
   // the tensor-bound shapes, whose epilogue would otherwise bound small-Kd (1x1) convs
-  static constexpr int NEPI = BN >= 128 ? 8 : 4;
+  static constexpr int NEPI = WIDE ? 8 : 4;
   static constexpr int THREADS = (NPW + 1 + NEPI) * 32;
   static constexpr int MMA_WARP = NPW;
   static constexpr int EPI_WARP0 = NPW + 1;
-  static constexpr int REG_BLOCKS = BN >= 128 ? 1 : (NPW == 4 ? IG_REG_BLOCKS : IG_REG_BLOCKS + 2);
+  static constexpr int REG_BLOCKS = WIDE ? 1 : (NPW == 4 ? IG_REG_BLOCKS : IG_REG_BLOCKS + 2);
 };
 
 // I2C: the im2col-operand variant (its producer branches are compiled only into it: extra
 // never-taken producer code measurably slowed the halo / tiled kernels of the CIFAR step)
 template <typename T, int MODE, int BN, int NPW, bool I2C = false>
-__global__ void __launch_bounds__(IgWarps<NPW, BN>::THREADS, IgWarps<NPW, BN>::REG_BLOCKS > IgCfg<BN, I2C>::CTAS_PER_SM
-                                                             ? IgWarps<NPW, BN>::REG_BLOCKS
+__global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, BN, I2C>::REG_BLOCKS > IgCfg<BN, I2C>::CTAS_PER_SM
+                                                             ? IgWarps<NPW, BN, I2C>::REG_BLOCKS
                                                              : IgCfg<BN, I2C>::CTAS_PER_SM)
     igemm_kernel(const dsp_igemm_args_t a, const __grid_constant__ CUtensorMap tmA,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmD,
                  const IgTma tm) {
   using Cfg = IgCfg<BN, I2C>;
-  constexpr int IG_THREADS = IgWarps<NPW, BN>::THREADS;
-  constexpr int IG_MMA_WARP = IgWarps<NPW, BN>::MMA_WARP;
-  constexpr int IG_EPI_WARP0 = IgWarps<NPW, BN>::EPI_WARP0;
-  constexpr int NEPI = IgWarps<NPW, BN>::NEPI;
+  constexpr int IG_THREADS = IgWarps<NPW, BN, I2C>::THREADS;
+  constexpr int IG_MMA_WARP = IgWarps<NPW, BN, I2C>::MMA_WARP;
+  constexpr int IG_EPI_WARP0 = IgWarps<NPW, BN, I2C>::EPI_WARP0;
+  constexpr int NEPI = IgWarps<NPW, BN, I2C>::NEPI;
   constexpr int EPI_T = NEPI * 32;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NACC = Cfg::NACC;
@@ -1578,7 +1580,7 @@ static void tma_out_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD)
 template <typename T, int MODE, int BN>
 static void dwarp_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
   static const bool disabled = getenv("DSP_B200_NO_DWARP") != nullptr;
-  if (disabled || tm.halo || IgCfg<BN>::DW_BYTES == 0 || MODE == DSP_IGEMM_WGRAD || sizeof(T) != 2 || (a.out_f32 & 1))
+  if (disabled || tm.halo || (tm.i2c ? IgCfg<BN, true>::DW_BYTES : IgCfg<BN>::DW_BYTES) == 0 || MODE == DSP_IGEMM_WGRAD || sizeof(T) != 2 || (a.out_f32 & 1))
     return;
   if ((reinterpret_cast<uintptr_t>(a.D) & 15) || (a.ldd % 8) || a.N % 16 || a.ldd < a.N) return;
   (void)tmD;
@@ -1637,7 +1639,7 @@ static cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t
   if (tm.on_a && tm.on_b && (!force4 || tm.i2c))  // nothing to gather: one producer warp
   {
     if (tm.i2c)
-      launch_k(igemm_kernel<T, MODE, BN, 1, true>, grid, IgWarps<1, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
+      launch_k(igemm_kernel<T, MODE, BN, 1, true>, grid, IgWarps<1, BN, true>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
     else
       launch_k(igemm_kernel<T, MODE, BN, 1>, grid, IgWarps<1, BN>::THREADS, smem, st, a, tmA, tmB, tmD, tm);
   }
