@@ -489,7 +489,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
         off += co;
         c.wpack = pack_elems;
         pack_elems += (int64_t)c.g.K * k * k * c.g.C;
-        if (stride == 1) {  // DGRAD's K-major weights (TMA / halo tiles)
+        if (stride == 1 || stride == 2) {  // DGRAD's K-major weights (TMA / halo tiles, parity-split stride 2)
           c.wpack_t = pack_elems;
           pack_elems += (int64_t)c.g.K * k * k * c.g.C;
         }

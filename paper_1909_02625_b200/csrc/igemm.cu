@@ -45,6 +45,15 @@ namespace dsp {
 
 constexpr int IG_BM = 128;
 
+// Stride-2 DGRAD, output parity ph: the taps r of an R-tap (pad (R-1)/2) kernel that reach
+// output rows 2i+ph, i.e. (ph + pad - r) even; they read dY row i + (ph + pad - r) / 2.
+__device__ __forceinline__ int s2_taps(int R, int pad, int ph, int (&list)[2]) {
+  int n = 0;
+  for (int r = 0; r < R && n < 2; ++r)
+    if (((ph + pad - r) & 1) == 0) list[n++] = r;
+  return n;
+}
+
 template <typename T>
 struct MmaTraits;
 template <>
@@ -196,6 +205,7 @@ struct IgTma {
   // transposed weights B_t, WGRAD): one box of 128 (WGRAD: 64) consecutive output pixels x 64
   // channels per (tap, channel chunk); the tap is the instruction's im2col offset
   int i2c;
+  int s2;       // stride-2 DGRAD split by output parity (ph, pw) into stride-1 sub-convolutions of dY
   int a2d;      // im2col plan of a 1x1 stride-1 conv: A is a plain [pixels][C] matrix (2-D tiled boxes)
   int d_warp;   // wide-tile epilogue: per-warp 32 x 16 slabs staged in smem, TMA-stored (box {16, 32})
   int i2c_pad;  // start coordinate of output pixel (p, q) = (p * st - i2c_pad, q * st - i2c_pad)
@@ -270,7 +280,9 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
   const int lane = tid & 31;
   if (kTrace && a.trace != nullptr && tid == 0) a.trace[192 + 8 * blockIdx.x] = (int64_t)globaltimer_ns();
   const dsp_conv_geom_t g = a.geom;
-  const int M = a.M, N = a.N, Kd = a.Kd;
+  // s2: the launch covers 4 output parities of M/4 pixels each (a.M = all dX pixels)
+  const bool s2 = I2C && MODE == DSP_IGEMM_DGRAD && tm.s2;
+  const int M = s2 ? a.M / 4 : a.M, N = a.N, Kd = a.Kd;
   const T* __restrict__ Asrc = reinterpret_cast<const T*>(a.A);
   const T* __restrict__ Bsrc = reinterpret_cast<const T*>(a.B);
 
@@ -301,11 +313,18 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
       return true;
     }
     const int mtile = blockIdx.x / nt + j * (gridDim.x / nt);
-    if (mtile >= mt) return false;
-    m0 = mtile * IG_BM;
+    if (mtile >= (s2 ? 4 * mt : mt)) return false;
     n0 = (blockIdx.x % nt) * BN;
-    z = 0;
     kb0 = 0;
+    if (s2) {  // z = output parity (ph, pw) = (z >> 1, z & 1); k-blocks = its taps x K/64
+      z = mtile / mt;
+      m0 = (mtile - z * mt) * IG_BM;
+      int rl[2], sl[2];
+      kb1 = s2_taps(g.R, g.pad, z >> 1, rl) * s2_taps(g.S, g.pad, z & 1, sl) * (g.K / KS);
+      return true;
+    }
+    m0 = mtile * IG_BM;
+    z = 0;
     kb1 = nkb_total;
     return true;
   };
@@ -395,8 +414,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
         fd_k{tm.fd_d[4], tm.fd_mul[4], tm.fd_shr[4]};
     const int sh = g.stride == 2 ? 1 : 0;  // stride is 1 or 2
     const int img_stride = MODE == DSP_IGEMM_DGRAD ? g.P * g.Q * g.K : g.H * g.W * g.C;
-    const int out_hw = MODE == DSP_IGEMM_DGRAD ? g.H * g.W : g.P * g.Q;
-    const int out_w = MODE == DSP_IGEMM_DGRAD ? g.W : g.Q;
+    const int out_hw = (MODE == DSP_IGEMM_DGRAD && !s2) ? g.H * g.W : g.P * g.Q;
+    const int out_w = (MODE == DSP_IGEMM_DGRAD && !s2) ? g.W : g.Q;
     if (tm.on_a && tid == 0) {
       tma_prefetch_desc(&tmA);
       if (tm.on_b) tma_prefetch_desc(&tmB);
@@ -495,7 +514,21 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           // (wide tiles compile only the 64-channel form: the extra producer code measured
           // 20% slower on the ResNet-50 stage-3 3x3 even when never executed)
           const int nbox = BN >= 128 ? 1 : KS / tm.cbox;
-          if (nbox == 1) {
+          if (s2) {
+            if (warp == 0 && lane == 0) {
+              // tap t of parity z: dY rows/cols i + dr, j + ds against weight tap (r, s)
+              mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(tm.box_a + tm.box_b));
+              const int kpb = g.K / KS;
+              const int tsub = kb / kpb, kc = (kb - tsub * kpb) * KS;
+              int rl[2], sl[2];
+              s2_taps(g.R, g.pad, z >> 1, rl);
+              const int ns = s2_taps(g.S, g.pad, z & 1, sl);
+              const int r = rl[tsub / ns], sx = sl[tsub % ns];
+              const int dr = ((z >> 1) + g.pad - r) >> 1, ds = ((z & 1) + g.pad - sx) >> 1;
+              tma_load_im2col_4d(sA, &tmA, &full_bar[s], kc, t_q0, t_h0, t_n0, (uint16_t)ds, (uint16_t)dr);
+              tma_load_2d(sB, &tmB, &full_bar[s], (r * g.S + sx) * g.K + kc, n0);
+            }
+          } else if (nbox == 1) {
             if (warp == 0 && lane == 0) {
               mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(tm.box_a + tm.box_b));
               const int k0 = kb * KS;
@@ -855,6 +888,15 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
       }
       const int m = m0 + row;
       const bool mok = m < M;
+      // dX row of tile row mm (s2: parity z's pixel (n, i, j) -> (n, 2i + ph, 2j + pw))
+      auto rowmap = [&](int mm) -> int {
+        if (!s2) return mm;
+        const int PQ = g.P * g.Q;
+        const int n = mm / PQ, rem = mm - n * PQ, ii = rem / g.Q, jj = rem - ii * g.Q;
+        return (n * g.H + 2 * ii + (z >> 1)) * g.W + 2 * jj + (z & 1);
+      };
+      const int mr = rowmap(m);
+      const bool zacc = s2 && kb1 == 0;  // a parity no tap reaches (1x1 stride 2): D = residual
       const uint32_t tl = tmem_d + acc * BN + ((uint32_t)(q * 32) << 16);
       // each warp: CPW 16-column chunks of its half; wide tiles load 32 TMEM columns per wait
       constexpr int CPW = BN / 16 / (NEPI / 4);
@@ -862,7 +904,10 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll 1
       for (int c2 = 0; c2 < CPW; c2 += LDW) {
         float vb[16 * LDW];
-        if constexpr (LDW == 2) {
+        if (zacc) {
+#pragma unroll
+          for (int e = 0; e < 16 * LDW; ++e) vb[e] = 0.f;
+        } else if constexpr (LDW == 2) {
           tmem_ld32(tl + (half * CPW + c2) * 16, vb);
         } else {
           tmem_ld16(tl + (half * CPW + c2) * 16, vb);
@@ -896,7 +941,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
               if (nb + e < nvalid) v[e] += a.bias[nb + e];
           }
           if (a.residual != nullptr && mok) {
-            const T* res = reinterpret_cast<const T*>(a.residual) + (size_t)m * a.ldd;
+            const T* res = reinterpret_cast<const T*>(a.residual) + (size_t)mr * a.ldd;
             if (nb + 16 <= N && (a.ldd % EPC) == 0) {
 #pragma unroll
               for (int qq = 0; qq < 16 / EPC; ++qq) {
@@ -915,7 +960,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           for (int e = 0; e < 16; ++e)
             if (nb + e >= nvalid) v[e] = 0.f;
           if (a.out_f32 & 1) {
-            float* out = reinterpret_cast<float*>(a.D) + (size_t)m * a.ldd;
+            float* out = reinterpret_cast<float*>(a.D) + (size_t)mr * a.ldd;
             if (mok) {
 #pragma unroll
               for (int e = 0; e < 16; ++e)
@@ -949,7 +994,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                              : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
                              : "r"(buf + r * 32 + (lane & 1) * 16));
                 if (r < rvalid && nb < N)  // N % 16 == 0: a slab is wholly inside or outside
-                  *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(m0 + q * 32 + r) * a.ldd + nb +
+                  *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)rowmap(m0 + q * 32 + r) * a.ldd + nb +
                                             (lane & 1) * 8) = raw;
               }
             }
@@ -995,7 +1040,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                            : "memory");
             }
           } else {
-            T* out = reinterpret_cast<T*>(a.D) + (size_t)m * a.ldd;
+            T* out = reinterpret_cast<T*>(a.D) + (size_t)mr * a.ldd;
             // round to the storage type first so BN statistics describe the stored tensor
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = to_f<T>(from_f<T>(v[e]));
@@ -1037,19 +1082,19 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
             float g[16], pr[16];
             {
               float mk[16];
-              ld_row16<T>(a.bnb_mask, mok, m, a.ldd, nb, N, mk);
+              ld_row16<T>(a.bnb_mask, mok, mr, a.ldd, nb, N, mk);
 #pragma unroll
               for (int e = 0; e < 16; ++e) g[e] = mk[e] > 0.f ? v[e] : 0.f;
             }
             const float s1 = colsum16(g, lane);
             float yv[16];
-            ld_row16<T>(a.bnb[0].y, mok, m, a.ldd, nb, N, yv);
+            ld_row16<T>(a.bnb[0].y, mok, mr, a.ldd, nb, N, yv);
 #pragma unroll
             for (int e = 0; e < 16; ++e) pr[e] = g[e] * ((yv[e] - bst[0][0][cl + e]) * bst[0][1][cl + e]);
             const float s2 = colsum16(pr, lane);
             float s3 = 0.f;
             if (a.bnb_count > 1) {
-              ld_row16<T>(a.bnb[1].y, mok, m, a.ldd, nb, N, yv);
+              ld_row16<T>(a.bnb[1].y, mok, mr, a.ldd, nb, N, yv);
 #pragma unroll
               for (int e = 0; e < 16; ++e) pr[e] = g[e] * ((yv[e] - bst[1][0][cl + e]) * bst[1][1][cl + e]);
               s3 = colsum16(pr, lane);
@@ -1113,7 +1158,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
       const int cbeg = t_own * BN, cend = min(N, cbeg + BN);
       if (kTrace && a.trace != nullptr && tid == 0) a.trace[186] = (int64_t)globaltimer_ns();
       const int nvalid = a.n_valid > 0 ? a.n_valid : N;
-      const double count = (double)M;
+      const double count = (double)a.M;
       const int G = (int)gridDim.x;
       auto finish = [&](int c, double s1, double s2) {
         float mean = 0.f, inv = 0.f, scale = 0.f, shift = 0.f;
@@ -1258,6 +1303,40 @@ static bool i2c_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmA, CUt
   const dsp_conv_geom_t& g = a.geom;
   if (disabled || enc2 == nullptr || g.R != g.S) return false;
   const int st = MODE == DSP_IGEMM_DGRAD ? 1 : g.stride;
+  if (MODE == DSP_IGEMM_DGRAD && g.stride == 2) {
+    // parity split: 4 stride-1 sub-convolutions of dY (dr, ds in {0, 1}) against the taps of
+    // B_t that reach each output parity; one launch, units = 4 parities x m-tiles
+    static const bool no_s2 = getenv("DSP_B200_NO_S2DGRAD") != nullptr;
+    if (no_s2 || a.B_t == nullptr || g.R != g.S || (g.R != 1 && g.R != 3) || g.pad != (g.R - 1) / 2 ||
+        g.H != 2 * g.P || g.W != 2 * g.Q || g.K % 64 || a.Kd % 64 || a.M % 4)
+      return false;
+    if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B_t) & 15)) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.Q, (cuuint64_t)g.P, (cuuint64_t)g.nimg};
+    cuuint64_t strides[3] = {(cuuint64_t)g.K * 2, (cuuint64_t)g.Q * g.K * 2, (cuuint64_t)g.P * g.Q * g.K * 2};
+    int lower[2] = {0, 0}, upper[2] = {0, 0};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc2(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.A), dims, strides, lower, upper, 64,
+             (cuuint32_t)IG_BM, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    cuuint64_t bd[2] = {(cuuint64_t)a.Kd, (cuuint64_t)a.N};
+    cuuint64_t bs[1] = {(cuuint64_t)a.Kd * 2};
+    cuuint32_t bb[2] = {64, (cuuint32_t)BN};
+    cuuint32_t be[2] = {1, 1};
+    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.B_t), bd, bs, bb, be,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    tm.on_a = tm.on_b = 1;
+    tm.i2c = 1;
+    tm.s2 = 1;
+    tm.i2c_pad = 0;
+    tm.cbox = 64;
+    tm.box_a = IG_BM * 128;
+    tm.swz_a = 2;
+    tm.box_b = BN * 128;
+    return true;
+  }
   if (MODE == DSP_IGEMM_DGRAD && (g.stride != 1 || a.B_t == nullptr)) return false;
   if (st != 1 && st != 2) return false;
   const int cdim = MODE == DSP_IGEMM_DGRAD ? g.K : g.C;  // channels of the im2col'd tensor

@@ -48,6 +48,8 @@ CASES = [
     (3, 7, 7, 64, 64, 1, 1, 0),         # ... ragged M
     (2, 20, 20, 8, 64, 7, 2, 3),        # ResNet-50 stem shape: 8-channel im2col boxes, Kd = 392
     (2, 14, 14, 16, 32, 3, 1, 1),       # 16 / 32-channel im2col boxes (SW32 / SW64)
+    (2, 14, 14, 256, 128, 3, 2, 1),     # stride-2 DGRAD split by output parity (BN=256)
+    (1, 14, 14, 512, 256, 1, 2, 0),     # 1x1 stride-2 projection: 3 parities without taps
 ]
 
 
