@@ -222,27 +222,44 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
     }
     const int64_t r0 = (int64_t)blockIdx.x * rows_per_chunk;
     const int64_t r1 = min(M, r0 + rows_per_chunk);
-    for (int64_t r = r0 + tr; r < r1; r += TR) {
-      const int64_t e0 = r * Cp + c0;
-      float g[VE];
-      ld16(gsrc + e0, g);
-      if (mask != nullptr) {
-        float mk[VE];
-        ld16(mask + e0, mk);
+    // RU rows per pass, every load of the pass issued before any use; rows are still
+    // accumulated in ascending order, so the sums are bitwise those of a one-row loop
+    constexpr int RU = 4;
+    for (int64_t rb = r0 + tr; rb < r1; rb += (int64_t)TR * RU) {
+      uint4 rg[RU], rm[RU], ry[RU];
 #pragma unroll
-        for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
-      }
-      if (y != nullptr) {
-        float yy[VE];
-        ld16(y + e0, yy);
-#pragma unroll
-        for (int i = 0; i < VE; ++i) {
-          s1[i] += g[i];
-          s2[i] += g[i] * ((yy[i] - mean[i]) * inv[i]);
+      for (int u = 0; u < RU; ++u) {
+        const int64_t r = rb + (int64_t)u * TR;
+        if (r < r1) {
+          const int64_t e0 = r * Cp + c0;
+          rg[u] = ldraw(gsrc + e0);
+          if (mask != nullptr) rm[u] = ldraw(mask + e0);
+          if (y != nullptr) ry[u] = ldraw(y + e0);
         }
-      } else {
+      }
 #pragma unroll
-        for (int i = 0; i < VE; ++i) s1[i] += g[i];
+      for (int u = 0; u < RU; ++u) {
+        if (rb + (int64_t)u * TR >= r1) break;
+        float g[VE];
+        cvt16<T>(rg[u], g);
+        if (mask != nullptr) {
+          float mk[VE];
+          cvt16<T>(rm[u], mk);
+#pragma unroll
+          for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
+        }
+        if (y != nullptr) {
+          float yy[VE];
+          cvt16<T>(ry[u], yy);
+#pragma unroll
+          for (int i = 0; i < VE; ++i) {
+            s1[i] += g[i];
+            s2[i] += g[i] * ((yy[i] - mean[i]) * inv[i]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < VE; ++i) s1[i] += g[i];
+        }
       }
     }
   }

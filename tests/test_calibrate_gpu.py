@@ -32,7 +32,7 @@ def test_device_straggler_changes_timing_not_values():
     cfg = P.default_queue_config(3)
     pool = R.synthetic_batches(4, 8, (3, 8, 8), 10, seed=1)
     out = []
-    for strag in (None, P.DeviceStraggler(prob=0.5, delay_s=2e-4, seed=3)):
+    for strag in (None, P.DeviceStraggler(prob=0.5, delay_s=1e-3, seed=3)):
         pm, _ = twin_models(layers, [2, 4], seed=2)
         eng = P.TrainEngine(pm, cfg, R.cycle(pool), P.LrSchedule(0.05), rule="sum", beta=0.9, straggler=strag)
         eng.rt.use_graphs = False  # both runs eager: compare like with like
@@ -47,6 +47,6 @@ def test_device_straggler_changes_timing_not_values():
     assert out[0][0] == out[1][0]
     for a, b in zip(out[0][2], out[1][2]):
         assert np.array_equal(a, b)
-    hits = sum(P.DeviceStraggler(prob=0.5, delay_s=2e-4, seed=3).hits(k, n, ph)
+    hits = sum(P.DeviceStraggler(prob=0.5, delay_s=1e-3, seed=3).hits(k, n, ph)
                for k in range(3) for n in range(4, 16) for ph in (0, 1))
     assert hits > 0 and out[1][1] > out[0][1]  # the injected device delays show up in GPU time
