@@ -78,6 +78,16 @@ struct dsp_block {
   float* grads = nullptr;
   bool tape_valid = false;
   const void* rec_x = nullptr;
+  // side stream for the weight gradients of residual units: WGRAD (+ split-K reduce) of a conv
+  // runs beside the DGRAD that reads the same dY, forked / joined with events (graph-capturable)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool side_busy = false;
+  ~dsp_block() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
 };
 
 namespace dsp {
@@ -167,6 +177,26 @@ int conv_wgrad(dsp_block* b, const ConvP& c, const void* x, const void* dy, cuda
   DSP_CUDA(igemm_launch(DSP_IGEMM_WGRAD, b->dtype, a, splits, st));
   DSP_CUDA(wgrad_reduce(at<float>(b, b->wpart), splits, a.M, a.N, c.g.R * c.g.S, c.g.C, c.ci_real, c.co_real, 0,
                         b->grads + c.w_off, st));
+  return DSP_OK;
+}
+
+// WGRAD of conv c on the block's side stream, ordered after everything already on st.
+int conv_wgrad_side(dsp_block* b, const ConvP& c, const void* x, const void* dy, cudaStream_t st) {
+  static const bool off = getenv("DSP_B200_NO_WGRAD_SIDE") != nullptr;
+  if (off || b->side == nullptr) return conv_wgrad(b, c, x, dy, st);
+  DSP_CUDA(cudaEventRecord(b->ev_fork, st));
+  DSP_CUDA(cudaStreamWaitEvent(b->side, b->ev_fork, 0));
+  DSP_TRY(conv_wgrad(b, c, x, dy, b->side));
+  DSP_CUDA(cudaEventRecord(b->ev_join, b->side));
+  b->side_busy = true;
+  return DSP_OK;
+}
+// st waits for every side-stream WGRAD issued so far (before their dY / x buffers are reused).
+int side_join(dsp_block* b, cudaStream_t st) {
+  if (b->side_busy) {
+    DSP_CUDA(cudaStreamWaitEvent(st, b->ev_join, 0));
+    b->side_busy = false;
+  }
   return DSP_OK;
 }
 
@@ -376,22 +406,24 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
       for (int i = nmain - 1; i >= 0; --i) {
         const ConvP& c = l.convs[i];
         const void* cin = i == 0 ? x : b->ws + (i == 1 ? l.z1 : l.z2);
-        DSP_TRY(conv_wgrad(b, c, cin, S0, st));
+        DSP_TRY(conv_wgrad_side(b, c, cin, S0, st));
         if (i == 0) break;
         // dz_{i}, with the BN-backward statistics of conv i-1 accumulated in the epilogue
         const ConvP& cb = l.convs[i - 1];
         const void* zmask = b->ws + (i == 1 ? l.z1 : l.z2);
         const BnbFuse fuse{zmask, &cb, nullptr};
         DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st, &fuse));
+        DSP_TRY(side_join(b, st));  // the WGRAD reading S0 is done before S0 is overwritten
         DSP_TRY(bn_backward_apply(b, S2, zmask, cb, S0, nullptr, nullptr, nullptr, st));
       }
       const void* res = S1;
       if (cs) {
-        DSP_TRY(conv_wgrad(b, *cs, x, S1, st));
+        DSP_TRY(conv_wgrad_side(b, *cs, x, S1, st));
         if (dx) DSP_TRY(conv_dgrad(b, *cs, S1, S3, nullptr, st));
         res = S3;
       }
       if (dx) DSP_TRY(conv_dgrad(b, l.convs[0], S0, dx, res, st, below));
+      DSP_TRY(side_join(b, st));
       return DSP_OK;
     }
   }
@@ -615,6 +647,11 @@ extern "C" int dsp_block_bind(dsp_block_t* b, void* workspace, float* params, fl
   b->grads = grads;
   b->tape_valid = false;
   cudaStream_t st = (cudaStream_t)stream;
+  if (b->side == nullptr) {  // created here, never during a graph capture
+    DSP_CUDA(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
+    DSP_CUDA(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+    DSP_CUDA(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
+  }
   // pad channels of every activation must read as zero; zero the whole workspace once
   DSP_CUDA(cudaMemsetAsync(b->ws, 0, b->ws_bytes, st));
   if (!b->packs.empty())
