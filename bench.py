@@ -38,11 +38,15 @@ DEPTH = 56
 CLASSES = 10
 IN_SHAPE = (3, 32, 32)
 
-# --model: BASELINE.json configs this bench can run (configs[1] is the default bench line;
-# configs[2] asks for Adam, which the reference rejects -- optim.py:70-71 -- so it is not offered)
+# --model: BASELINE.json configs this bench can run (configs[1] is the default bench line).
+# configs[2] asks for Adam, which the reference rejects (optim.py:70-71): it runs this package's
+# rule="adam" extension, checked against the oracle restatement only (tests/test_optim_gpu.py).
 MODELS = {
     "resnet56": dict(cfg=1, depth=56, classes=10, in_shape=(3, 32, 32), batch=128,
                      desc="ResNet-56 DSP K={K}, synthetic CIFAR-10-shaped 32x32x3, batch {B}"),
+    "resnet110": dict(cfg=2, depth=110, classes=10, in_shape=(3, 32, 32), batch=128, k=8,
+                      opt=dict(rule="adam", beta=0.0, s=1.0, lr=1e-3),
+                      desc="ResNet-110 DSP K={K}, synthetic CIFAR-10-shaped 32x32x3, batch {B}, Adam"),
     "resnet164": dict(cfg=3, depth=164, classes=100, in_shape=(3, 32, 32), batch=256,
                       desc="ResNet-164 (bottleneck) DSP K={K}, synthetic CIFAR-100-shaped 32x32x3, batch {B}"),
     "resnet50": dict(cfg=4, depth=50, classes=1000, in_shape=(3, 224, 224), batch=256,
@@ -74,10 +78,25 @@ def parse():
     return ap.parse_args()
 
 
+SUM_OPT = dict(rule="sum", beta=0.9, s=1.0, lr=0.1)
+
+
+def opt_of(args) -> dict:
+    """Optimizer of the --model config: SUM momentum, or Adam for configs[2]."""
+    return MODELS[args.model].get("opt", SUM_OPT)
+
+
+def opt_desc(args) -> str:
+    o = opt_of(args)
+    if o["rule"] == "adam":
+        return f"Adam b1=0.9 b2=0.999 eps=1e-8 (extension), lr {o['lr']}, wd 5e-4"
+    return f"SUM momentum beta={o['beta']} s={o['s']}, lr {o['lr']}, wd 5e-4"
+
+
 def blocks_for(args) -> int:
     if args.k:
         return args.k
-    return 8 if args.gpus >= 8 else 4
+    return MODELS[args.model].get("k", 8 if args.gpus >= 8 else 4)
 
 
 def workload(args):
@@ -102,7 +121,7 @@ def config_dict(args, K, world):
     m = MODELS[args.model]
     return {"workload": m["desc"].format(K=K, B=args.batch), "baseline_config": m["cfg"],
             "model": args.model if args.model == "resnet50" else f"{args.model}-cifar", "global_batch": args.batch, "k_blocks": K,
-            "queues": "p_k=1, m_k=2(K-1-k)", "optimizer": "SUM momentum beta=0.9 s=1, lr 0.1, wd 5e-4",
+            "queues": "p_k=1, m_k=2(K-1-k)", "optimizer": opt_desc(args),
             "parallelism": f"dsp-pipeline k{K} over {world} gpu(s)",
             "l2": "L2 flushed (256 MiB write) between timed steps; step working set > L2"}
 
@@ -169,8 +188,8 @@ def cpu_oracle_steps(args, steps: int, warmup: int, batch: int):
     om = R.build_model(olayers, bounds)
     R.init_params(om, 0)
     pool = R.synthetic_batches(4, batch, IN_SHAPE, CLASSES, seed=0)
-    eng = R.Engine(om, R.validate_config(cfg.p, cfg.m), R.cycle(pool), R.LrSchedule(0.1), rule="sum", beta=0.9,
-                   weight_decay=5e-4)
+    eng = R.Engine(om, R.validate_config(cfg.p, cfg.m), R.cycle(pool), R.LrSchedule(opt_of(args)["lr"]),
+                   rule=opt_of(args)["rule"], beta=opt_of(args)["beta"], weight_decay=5e-4)
     eng.run(warmup)
     t0 = time.perf_counter()
     r0 = os.times()
@@ -202,7 +221,7 @@ def run_reference(args):
     warm = max(1, min(args.warmup, 1 if big else 3))
     # bound the run to a few minutes: ~2.7 s per ResNet-56 K=4 step at batch 32 on 8 cores
     budget_s = 150.0
-    est = sub * {"resnet56": 0.085, "resnet164": 0.17, "resnet50": 3.0}.get(args.model, 0.1)
+    est = sub * {"resnet56": 0.085, "resnet110": 0.17, "resnet164": 0.17, "resnet50": 3.0}.get(args.model, 0.1)
     if (steps + warm) * est > budget_s:
         steps = max(1, int(budget_s / est) - warm)
     v, dt, cpu_s = cpu_oracle_steps(args, steps, warm, sub)
@@ -349,9 +368,10 @@ def run_b200(args):
     # device-resident pool generated on the GPU (csrc/synth.cu): bitwise the packed host pool
     from paper_1909_02625_b200.data import device_synthetic_batches
 
+    o = opt_of(args)
     dev_pool = device_synthetic_batches(npool, args.batch, IN_SHAPE, CLASSES, seed=0, device=dev, stream=stream)
-    eng = P.TrainEngine(model, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(0.1), rule="sum",
-                        beta=0.9, s=1.0, weight_decay=5e-4, device=dev)
+    eng = P.TrainEngine(model, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(o["lr"]), rule=o["rule"],
+                        beta=o["beta"], s=o["s"], weight_decay=5e-4, device=dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -433,8 +453,8 @@ def run_b200(args):
         if world == 1:
             from paper_1909_02625_b200.native import NativeEngine
 
-            eng2 = NativeEngine(model2, cfg, args.batch, P.LrSchedule(0.1), rule="sum", beta=0.9, s=1.0,
-                                weight_decay=5e-4, device=dev.index)
+            eng2 = NativeEngine(model2, cfg, args.batch, P.LrSchedule(o["lr"]), rule=o["rule"], beta=o["beta"],
+                                s=o["s"], weight_decay=5e-4, device=dev.index)
             xs = np.stack([np.asarray(x, dtype=np.float32) for x, _ in host_pool])
             ls = np.stack([np.asarray(lab, dtype=np.int64) for _, lab in host_pool])
             warm2 = max(warm, eng2.horizon + eng2.ring + 1)  # every graph phase captured before timing
@@ -451,8 +471,8 @@ def run_b200(args):
             how = ("host wall clock around dsp_run (engine C-ABI): per step pinned H2D of the fp32 batch + labels "
                    "and async D2H of the step's loss/grad-norm row; graphs replayed natively")
         else:
-            eng2 = P.TrainEngine(model2, cfg, cycle(host_pool), P.LrSchedule(0.1), rule="sum", beta=0.9, s=1.0,
-                                 weight_decay=5e-4, device=dev)
+            eng2 = P.TrainEngine(model2, cfg, cycle(host_pool), P.LrSchedule(o["lr"]), rule=o["rule"],
+                                 beta=o["beta"], s=o["s"], weight_decay=5e-4, device=dev)
             for _ in range(warm):
                 eng2.run(1)
                 eng2.last_loss()

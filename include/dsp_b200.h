@@ -57,6 +57,12 @@ extern "C" {
 
 #define DSP_RULE_SGD 0
 #define DSP_RULE_SUM 1
+/* Bias-corrected Adam: an EXTENSION for BASELINE configs[2] (the reference rejects rule "adam",
+ * optim.py:70-71; parity is against this repo's restatement oracle/dsp_ref.py adam_step only). */
+#define DSP_RULE_ADAM 2
+/* fp32 Adam state of an n-parameter block: m[n], v[n], then an int64 step counter at float
+ * offset 2n (counts applied updates; zero = fresh, OptimizerState.for_params). */
+#define DSP_ADAM_STATE_BYTES(n) ((size_t)(n) * 8 + 8)
 
 /* ------------------------------------------------------------ kernel level */
 typedef struct {
@@ -180,6 +186,19 @@ int dsp_block_forward(dsp_block_t* blk, const void* x, void* y, int record, void
 /* softmax_xent on the recorded logits (last block only): writes the mean loss
  * to *loss_dev (device fp32) and keeps dlogits as the backward upstream. */
 int dsp_block_loss(dsp_block_t* blk, const int64_t* labels_dev, float* loss_dev, void* stream);
+/* Bias-corrected Adam (DSP_RULE_ADAM extension), flat vectors of length n:
+ *   g = grad + wd*x (only if wd != 0); m' = b1*m + (1-b1)*g; v' = b2*v + (1-b2)*g*g
+ *   x' = x - (lr*(m'/bc1)) / (sqrt(v'/bc2) + eps),  bc_i = 1 - b_i^t
+ * t = *tstep + 1 when tstep (device int64) is given -- the call then also increments it --,
+ * else bc1/bc2 are taken from the host.  The fp64 variant keeps the restatement's IEEE op
+ * order (no FMA contraction). */
+int dsp_update_adam_f64(int64_t n, double* x, const double* grad, double* m, double* v, int64_t* tstep, double bc1,
+                        double bc2, double lr, double b1, double b2, double eps, double wd, double* grad_sq,
+                        void* stream);
+int dsp_update_adam_f32(int64_t n, float* x, const float* grad, float* m, float* v, int64_t* tstep, double bc1,
+                        double bc2, double lr, double b1, double b2, double eps, double wd, float* grad_sq,
+                        void* stream);
+
 /* block_backward on the recorded tape.  upstream: padded dY (NULL for the
  * last block, which uses dlogits).  grad_in: padded dX or NULL to skip the
  * input gradient (block 0).  Writes the flat fp32 parameter gradient. */
@@ -187,6 +206,11 @@ int dsp_block_backward(dsp_block_t* blk, const void* upstream, void* grad_in, vo
 /* Update the bound params from the bound grads and re-pack the weight shadow. */
 int dsp_block_update(dsp_block_t* blk, int rule, float* ys, double lr, double slr, double beta, double wd,
                      int apply, float* grad_sq_out, void* stream);
+
+/* Adam variant of dsp_block_update: state = DSP_ADAM_STATE_BYTES(param_count) bytes of device
+ * memory laid out as described at DSP_ADAM_STATE_BYTES (the step counter advances on apply). */
+int dsp_block_update_adam(dsp_block_t* blk, void* state, double lr, double b1, double b2, double eps, double wd,
+                          int apply, float* grad_sq_out, void* stream);
 
 /* ------------------------------------------------------------ utilities */
 /* Host fp64 batch -> padded device activation (storage dtype).  x_dev points
@@ -258,6 +282,9 @@ size_t dsp_param_count(dsp_engine_t* eng, int k);
  * (optim.py:38-45); wd couples into the gradient (pipeline.py:591-593). */
 int dsp_set_optimizer(dsp_engine_t* eng, int rule, double beta, double s, double wd, double base_lr,
                       const int64_t* decay_steps, const double* factors, int n_decay);
+/* Adam hyper-parameters (rule DSP_RULE_ADAM; defaults 0.9 / 0.999 / 1e-8, oracle adam_step).
+ * beta / s of dsp_set_optimizer are unused by Adam. */
+int dsp_set_adam(dsp_engine_t* eng, double beta1, double beta2, double eps);
 /* n_steps DSP steps. x: host float32 [n_steps][B][C*H*W], labels: host int64
  * [n_steps][B] -- batch n of this call is the data stream's next batch. Each
  * step copies its batch host->device and its loss / grad-norm row device->host

@@ -36,7 +36,7 @@ from .blocks import (
 from .data import Dataset, TeacherSpec, batch_iter, epoch_stream, gen_teacher_dataset
 from .deviation import DeviationRow, DeviceOperators
 from .native import NativeEngine
-from .optim import LrSchedule, NonFiniteError, OptimizerState, apply_update, lr_at, sgd_step, sum_step
+from .optim import LrSchedule, NonFiniteError, OptimizerState, adam_step, apply_update, lr_at, sgd_step, sum_step
 from .pipeline import (
     ActivationPacket,
     ConfigError,
@@ -61,7 +61,7 @@ __all__ = [
     "ActivationPacket", "B200Unavailable", "Block", "ConfigError", "DeadlockError", "DspError", "GradPacket",
     "LayerSpec", "LogRecord", "NativeEngine", "LrSchedule", "Model", "NonFiniteError", "OptimizerState", "PipelineConfig",
     "ProtocolError", "RuntimeStraggler", "SeededRng", "ShapeError", "StalenessProfile", "TrainEngine", "TrainLog",
-    "apply_update", "avgpool", "basic_unit", "bottleneck", "build_model", "conv_bn_relu", "default_placement",
+    "adam_step", "apply_update", "avgpool", "basic_unit", "bottleneck", "build_model", "conv_bn_relu", "default_placement",
     "default_queue_config", "dense", "derive_seed", "flop_balanced_boundaries", "init_params", "lr_at", "maxpool",
     "mix64", "relu", "resnet50_layers", "resnet_cifar_bottleneck_layers", "resnet_cifar_layers", "sgd_step",
     "staleness_of", "suggest_boundaries", "sum_step", "tanh", "validate_config",

@@ -37,6 +37,7 @@ DSP_LAYER_MAXPOOL = 14
 
 DSP_RULE_SGD = 0
 DSP_RULE_SUM = 1
+DSP_RULE_ADAM = 2  # extension (BASELINE configs[2]); the reference rejects 'adam'
 
 
 class B200Unavailable(RuntimeError):
@@ -131,6 +132,13 @@ _SIGNATURES = {
     "dsp_block_forward": (C.c_int, [_P, _P, _P, C.c_int, _P]),
     "dsp_block_loss": (C.c_int, [_P, _P, _P, _P]),
     "dsp_block_backward": (C.c_int, [_P, _P, _P, _P]),
+    "dsp_update_adam_f64": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, C.c_double, C.c_double, _P, _P]),
+    "dsp_update_adam_f32": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, C.c_double, C.c_double, _P, _P]),
+    "dsp_block_update_adam": (C.c_int, [_P, _P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                        C.c_int, _P, _P]),
+    "dsp_set_adam": (C.c_int, [_P, C.c_double, C.c_double, C.c_double]),
     "dsp_block_update": (C.c_int, [_P, C.c_int, _P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
                                    _P, _P]),
     "dsp_pack_input": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),

@@ -134,3 +134,39 @@ extern "C" int dsp_unpack_output(const void* in, float* out_dev, int batch, int 
   return cuda_check(unpack_output(in, out_dev, batch, c, h, w, c_pad, dtype, nchw, (cudaStream_t)stream),
                     "unpack_output");
 }
+
+namespace {
+template <typename T>
+int update_adam_abi(const char* fn, int64_t n, T* x, const T* grad, T* m, T* v, int64_t* tstep, double bc1,
+                    double bc2, double lr, double b1, double b2, double eps, double wd, T* grad_sq, void* stream,
+                    cudaError_t (*sum_parts)(const T*, int, T*, cudaStream_t)) {
+  if (n < 0 || (n > 0 && (!x || !grad || !m || !v))) return set_error(DSP_E_INVALID, "%s: bad vectors", fn);
+  if (!(b1 >= 0.0 && b1 < 1.0) || !(b2 >= 0.0 && b2 < 1.0) || !(eps > 0.0))
+    return set_error(DSP_E_INVALID, "%s: bad hyper-parameters", fn);
+  if (tstep == nullptr && !(bc1 > 0.0 && bc2 > 0.0)) return set_error(DSP_E_INVALID, "%s: bad bias corrections", fn);
+  if (n == 0) return DSP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  T* part = nullptr;
+  if (grad_sq) DSP_CUDA(cudaMallocAsync((void**)&part, sizeof(T) * update_grid(n), st));
+  DSP_CUDA(update_adam<T>(n, x, grad, m, v, tstep, bc1, bc2, lr, b1, b2, eps, wd, part, st));
+  if (grad_sq) {
+    DSP_CUDA(sum_parts(part, update_grid(n), grad_sq, st));
+    DSP_CUDA(cudaFreeAsync(part, st));
+  }
+  return DSP_OK;
+}
+}  // namespace
+
+extern "C" int dsp_update_adam_f64(int64_t n, double* x, const double* grad, double* m, double* v, int64_t* tstep,
+                                   double bc1, double bc2, double lr, double b1, double b2, double eps, double wd,
+                                   double* grad_sq, void* stream) {
+  return update_adam_abi<double>("dsp_update_adam_f64", n, x, grad, m, v, tstep, bc1, bc2, lr, b1, b2, eps, wd,
+                                 grad_sq, stream, sum_partials_f64);
+}
+
+extern "C" int dsp_update_adam_f32(int64_t n, float* x, const float* grad, float* m, float* v, int64_t* tstep,
+                                   double bc1, double bc2, double lr, double b1, double b2, double eps, double wd,
+                                   float* grad_sq, void* stream) {
+  return update_adam_abi<float>("dsp_update_adam_f32", n, x, grad, m, v, tstep, bc1, bc2, lr, b1, b2, eps, wd,
+                                grad_sq, stream, sum_partials_f32);
+}

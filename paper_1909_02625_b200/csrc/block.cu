@@ -756,3 +756,28 @@ extern "C" int dsp_block_update(dsp_block_t* b, int rule, float* ys, double lr, 
   if (apply) DSP_TRY(dsp_block_pack(b, stream));
   return DSP_OK;
 }
+
+extern "C" int dsp_block_update_adam(dsp_block_t* b, void* state, double lr, double b1, double b2, double eps,
+                                     double wd, int apply, float* grad_sq_out, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_update_adam: block not bound");
+  if (!state) return set_error(DSP_E_INVALID, "dsp_block_update_adam: null state");
+  if (!(b1 >= 0.0 && b1 < 1.0) || !(b2 >= 0.0 && b2 < 1.0) || !(eps > 0.0))
+    return set_error(DSP_E_INVALID, "dsp_block_update_adam: bad hyper-parameters");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = b->param_count;
+  if (n == 0) {
+    if (grad_sq_out) DSP_CUDA(cudaMemsetAsync(grad_sq_out, 0, sizeof(float), st));
+    return DSP_OK;
+  }
+  float* part = at<float>(b, b->upart);
+  float* m = static_cast<float*>(state);
+  if (apply) {
+    int64_t* t = reinterpret_cast<int64_t*>(m + 2 * n);
+    DSP_CUDA(update_adam<float>(n, b->params, b->grads, m, m + n, t, 0.0, 0.0, lr, b1, b2, eps, wd, part, st));
+  } else {
+    DSP_CUDA(sumsq_f32(n, b->grads, part, st));  // grad norm only (discarded warmup update)
+  }
+  if (grad_sq_out) DSP_CUDA(sum_partials_f32(part, update_grid(n), grad_sq_out, st));
+  if (apply) DSP_TRY(dsp_block_pack(b, stream));
+  return DSP_OK;
+}

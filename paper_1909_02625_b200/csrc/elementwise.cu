@@ -848,6 +848,71 @@ __global__ void update_f64_k(int64_t n, double* __restrict__ x, const double* __
   if (threadIdx.x == 0 && part) part[blockIdx.x] = red[0];
 }
 
+// IEEE round-to-nearest ops without FMA contraction, per precision (optimizer kernels)
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+
+// Bias-corrected Adam per block (BASELINE configs[2]; an extension -- the reference rejects
+// rule "adam", optim.py:70-71 -- restated in oracle/dsp_ref.py adam_step, same IEEE op order):
+//   g = grad (+ wd*x);  m' = b1*m + (1-b1)*g;  v' = b2*v + (1-b2)*(g*g)
+//   x' = x - (lr * (m'/bc1)) / (sqrt(v'/bc2) + eps),  bc_i = 1 - b_i^t
+// t = *tstep + 1 read from device memory (so step graphs stay valid as t advances; the
+// caller bumps the counter after the launch), or bc1/bc2 from the host when tstep == nullptr.
+template <typename T, bool WD>
+__global__ void update_adam_k(int64_t n, T* __restrict__ x, const T* __restrict__ grad, T* __restrict__ m,
+                              T* __restrict__ v, const int64_t* __restrict__ tstep, double bc1h, double bc2h, T lr,
+                              double b1, double b2, double eps, T wd, T* __restrict__ part) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  __shared__ T red[kThreads];
+  __shared__ double bc[2];
+  if (threadIdx.x == 0) {
+    if (tstep != nullptr) {
+      const double t = (double)(*tstep + 1);
+      bc[0] = 1.0 - pow(b1, t);
+      bc[1] = 1.0 - pow(b2, t);
+    } else {
+      bc[0] = bc1h;
+      bc[1] = bc2h;
+    }
+  }
+  __syncthreads();
+  const T c1 = (T)bc[0], c2 = (T)bc[1];
+  const T B1 = (T)b1, A1 = (T)(1.0 - b1), B2 = (T)b2, A2 = (T)(1.0 - b2), E = (T)eps;
+  T sq = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T g0 = grad[i];
+    sq = add_rn(sq, mul_rn(g0, g0));
+    const T xv = x[i];
+    const T g = WD ? add_rn(g0, mul_rn(wd, xv)) : g0;
+    const T mi = add_rn(mul_rn(B1, m[i]), mul_rn(A1, g));
+    const T vi = add_rn(mul_rn(B2, v[i]), mul_rn(A2, mul_rn(g, g)));
+    m[i] = mi;
+    v[i] = vi;
+    const T den = add_rn(sqrt_rn(div_rn(vi, c2)), E);
+    x[i] = sub_rn(xv, div_rn(mul_rn(lr, div_rn(mi, c1)), den));
+  }
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && part) part[blockIdx.x] = red[0];
+}
+
+__global__ void step_bump_k(int64_t* tstep) {
+  pdl_wait();
+  *tstep += 1;
+}
+
 __global__ void sumsq_k(int64_t n, const float* __restrict__ v, float* __restrict__ part) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   __shared__ float red[kThreads];
@@ -1104,6 +1169,29 @@ cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* 
   }
   return note_launch(), cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t update_adam(int64_t n, T* x, const T* grad, T* m, T* v, const int64_t* tstep, double bc1, double bc2,
+                        double lr, double b1, double b2, double eps, double wd, T* part, cudaStream_t st) {
+  const int g = update_grid(n);
+  if (wd != 0.0)
+    launch_k(update_adam_k<T, true>, g, kThreads, 0, st, n, x, grad, m, v, tstep, bc1, bc2, (T)lr, b1, b2, eps,
+             (T)wd, part);
+  else
+    launch_k(update_adam_k<T, false>, g, kThreads, 0, st, n, x, grad, m, v, tstep, bc1, bc2, (T)lr, b1, b2, eps,
+             (T)wd, part);
+  note_launch();
+  if (tstep != nullptr) {
+    // device-side step counter: bumped after every CTA of the update has read it
+    launch_k(step_bump_k, 1, 1, 0, st, const_cast<int64_t*>(tstep));
+    note_launch();
+  }
+  return cudaGetLastError();
+}
+template cudaError_t update_adam<float>(int64_t, float*, const float*, float*, float*, const int64_t*, double, double,
+                                        double, double, double, double, double, float*, cudaStream_t);
+template cudaError_t update_adam<double>(int64_t, double*, const double*, double*, double*, const int64_t*, double,
+                                         double, double, double, double, double, double, double*, cudaStream_t);
 
 cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr, double slr,
                        double beta, double wd, double* part, cudaStream_t st) {

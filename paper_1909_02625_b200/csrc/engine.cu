@@ -72,6 +72,7 @@ struct dsp_engine {
   // optimizer
   int rule = DSP_RULE_SGD;
   double beta = 0.0, s = 1.0, wd = 0.0, base_lr = 0.01;
+  double adam_b1 = 0.9, adam_b2 = 0.999, adam_eps = 1e-8;  // rule DSP_RULE_ADAM (extension)
   std::vector<std::pair<int64_t, double>> decays;
   // execution
   cudaStream_t stream = nullptr;
@@ -166,6 +167,9 @@ int issue_block(dsp_engine* e, int k, int64_t n, cudaStream_t st) {
     DSP_TRY(dsp_block_backward(e->blk[k], nullptr, k > 0 ? e->ring_gin[k][ph] : nullptr, st));
   }
   const double lr = lr_at(e, n);
+  if (e->rule == DSP_RULE_ADAM)  // ys[k] holds the Adam state (m, v, step counter)
+    return dsp_block_update_adam(e->blk[k], e->ys[k], lr, e->adam_b1, e->adam_b2, e->adam_eps, e->wd,
+                                 apply_update(e, k, n) ? 1 : 0, loss_slot + 1, st);
   return dsp_block_update(e->blk[k], e->rule, e->ys[k], lr, e->s * lr, e->beta, e->wd, apply_update(e, k, n) ? 1 : 0,
                           loss_slot + 1, st);
 }
@@ -268,7 +272,10 @@ extern "C" int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out) {
     if ((rc = dmalloc(&e->ws[k], dsp_block_workspace_bytes(e->blk[k]))) != DSP_OK) return fail(rc);
     if ((rc = dmalloc(&e->params[k], sizeof(float) * e->nparam[k], true)) != DSP_OK) return fail(rc);
     if ((rc = dmalloc(&e->grads[k], sizeof(float) * e->nparam[k], true)) != DSP_OK) return fail(rc);
-    if ((rc = dmalloc(&e->ys[k], sizeof(float) * e->nparam[k], true)) != DSP_OK) return fail(rc);
+    // optimizer state: ys (SUM) or the Adam state, whichever rule dsp_set_optimizer picks
+    if ((rc = dmalloc(&e->ys[k], std::max(sizeof(float) * e->nparam[k], DSP_ADAM_STATE_BYTES(e->nparam[k])), true)) !=
+        DSP_OK)
+      return fail(rc);
   }
   if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(DSP_E_CUDA);
   for (int k = 0; k < K; ++k) {
@@ -333,7 +340,11 @@ extern "C" int dsp_set_params(dsp_engine_t* e, int k, const void* src, size_t n,
     ENG_CUDA(cudaStreamSynchronize(e->stream));
   }
   // optimizer state follows the parameters (OptimizerState.for_params: ys_0 = x_0)
-  ENG_CUDA(cudaMemcpyAsync(e->ys[k], e->params[k], sizeof(float) * n, cudaMemcpyDeviceToDevice, e->stream));
+  // (Adam: m = v = 0, step counter 0)
+  if (e->rule == DSP_RULE_ADAM)
+    ENG_CUDA(cudaMemsetAsync(e->ys[k], 0, DSP_ADAM_STATE_BYTES(n), e->stream));
+  else
+    ENG_CUDA(cudaMemcpyAsync(e->ys[k], e->params[k], sizeof(float) * n, cudaMemcpyDeviceToDevice, e->stream));
   DSP_TRY(dsp_block_pack(e->blk[k], e->stream));
   ENG_CUDA(cudaStreamSynchronize(e->stream));
   return DSP_OK;
@@ -353,9 +364,20 @@ extern "C" int dsp_get_params(dsp_engine_t* e, int k, double* dst, size_t n) {
 extern "C" int dsp_set_optimizer(dsp_engine_t* e, int rule, double beta, double s, double wd, double base_lr,
                                  const int64_t* decay_steps, const double* factors, int n_decay) {
   if (!e) return set_error(DSP_E_INVALID, "dsp_set_optimizer: null engine");
-  if (rule != DSP_RULE_SGD && rule != DSP_RULE_SUM) return set_error(DSP_E_INVALID, "dsp_set_optimizer: bad rule %d", rule);
+  if (rule != DSP_RULE_SGD && rule != DSP_RULE_SUM && rule != DSP_RULE_ADAM)
+    return set_error(DSP_E_INVALID, "dsp_set_optimizer: bad rule %d", rule);
   if (n_decay < 0 || (n_decay > 0 && (!decay_steps || !factors)))
     return set_error(DSP_E_INVALID, "dsp_set_optimizer: bad decay list");
+  if (rule != e->rule) {  // re-initialise the optimizer state for the new rule (for_params)
+    for (int k = 0; k < e->K; ++k) {
+      const size_t n = (size_t)e->nparam[k];
+      if (rule == DSP_RULE_ADAM)
+        ENG_CUDA(cudaMemsetAsync(e->ys[k], 0, DSP_ADAM_STATE_BYTES(n), e->stream));
+      else if (n)
+        ENG_CUDA(cudaMemcpyAsync(e->ys[k], e->params[k], sizeof(float) * n, cudaMemcpyDeviceToDevice, e->stream));
+    }
+    ENG_CUDA(cudaStreamSynchronize(e->stream));
+  }
   e->rule = rule;
   e->beta = beta;
   e->s = s;
@@ -472,4 +494,19 @@ extern "C" void dsp_destroy(dsp_engine_t* e) {
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   delete e;
+}
+
+extern "C" int dsp_set_adam(dsp_engine_t* e, double beta1, double beta2, double eps) {
+  if (!e) return set_error(DSP_E_INVALID, "dsp_set_adam: null engine");
+  if (!(beta1 >= 0.0 && beta1 < 1.0) || !(beta2 >= 0.0 && beta2 < 1.0) || !(eps > 0.0))
+    return set_error(DSP_E_INVALID, "dsp_set_adam: bad hyper-parameters");
+  e->adam_b1 = beta1;
+  e->adam_b2 = beta2;
+  e->adam_eps = eps;
+  for (auto& P : e->phases)  // captured steps baked the old constants in
+    if (P.exec) {
+      cudaGraphExecDestroy(P.exec);
+      P.exec = nullptr;
+    }
+  return DSP_OK;
 }

@@ -89,6 +89,11 @@ cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* 
                        float wd, float* part, cudaStream_t st);
 cudaError_t update_f64(int rule, int64_t n, double* x, const double* grad, double* ys, double* y, double lr,
                        double slr, double beta, double wd, double* part, cudaStream_t st);
+// Bias-corrected Adam (extension, BASELINE configs[2]); tstep: device step counter (bumped by
+// a follow-up launch) or nullptr with host bias corrections bc1/bc2.
+template <typename T>
+cudaError_t update_adam(int64_t n, T* x, const T* grad, T* m, T* v, const int64_t* tstep, double bc1, double bc2,
+                        double lr, double b1, double b2, double eps, double wd, T* part, cudaStream_t st);
 // Per-CTA partial sums of v^2 (grid = update_grid(n)).
 cudaError_t sumsq_f32(int64_t n, const float* v, float* part, cudaStream_t st);
 // Sum per-CTA partials in fixed order into *out.

@@ -77,6 +77,7 @@ class B200Runtime:
         self.num_classes = model.output_dim
         self.dev = {}
         self.ys = {}
+        self.adam = OptimizerState(rule="adam")  # Adam hyper-parameters (extension; defaults of the oracle)
         for k in self.local:
             blk = model.blocks[k]
             db = DeviceBlock(blk, batch, is_last=(k == self.K - 1), device=self.device, stream=self.stream)
@@ -85,6 +86,9 @@ class B200Runtime:
             if rule == "sum":
                 with torch.cuda.stream(self.stream):
                     self.ys[k] = db.params.clone()
+            elif rule == "adam":  # [m | v | int64 step counter] (DSP_ADAM_STATE_BYTES), zero = fresh
+                n = db.params.numel()
+                self.ys[k] = torch.zeros(2 * n + 2, dtype=torch.float32, device=self.device)
         # ---- rings (slot = step mod R) -------------------------------------------
         if config is not None:
             p, m, q = config.p, config.m, config.q
@@ -314,14 +318,26 @@ class B200Runtime:
         return gin
 
     def update(self, k: int, lr: float, slr: float, apply: bool, n: int = 0):
-        if self.mode != "replay":
+        if self.mode != "replay" and self.rule == "adam":
+            st = self.adam
+            self.dev[k].update_adam(self.ys[k], lr, st.beta1, st.beta2, st.eps, self.wd, apply,
+                                    self._slot_tensor(n, k, 1), stream=self._s(k))
+        elif self.mode != "replay":
             self.dev[k].update(self.rule_code, self.ys.get(k), lr, slr, self.beta, self.wd, apply,
                                self._slot_tensor(n, k, 1), stream=self._s(k))
         return self._slot(n, k, 1)
 
     def opt_state(self, k: int) -> OptimizerState:
         st = OptimizerState(rule=self.rule, beta=self.beta, s=self.s)
-        st.ys = self.ys.get(k)
+        if self.rule == "adam":
+            torch = self.torch
+            n = self.dev[k].params.numel()
+            self.synchronize()
+            state = self.ys[k]
+            st.m1, st.m2 = state[:n], state[n:2 * n]
+            st.n = int(state[2 * n:2 * n + 2].view(torch.int64)[0].item())  # applied updates
+        else:
+            st.ys = self.ys.get(k)
         return st
 
     # ---------------------------------------------------------------- graph steps

@@ -76,6 +76,11 @@ class NativeEngine:
         L.check(lib.dsp_set_optimizer(h, RULES[rule], beta, s, weight_decay, schedule.base,
                                       steps.ctypes.data_as(C.POINTER(C.c_int64)),
                                       facs.ctypes.data_as(C.POINTER(C.c_double)), len(steps)))
+        if rule == "adam":  # extension: the oracle's fixed Adam hyper-parameters
+            from .optim import OptimizerState
+
+            ad = OptimizerState(rule="adam")
+            L.check(lib.dsp_set_adam(h, ad.beta1, ad.beta2, ad.eps))
 
     def __del__(self):
         h = getattr(self, "h", None)

@@ -11,6 +11,11 @@
 
 The SUM state keeps ``ys`` on the device; ``y`` (written but never read by the
 reference, optim.py:97) is materialised only on the float64 path.
+
+``rule="adam"`` is this package's EXTENSION for BASELINE configs[2] (ResNet-110,
+Adam): the reference rejects it (optim.py:70-71), so its parity is pinned only
+against the restatement ``oracle/dsp_ref.py`` ``adam_step`` (bias-corrected
+Adam, beta1 0.9, beta2 0.999, eps 1e-8; ``beta`` / ``s`` are unused by it).
 """
 
 from __future__ import annotations
@@ -54,7 +59,7 @@ def lr_at(schedule: LrSchedule, n: int) -> float:
     return lr
 
 
-RULES = {"sgd": L.DSP_RULE_SGD, "sum": L.DSP_RULE_SUM}
+RULES = {"sgd": L.DSP_RULE_SGD, "sum": L.DSP_RULE_SUM, "adam": L.DSP_RULE_ADAM}
 
 
 @dataclass
@@ -67,6 +72,12 @@ class OptimizerState:
     y: object = None
     ys: object = None
     n: int = 0
+    # adam (extension; unpinned against the reference, which rejects it)
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    m1: object = None
+    m2: object = None
 
     def __post_init__(self):
         if self.rule not in RULES:
@@ -82,6 +93,9 @@ class OptimizerState:
         if rule == "sum":
             st.ys = _clone(x0)  # ys[0] = x[0]: first momentum correction is zero
             st.y = _clone(x0)
+        elif rule == "adam":
+            st.m1 = np.zeros_like(x0) if isinstance(x0, np.ndarray) else x0.new_zeros(x0.shape)
+            st.m2 = _clone(st.m1)
         return st
 
 
@@ -140,8 +154,42 @@ def sum_step(state: OptimizerState, x, g, lr: float):
     return out
 
 
+def adam_step(state: OptimizerState, x, g, lr: float):
+    """Bias-corrected Adam on the device (extension; oracle/dsp_ref.py adam_step, same op order).
+
+    Float64 inputs are bitwise equal to the restatement: bc_i = 1 - beta_i**t is formed here
+    exactly as the oracle forms it and handed to ``dsp_update_adam_f64``."""
+    if state.rule != "adam" or state.m1 is None:
+        raise RuntimeError("adam state not initialized; use OptimizerState.for_params")
+    torch = torch_mod()
+    xd, host = _to_dev64(x)
+    gd, _ = _to_dev64(g)
+    if not bool(torch.isfinite(gd).all()):
+        raise NonFiniteError("non-finite gradient in update")
+    xo = xd.clone()
+    m1 = _to_dev64(state.m1)[0].clone()
+    m2 = _to_dev64(state.m2)[0].clone()
+    t = state.n + 1
+    bc1 = 1.0 - state.beta1 ** t
+    bc2 = 1.0 - state.beta2 ** t
+    stream = torch.cuda.current_stream()
+    L.check(L.load().dsp_update_adam_f64(xo.numel(), ptr(xo), ptr(gd), ptr(m1), ptr(m2), None, C.c_double(bc1),
+                                         C.c_double(bc2), C.c_double(lr), C.c_double(state.beta1),
+                                         C.c_double(state.beta2), C.c_double(state.eps), C.c_double(0.0), None,
+                                         C.c_void_p(stream.cuda_stream)))
+    if host:
+        xo, m1, m2 = xo.cpu().numpy(), m1.cpu().numpy(), m2.cpu().numpy()
+    state.m1, state.m2 = m1, m2
+    return xo
+
+
 def apply_update(state: OptimizerState, x, g, lr: float):
     """Advance one step under the state's rule (optim.py:102-109)."""
-    out = sgd_step(x, g, lr) if state.rule == "sgd" else sum_step(state, x, g, lr)
+    if state.rule == "sgd":
+        out = sgd_step(x, g, lr)
+    elif state.rule == "sum":
+        out = sum_step(state, x, g, lr)
+    else:
+        out = adam_step(state, x, g, lr)
     state.n += 1
     return out

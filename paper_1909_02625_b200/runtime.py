@@ -117,6 +117,12 @@ class DeviceBlock:
                                           stream_ptr(stream or self.stream)))
 
 
+    def update_adam(self, state, lr: float, b1: float, b2: float, eps: float, wd: float, apply: bool, grad_sq_out,
+                    stream=None) -> None:
+        L.check(self.lib.dsp_block_update_adam(self.h, ptr(state), C.c_double(lr), C.c_double(b1), C.c_double(b2),
+                                               C.c_double(eps), C.c_double(wd), int(apply), ptr(grad_sq_out),
+                                               stream_ptr(stream or self.stream)))
+
 def pack_input(x_host: np.ndarray, shape: tuple, device, stream):
     """Host float batch (B, C*H*W) in (C,H,W) order -> padded NHWC bf16 device packet."""
     torch = torch_mod()

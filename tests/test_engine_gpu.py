@@ -42,7 +42,7 @@ def _run(layers, boundaries, p, m, B, steps, in_shape, classes, rule="sum", beta
     return eng, pm, refs
 
 
-def _check(eng, pm, refs, m):
+def _check(eng, pm, refs, m, scale=1.0):
     log = eng.log
     assert eng.realized_staleness() == list(m)
     for mode, (ref, om) in refs.items():
@@ -52,14 +52,14 @@ def _check(eng, pm, refs, m):
         ref_loss = {r.step: r.loss for r in ref.records if r.loss is not None}
         for step, loss in log.losses():
             want = ref_loss[step]
-            assert abs(loss - want) <= LOSS_TOL[mode] * max(1.0, abs(want)), (mode, step, loss, want)
+            assert abs(loss - want) <= scale * LOSS_TOL[mode] * max(1.0, abs(want)), (mode, step, loss, want)
         ref_gn = {(r.step, r.block): r.grad_norm for r in ref.records}
         for r in log.records:
             want = ref_gn[(r.step, r.block)]
-            assert abs(r.grad_norm - want) <= GN_TOL[mode] * max(want, 1e-3), (mode, r.step, r.block, r.grad_norm,
+            assert abs(r.grad_norm - want) <= scale * GN_TOL[mode] * max(want, 1e-3), (mode, r.step, r.block, r.grad_norm,
                                                                              want)
         for bp, bo in zip(pm.blocks, om.blocks):
-            assert rel_err(bp.params, bo.params) < PARAM_TOL[mode], (mode, bp.index, rel_err(bp.params, bo.params))
+            assert rel_err(bp.params, bo.params) < scale * PARAM_TOL[mode], (mode, bp.index, rel_err(bp.params, bo.params))
 
 
 def test_resnet_k2_sum():
@@ -191,3 +191,17 @@ def test_resnet20_k8_default_queues_graph_replay():
     assert np.all(dev <= 3 * floor + 5e-3), ("device (loss, grad-norm, params) err", dev, "noise floor", floor)
     f64 = _divergence(eng.log.records, eng.log.losses(), pm.blocks, refs["f64"][0], refs["f64"][1].blocks)
     assert np.all(f64 <= [LOSS_TOL["f64"], GN_TOL["f64"], PARAM_TOL["f64"]]), f64
+
+
+def test_resnet_k3_adam_extension():
+    """rule="adam" (BASELINE configs[2]; an extension the reference rejects) vs the oracle's
+    adam_step restatement, discard warmup + weight decay, lr decay mid-run.  Adam's normalised
+    step turns the bf16 storage rounding into O(lr) parameter moves wherever g ~ 0, so the
+    trajectory tolerances are 3x the SUM/SGD ones (the update kernel itself is pinned to 1e-5
+    in tests/test_optim_gpu.py)."""
+    layers = small_resnet(in_shape=(3, 8, 8))
+    eng, pm, refs = _run(layers, [2, 4], (1, 1, 0), (4, 2, 0), 8, 12, (3, 8, 8), 10, rule="adam", beta=0.0,
+                         lr=2e-3, warmup="discard_warmup_updates", wd=5e-4)
+    _check(eng, pm, refs, (4, 2, 0), scale=3.0)
+    for k in range(3):  # applied-update counter = steps whose stale tag is >= 0
+        assert eng.rt.opt_state(k).n == sum(1 for r in eng.log.records if r.block == k and r.batch_index >= 0)

@@ -138,7 +138,10 @@ def test_trainlog_checksum_format_matches_reference():
 
 def test_optimizer_state_validation():
     with pytest.raises(ValueError):
-        P.OptimizerState(rule="adam")
+        P.OptimizerState(rule="rmsprop")
+    # "adam" is this package's extension (BASELINE configs[2]); the reference rejects it
+    ad = P.OptimizerState.for_params("adam", np.ones(3))
+    assert np.array_equal(ad.m1, np.zeros(3)) and np.array_equal(ad.m2, np.zeros(3)) and ad.n == 0
     with pytest.raises(ValueError):
         P.OptimizerState(rule="sum", beta=1.0)
     with pytest.raises(ValueError):

@@ -56,6 +56,14 @@ def test_k3_discard_sgd_wd_matches_python_engine():
     _same(py, pm, ne)
 
 
+def test_k4_adam_graphs_match_python_engine():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    cfg = P.default_queue_config(4)
+    py, pm, ne, *_ = _pair(layers, [1, 2, 3], cfg.p, cfg.m, 8, 24, (3, 8, 8), 10, rule="adam", beta=0.0, lr=2e-3,
+                           wd=5e-4)
+    _same(py, pm, ne)
+
+
 def test_k1_plain_bp_matches_python_engine():
     layers = small_resnet(in_shape=(3, 8, 8))
     py, pm, ne, *_ = _pair(layers, [], (0,), (0,), 16, 10, (3, 8, 8), 10, rule="sgd", beta=0.0)
