@@ -177,6 +177,74 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+class NvmlClockSampler:
+    """SM clocks + clock-event reasons sampled in-process through NVML every 5 ms while the
+    timed region runs (the nvidia-smi sampler's ~1 s start-up outlasts a 50 ms timed region,
+    leaving it without samples); falls back to ClockSampler when NVML is absent."""
+
+    PERIOD_S = 0.005
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.fallback = None
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = None
+            try:  # the CUDA device by UUID (NVML indices ignore CUDA_VISIBLE_DEVICES)
+                import torch
+
+                uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+                self.h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self._sample()  # one sample at the region start
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.N = None
+            self.fallback = ClockSampler(self.index).__enter__()
+        return self
+
+    def _sample(self):
+        N = self.N
+        self.rows.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM), self.max_mhz,
+                          N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+
+    def _loop(self):
+        while not self._stop.wait(self.PERIOD_S):
+            try:
+                self._sample()
+            except Exception:
+                return
+
+    def __exit__(self, *exc):
+        if self.fallback is not None:
+            return self.fallback.__exit__(*exc)
+        self._stop.set()
+        self.thread.join(timeout=1)
+        return False
+
+    def summary(self):
+        if self.fallback is not None:
+            return self.fallback.summary()
+        N = self.N
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({name for _, _, r in self.rows for name, b in bits.items() if r & b})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 5 ms period over the timed region"}
+
+
 # ------------------------------------------------------------------ CPU oracle (reference algorithm)
 def cpu_oracle_steps(args, steps: int, warmup: int, batch: int):
     """Time the float64 CPU restatement of the reference DSP step (oracle/)."""
@@ -399,7 +467,7 @@ def run_b200(args):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = eng.rt.kernels_executed()
-    with ClockSampler(dev.index) as clk:
+    with NvmlClockSampler(dev.index) as clk:
         for i in range(args.steps):
             flush.zero_()  # evict L2 between timed steps (outside the timed window)
             starts[i].record(stream)
