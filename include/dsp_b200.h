@@ -176,6 +176,13 @@ int64_t dsp_block_param_count(const dsp_block_t* blk);
 int dsp_block_bind(dsp_block_t* blk, void* workspace, float* params, float* grads, void* stream);
 /* Re-pack the storage-dtype weight shadow from the fp32 params (after an external write). */
 int dsp_block_pack(dsp_block_t* blk, void* stream);
+/* Make `twin` (planned from the same layer program and batch, bound to its own workspace and
+ * to the primary's params) a FORWARD TWIN of `primary`: its convs read the primary's packed
+ * weight shadow, and dsp_block_pack on it becomes a no-op.  A block's fresh forward
+ * (pipeline.py:564) then runs on the twin, on its own stream, concurrently with the primary's
+ * recompute + backward (pipeline.py:566-582); the caller joins it before the update.  Call
+ * again after re-binding the primary. */
+int dsp_block_share_weights(dsp_block_t* twin, const dsp_block_t* primary);
 
 /* block_forward: x (padded input, storage dtype) -> y (padded output).
  * record=1 keeps the tape for dsp_block_backward (recompute pass); y may be

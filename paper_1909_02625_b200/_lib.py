@@ -129,6 +129,7 @@ _SIGNATURES = {
     "dsp_block_param_count": (C.c_int64, [_P]),
     "dsp_block_bind": (C.c_int, [_P, _P, _P, _P, _P]),
     "dsp_block_pack": (C.c_int, [_P, _P]),
+    "dsp_block_share_weights": (C.c_int, [_P, _P]),
     "dsp_block_forward": (C.c_int, [_P, _P, _P, C.c_int, _P]),
     "dsp_block_loss": (C.c_int, [_P, _P, _P, _P]),
     "dsp_block_backward": (C.c_int, [_P, _P, _P, _P]),

@@ -20,6 +20,7 @@
 #include "abi_internal.h"
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 namespace dsp {
@@ -78,6 +79,10 @@ struct dsp_block {
   float* grads = nullptr;
   bool tape_valid = false;
   const void* rec_x = nullptr;
+  // forward twin (dsp_block_share_weights): reads the primary block's packed weight shadow
+  // instead of its own, so a fresh forward runs on its own workspace beside the primary's
+  // recompute + backward
+  const uint8_t* wsrc = nullptr;
   // side stream for the weight gradients of residual units: WGRAD (+ split-K reduce) of a conv
   // runs beside the DGRAD that reads the same dY, forked / joined with events (graph-capturable)
   cudaStream_t side = nullptr;
@@ -140,6 +145,9 @@ inline P* at(dsp_block* b, size_t off) {
   return reinterpret_cast<P*>(b->ws + off);
 }
 
+// packed storage-dtype weights this block's convs read (its own, or a forward twin's primary's)
+inline const uint8_t* packed_base(const dsp_block* b) { return b->wsrc ? b->wsrc : b->ws + b->packed; }
+
 // ------------------------------------------------------------------ kernels per conv
 int conv_fprop(dsp_block* b, const ConvP& c, const void* x, cudaStream_t st) {
   dsp_igemm_args_t a{};
@@ -148,7 +156,7 @@ int conv_fprop(dsp_block* b, const ConvP& c, const void* x, cudaStream_t st) {
   a.N = c.g.K;
   a.Kd = c.g.R * c.g.S * c.g.C;
   a.A = x;
-  a.B = b->ws + b->packed + (size_t)c.wpack * b->esz;
+  a.B = packed_base(b) + (size_t)c.wpack * b->esz;
   a.D = b->ws + c.y;
   a.ldd = c.g.K;
   a.stats = at<float>(b, b->fpart);
@@ -224,12 +232,12 @@ int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const voi
   a.N = c.g.C;
   a.Kd = c.g.R * c.g.S * c.g.K;
   a.A = dy;
-  a.B = b->ws + b->packed + (size_t)c.wpack * b->esz;
+  a.B = packed_base(b) + (size_t)c.wpack * b->esz;
   a.D = dx;
   a.ldd = c.g.C;
   a.residual = residual;
   a.n_valid = c.ci_real;
-  if (c.wpack_t >= 0) a.B_t = b->ws + b->packed + (size_t)c.wpack_t * b->esz;
+  if (c.wpack_t >= 0) a.B_t = packed_base(b) + (size_t)c.wpack_t * b->esz;
   if (fuse != nullptr) {
     a.stats = at<float>(b, b->fpart);
     a.sem = at<int32_t>(b, b->sem);
@@ -280,7 +288,7 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
       a.N = l.out_cp;
       a.Kd = l.in_cp;
       a.A = x;
-      a.B = b->ws + b->packed + (size_t)l.dense.wpack * b->esz;
+      a.B = packed_base(b) + (size_t)l.dense.wpack * b->esz;
       a.D = out;
       a.ldd = l.out_cp;
       a.out_f32 = l.logits ? 1 : 0;
@@ -634,6 +642,7 @@ extern "C" int64_t dsp_block_param_count(const dsp_block_t* b) { return b ? b->p
 
 extern "C" int dsp_block_pack(dsp_block_t* b, void* stream) {
   if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_pack: block not bound");
+  if (b->wsrc) return DSP_OK;  // forward twin: the primary's pack is the one read
   DSP_CUDA(pack_weights(b->dtype, b->params, b->ws + b->packed, at<PackEntry>(b, b->ptable), (int)b->packs.size(),
                         b->pack_max, (cudaStream_t)stream));
   return DSP_OK;
@@ -779,5 +788,21 @@ extern "C" int dsp_block_update_adam(dsp_block_t* b, void* state, double lr, dou
   }
   if (grad_sq_out) DSP_CUDA(sum_partials_f32(part, update_grid(n), grad_sq_out, st));
   if (apply) DSP_TRY(dsp_block_pack(b, stream));
+  return DSP_OK;
+}
+
+extern "C" int dsp_block_share_weights(dsp_block_t* twin, const dsp_block_t* primary) {
+  if (!twin || !primary || !twin->ws || !primary->ws)
+    return set_error(DSP_E_STATE, "dsp_block_share_weights: both blocks must be bound");
+  if (twin == primary) return set_error(DSP_E_INVALID, "dsp_block_share_weights: a block cannot twin itself");
+  bool same = twin->B == primary->B && twin->dtype == primary->dtype && twin->param_count == primary->param_count &&
+              twin->packs.size() == primary->packs.size() && twin->params == primary->params;
+  for (size_t i = 0; same && i < twin->packs.size(); ++i)
+    same = memcmp(&twin->packs[i], &primary->packs[i], sizeof(PackEntry)) == 0;
+  if (!same)
+    return set_error(DSP_E_INVALID,
+                     "dsp_block_share_weights: twin must be planned from the same program and bound to the "
+                     "primary's params");
+  twin->wsrc = primary->ws + primary->packed;
   return DSP_OK;
 }

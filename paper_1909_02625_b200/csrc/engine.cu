@@ -21,8 +21,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <numeric>
 #include <vector>
 
 namespace {
@@ -45,6 +47,12 @@ struct dsp_engine {
   int horizon = 0;
   std::vector<dsp_layer_desc_t> layers;
   dsp_block_t* blk[DSP_MAX_BLOCKS] = {};
+  // forward twins (k < K-1): the fresh forward runs on twin[k] / fstream[k], beside the
+  // recompute + backward of blk[k] on the block stream, joined before the update
+  dsp_block_t* twin[DSP_MAX_BLOCKS] = {};
+  void* tws[DSP_MAX_BLOCKS] = {};
+  cudaStream_t fstream[DSP_MAX_BLOCKS] = {};
+  cudaEvent_t fev_fork[DSP_MAX_BLOCKS] = {}, fev_join[DSP_MAX_BLOCKS] = {};
   int64_t nparam[DSP_MAX_BLOCKS] = {};
   int64_t in_elems[DSP_MAX_BLOCKS] = {}, out_elems[DSP_MAX_BLOCKS] = {};
   void* ws[DSP_MAX_BLOCKS] = {};
@@ -158,9 +166,18 @@ int issue_block(dsp_engine* e, int k, int64_t n, cudaStream_t st) {
   const int ph = (int)(n % e->R);
   float* loss_slot = e->slots + ((size_t)ph * K + k) * 2;
   if (k < K - 1) {
-    DSP_TRY(dsp_block_forward(e->blk[k], fresh_in(e, k, n), e->ring_out[k][ph], 0, st));
+    if (e->twin[k]) {  // fresh forward on the twin's stream, overlapping recompute + backward
+      ENG_CUDA(cudaEventRecord(e->fev_fork[k], st));
+      ENG_CUDA(cudaStreamWaitEvent(e->fstream[k], e->fev_fork[k], 0));
+      DSP_TRY(dsp_block_forward(e->twin[k], fresh_in(e, k, n), e->ring_out[k][ph], 0, e->fstream[k]));
+      ENG_CUDA(cudaEventRecord(e->fev_join[k], e->fstream[k]));
+    } else {
+      DSP_TRY(dsp_block_forward(e->blk[k], fresh_in(e, k, n), e->ring_out[k][ph], 0, st));
+    }
     DSP_TRY(dsp_block_forward(e->blk[k], stale_in(e, k, n), nullptr, 1, st));
     DSP_TRY(dsp_block_backward(e->blk[k], upstream(e, k, n), k > 0 ? e->ring_gin[k][ph] : nullptr, st));
+    // the update rewrites the packed weights the fresh forward reads
+    if (e->twin[k]) ENG_CUDA(cudaStreamWaitEvent(st, e->fev_join[k], 0));
   } else {
     DSP_TRY(dsp_block_forward(e->blk[k], stale_in(e, k, n), nullptr, 1, st));
     DSP_TRY(dsp_block_loss(e->blk[k], stale_labels(e, n), loss_slot, st));
@@ -283,6 +300,21 @@ extern "C" int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out) {
     if (cudaEventCreateWithFlags(&e->join_ev[k], cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
     int rc = dsp_block_bind(e->blk[k], e->ws[k], e->params[k], e->grads[k], e->stream);
     if (rc != DSP_OK) return fail(rc);
+    // forward twins when the device holds few blocks (engine_b200.use_twins; DSP_B200_TWIN=0/1)
+    static const char* tw_env = getenv("DSP_B200_TWIN");
+    const bool twins = tw_env ? tw_env[0] == '1' : K <= 4;
+    if (k < K - 1 && twins) {
+      const int off_k = (int)(std::accumulate(cfg->n_layers, cfg->n_layers + k, 0));
+      if ((rc = dsp_block_create(e->layers.data() + off_k, cfg->n_layers[k], e->B, cfg->dtype, 0, &e->twin[k])) !=
+          DSP_OK)
+        return fail(rc);
+      if ((rc = dmalloc(&e->tws[k], dsp_block_workspace_bytes(e->twin[k]))) != DSP_OK) return fail(rc);
+      if ((rc = dsp_block_bind(e->twin[k], e->tws[k], e->params[k], e->grads[k], e->stream)) != DSP_OK) return fail(rc);
+      if ((rc = dsp_block_share_weights(e->twin[k], e->blk[k])) != DSP_OK) return fail(rc);
+      if (cudaStreamCreateWithFlags(&e->fstream[k], cudaStreamNonBlocking) != cudaSuccess) return fail(DSP_E_CUDA);
+      if (cudaEventCreateWithFlags(&e->fev_fork[k], cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
+      if (cudaEventCreateWithFlags(&e->fev_join[k], cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
+    }
   }
   if (cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
   const int R = e->R;
@@ -468,6 +500,11 @@ extern "C" void dsp_destroy(dsp_engine_t* e) {
   for (int k = 0; k < DSP_MAX_BLOCKS; ++k) {
     if (e->blk[k]) dsp_block_destroy(e->blk[k]);
     cudaFree(e->ws[k]);
+    if (e->twin[k]) dsp_block_destroy(e->twin[k]);
+    if (e->tws[k]) cudaFree(e->tws[k]);
+    if (e->fstream[k]) cudaStreamDestroy(e->fstream[k]);
+    if (e->fev_fork[k]) cudaEventDestroy(e->fev_fork[k]);
+    if (e->fev_join[k]) cudaEventDestroy(e->fev_join[k]);
     cudaFree(e->params[k]);
     cudaFree(e->grads[k]);
     cudaFree(e->ys[k]);

@@ -56,6 +56,18 @@ def block_priorities(model, local) -> dict:
     return {k: -min(3, len(order) - 1 - order.index(k)) if len(order) > 1 else 0 for k in local}
 
 
+def use_twins(n_local: int) -> bool:
+    """Forward twins when a rank holds few blocks. Measured on B200 (tools/block_step_latency.py,
+    profiles/r01_twins.md): a GPU owning one block steps 11-22% faster on the CIFAR ResNets
+    (ResNet-56 block 0 905 -> 775 us), while a GPU already running 4 blocks concurrently gains
+    nothing (ResNet-56 K=4 +0.3%) and one running 8 loses 3% (ResNet-110 K=8).
+    DSP_B200_TWIN=0/1 overrides."""
+    env = os.environ.get("DSP_B200_TWIN")
+    if env is not None:
+        return env == "1"
+    return n_local <= 4
+
+
 class B200Runtime:
     LOG_CHUNK = 4096
 
@@ -116,6 +128,14 @@ class B200Runtime:
         prio = block_priorities(model, self.local)
         self._block_streams = {k: torch.cuda.Stream(self.device, priority=prio[k]) for k in self.local}
         self.eager_concurrent = True  # eager steps: local blocks on their own streams too
+        # forward twins: block k's fresh forward (pipeline.py:564) runs on a twin with its own
+        # workspace and stream, overlapping the recompute + backward; joined before the update
+        self.twins, self._fwd_streams, self._fwd_pending = {}, {}, {}
+        if use_twins(len(self.local)):
+            for k in self.local:
+                if k < self.K - 1:
+                    self.twins[k] = self.dev[k].make_twin()
+                    self._fwd_streams[k] = torch.cuda.Stream(self.device, priority=prio[k])
         self.replayed_kernels = 0  # library kernels executed through graph replays
 
     def kernels_executed(self) -> int:
@@ -273,7 +293,14 @@ class B200Runtime:
     def forward(self, k: int, x, n: int = 0):
         y = self.ring_out[k][n % self.R]
         if self.mode != "replay":
-            self.dev[k].forward(x, y, record=False, stream=self._s(k))
+            tw = self.twins.get(k)
+            if tw is None:
+                self.dev[k].forward(x, y, record=False, stream=self._s(k))
+            else:  # fork onto the twin's stream; joined in update() before the weights change
+                fs = self._fwd_streams[k]
+                fs.wait_stream(self._s(k))
+                tw.forward(x, y, record=False, stream=fs)
+                self._fwd_pending[k] = fs
         return y
 
     def forward_record(self, k: int, x, n: int = 0, y=None) -> None:
@@ -318,6 +345,9 @@ class B200Runtime:
         return gin
 
     def update(self, k: int, lr: float, slr: float, apply: bool, n: int = 0):
+        fs = self._fwd_pending.pop(k, None)
+        if fs is not None:
+            self._s(k).wait_stream(fs)
         if self.mode != "replay" and self.rule == "adam":
             st = self.adam
             self.dev[k].update_adam(self.ys[k], lr, st.beta1, st.beta2, st.eps, self.wd, apply,

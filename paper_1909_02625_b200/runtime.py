@@ -71,6 +71,26 @@ class DeviceBlock:
             self.grads = torch.zeros_like(self.params)
         L.check(self.lib.dsp_block_bind(h, ptr(self.ws), ptr(self.params), ptr(self.grads), stream_ptr(self.stream)))
 
+    def make_twin(self) -> "DeviceBlock":
+        """A forward twin (dsp_block_share_weights): same program, own workspace, this block's
+        params and packed weights -- runs the fresh forward beside this block's recompute."""
+        torch = torch_mod()
+        tw = DeviceBlock.__new__(DeviceBlock)
+        tw.device, tw.lib, tw.block, tw.batch, tw.is_last = self.device, self.lib, self.block, self.batch, False
+        tw.stream = self.stream
+        descs = self.block.layer_descs()
+        h = C.c_void_p()
+        L.check(self.lib.dsp_block_create(descs, len(descs), self.batch, L.DSP_DTYPE_BF16, 0, C.byref(h)))
+        tw.h = h
+        tw.ws_bytes = int(self.lib.dsp_block_workspace_bytes(h))
+        tw.in_elems, tw.out_elems = self.in_elems, self.out_elems
+        with torch.cuda.stream(self.stream):
+            tw.ws = torch.empty(max(tw.ws_bytes, 1), dtype=torch.uint8, device=self.device)
+        tw.params, tw.grads = self.params, self.grads
+        L.check(self.lib.dsp_block_bind(h, ptr(tw.ws), ptr(tw.params), ptr(tw.grads), stream_ptr(self.stream)))
+        L.check(self.lib.dsp_block_share_weights(h, self.h))
+        return tw
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:

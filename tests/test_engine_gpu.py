@@ -205,3 +205,22 @@ def test_resnet_k3_adam_extension():
     _check(eng, pm, refs, (4, 2, 0), scale=3.0)
     for k in range(3):  # applied-update counter = steps whose stale tag is >= 0
         assert eng.rt.opt_state(k).n == sum(1 for r in eng.log.records if r.block == k and r.batch_index >= 0)
+
+
+def test_forward_twin_is_bitwise_neutral(monkeypatch):
+    """The fresh forward on a forward twin (own workspace + stream, dsp_block_share_weights)
+    gives the same log and parameters, bit for bit, as the fresh forward on the block itself."""
+    layers = small_resnet(in_shape=(3, 8, 8))
+    cfg = P.default_queue_config(3)
+    pool = R.synthetic_batches(6, 8, (3, 8, 8), 10, seed=1)
+    runs = []
+    for env in ("0", "1"):
+        monkeypatch.setenv("DSP_B200_TWIN", env)
+        pm, _ = twin_models(layers, [2, 4], seed=3)
+        eng = P.TrainEngine(pm, cfg, R.cycle(pool), P.LrSchedule(0.05, ((8, 0.5),)), rule="sum", beta=0.9)
+        assert bool(eng.rt.twins) == (env == "1")
+        eng.run(16)
+        runs.append((eng.log.checksum(), [b.params.copy() for b in pm.blocks]))
+    assert runs[0][0] == runs[1][0]
+    for a, b in zip(runs[0][1], runs[1][1]):
+        assert np.array_equal(a, b)
