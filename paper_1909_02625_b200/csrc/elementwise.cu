@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Non-GEMM kernels of the DSP block step: BatchNorm statistics / apply /
 // backward, dense activations, pooling, softmax cross-entropy, split-K
 // reduction, weight-shadow packing, the per-block optimizer update, and the
@@ -111,7 +112,7 @@ __global__ void bn_finalize_k(const float* __restrict__ part, int tiles, int Cp,
 }
 
 template <typename T, int UNR>
-__global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
+__device__ __forceinline__ void bn_apply_k_body(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
                            int64_t nvec, int Cp, int relu) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
@@ -182,6 +183,20 @@ __global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ st
       st16(out + e0, a);
     }
   }
+}
+
+// default form (compiler-chosen registers) and launch-bounded variants (A/B knob)
+template <typename T, int UNR>
+__global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
+                           const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
+                           int64_t nvec, int Cp, int relu) {
+  bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu);
+}
+template <typename T, int UNR, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bn_apply_k_lb(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
+                           const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
+                           int64_t nvec, int Cp, int relu) {
+  bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu);
 }
 
 // ------------------------------------------------------------------ BatchNorm backward
@@ -341,7 +356,7 @@ __global__ void bn_bwd_finalize_k(const float* __restrict__ part, int chunks, in
 }
 
 template <typename T, int UNR>
-__global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+__device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
@@ -415,6 +430,24 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
       }
     }
   }
+}
+
+// default form (compiler-chosen registers) and launch-bounded variants (A/B knob)
+template <typename T, int UNR>
+__global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+                               const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
+                               const T* __restrict__ yb, const float* __restrict__ statb,
+                               const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
+                               int64_t nvec, int Cp) {
+  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp);
+}
+template <typename T, int UNR, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) bn_bwd_apply_k_lb(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+                               const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
+                               const T* __restrict__ yb, const float* __restrict__ statb,
+                               const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
+                               int64_t nvec, int Cp) {
+  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp);
 }
 
 // Tensors within one wave (CIFAR shapes, one vector per thread): the plain form -- per-vector
@@ -996,9 +1029,22 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
-    if (nvec > kWave)
-      launch_k(bn_apply_k<T, 4>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2,
-               (T*)out, nvec, Cp, relu);
+    // variant (UNR x min CTAs per SM) via DSP_B200_BNA = 10*UNR + MINB (A/B knob). ncu on
+    // ResNet-50: the unbounded UNR-4 form took 117 registers -> 2 CTAs/SM, 24% warps active,
+    // 44-59% of DRAM peak; one vector per thread per pass at 4 CTAs/SM measured +1.6%
+    // (ResNet-50) / +5.3% (ResNet-164) samples/s
+    static const int var = getenv("DSP_B200_BNA") ? atoi(getenv("DSP_B200_BNA")) : 13;
+    auto go = [&](auto kern) {
+      launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
+               nvec, Cp, relu);
+    };
+    if (nvec > kWave) {
+      if (var == 23) go(bn_apply_k_lb<T, 2, 3>);
+      else if (var == 24) go(bn_apply_k_lb<T, 2, 4>);
+      else if (var == 43) go(bn_apply_k_lb<T, 4, 3>);
+      else if (var == 13) go(bn_apply_k_lb<T, 1, 4>);  // default: 62 regs, 4 CTAs/SM, no spill
+      else go(bn_apply_k<T, 4>);  // 41: compiler-chosen 117 regs, 2 CTAs/SM
+    }
     else
       launch_k(bn_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2,
                stat2, (T*)out, nvec, Cp, relu);
@@ -1060,9 +1106,21 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
-    if (nvec > kWave)
-      launch_k(bn_bwd_apply_k<T, 2>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat,
-               coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
+    // variant (UNR x min CTAs per SM) via DSP_B200_BNB = 10*UNR + MINB (A/B knob): the
+    // unbounded UNR-2 form took 128 registers (2 CTAs/SM); UNR 1 at 3 CTAs/SM measured +0.9%
+    // (ResNet-50) / +2.6% (ResNet-164)
+    static const int var = getenv("DSP_B200_BNB") ? atoi(getenv("DSP_B200_BNB")) : 13;
+    auto go = [&](auto kern) {
+      launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef, (T*)dy,
+               (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
+    };
+    if (nvec > kWave) {
+      if (var == 23) go(bn_bwd_apply_k_lb<T, 2, 3>);
+      else if (var == 24) go(bn_bwd_apply_k_lb<T, 2, 4>);
+      else if (var == 13) go(bn_bwd_apply_k_lb<T, 1, 3>);  // default: 80 regs, 3 CTAs/SM, no spill
+      else if (var == 14) go(bn_bwd_apply_k_lb<T, 1, 4>);
+      else go(bn_bwd_apply_k<T, 2>);
+    }
     else
       launch_k(bn_bwd_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y,
                stat, coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
