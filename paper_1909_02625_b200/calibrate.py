@@ -11,7 +11,11 @@ module measures the costs on the device instead of assuming them:
 * ``simulate_dsp`` / ``simulate_bp``: the reference's event recurrences (restated) driven by
   those costs, optionally with straggler multipliers, giving makespan and steady interval;
 * ``measured_cuts``: FLOP-free cut selection -- every layer timed as its own block, then the
-  contiguous partition minimising the predicted steady interval (DP over cut points).
+  contiguous partition minimising the predicted steady interval (DP over cut points);
+* ``block_step_cost`` / ``twin_balanced_cuts``: the per-GPU step of a block that owns its GPU
+  (fresh forward on a forward twin beside recompute + backward, then the update) timed whole,
+  and a local search over the cut points that minimises the slowest block's step -- the K-GPU
+  DSP step interval (simulate.py:160-217) once the blocks run on their own GPUs.
 """
 
 from __future__ import annotations
@@ -156,3 +160,87 @@ def measured_cuts(layers, k: int, batch: int, reps: int = 5) -> list:
             cuts.append(i)
         j = i
     return sorted(cuts)
+
+
+def block_step_cost(layers, lo: int, hi: int, batch: int, last: bool, reps: int = 10, device=None,
+                    twin: bool = True) -> float:
+    """Seconds per DSP step of the block made of layers[lo:hi] on a GPU of its own: fresh forward
+    (on a forward twin when `twin`, beside the recompute + backward), recompute forward,
+    [loss,] backward, update -- CUDA-graph replay of the real block kernels."""
+    torch = torch_mod()
+    dev = torch.device("cuda") if device is None else device
+    sub = layers[lo:hi]
+    model = B.build_model(sub, [])
+    B.init_params(model, 0)
+    blk = model.blocks[0]
+    db = DeviceBlock(blk, batch, is_last=last, device=dev)
+    tw = db.make_twin() if (twin and not last) else None
+    x = torch.randn(db.in_elems, device=dev).bfloat16()
+    x2 = torch.randn(db.in_elems, device=dev).bfloat16()
+    up = None if last else torch.randn(db.out_elems, device=dev).bfloat16() * 1e-3
+    y = None if last else torch.empty(db.out_elems, dtype=torch.bfloat16, device=dev)
+    gin = torch.empty(db.in_elems, dtype=torch.bfloat16, device=dev) if lo > 0 else None
+    labels = torch.zeros(batch, dtype=torch.int64, device=dev)
+    loss = torch.zeros(1, device=dev)
+    gsq = torch.zeros(1, device=dev)
+    ys = db.params.clone()
+    fs = torch.cuda.Stream(dev)
+
+    def step(st):
+        if not last:
+            if tw is not None:
+                fs.wait_stream(st)
+                tw.forward(x, y, record=False, stream=fs)
+            else:
+                db.forward(x, y, record=False, stream=st)
+        db.forward(x2, None, record=True, stream=st)
+        if last:
+            db.loss(labels, loss, stream=st)
+        db.backward(up, gin, stream=st)
+        if tw is not None:
+            st.wait_stream(fs)
+        db.update(1, ys, 1e-9, 1e-9, 0.9, 0.0, True, gsq, stream=st)
+
+    return _graph_time(torch, step, reps)
+
+
+def twin_balanced_cuts(layers, k: int, batch: int, start=None, reps: int = 10, max_moves: int = 16,
+                       device=None, log=None) -> tuple:
+    """Local search over the cut points minimising max_k(block_step_cost): move one layer out
+    of the slowest block into a neighbour while that lowers the maximum. Returns (cuts, costs)."""
+    cuts = list(start if start is not None else B.flop_balanced_boundaries(layers, k))
+    L = len(layers)
+    cache = {}
+
+    def cost(lo, hi):
+        key = (lo, hi, hi == L)
+        if key not in cache:
+            cache[key] = block_step_cost(layers, lo, hi, batch, hi == L, reps=reps, device=device)
+        return cache[key]
+
+    def costs_of(c):
+        b = [0] + list(c) + [L]
+        return [cost(b[i], b[i + 1]) for i in range(k)]
+
+    cur = costs_of(cuts)
+    for _ in range(max_moves):
+        j = int(np.argmax(cur))
+        best = None
+        for d in ((j - 1, +1), (j, -1)):  # first layer of j to j-1 / last layer of j to j+1
+            ci, step = d
+            if ci < 0 or ci >= k - 1:
+                continue
+            cand = list(cuts)
+            cand[ci] += step
+            b = [0] + cand + [L]
+            if any(b[i + 1] <= b[i] for i in range(k)):
+                continue
+            cc = costs_of(cand)
+            if max(cc) < max(cur) and (best is None or max(cc) < max(best[1])):
+                best = (cand, cc)
+        if best is None:
+            break
+        cuts, cur = best
+        if log:
+            log(f"cuts {cuts}: max {max(cur) * 1e6:.0f} us")
+    return cuts, cur

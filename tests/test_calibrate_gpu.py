@@ -26,6 +26,17 @@ def test_measured_costs_drive_the_des():
     assert len(cuts) == 2 and 0 < cuts[0] < cuts[1] < len(layers)
 
 
+def test_twin_balanced_cuts_never_worse_than_start():
+    layers = P.resnet_cifar_layers(20, 10, width=8)
+    start = [1, 2]  # deliberately unbalanced: a 1-layer block 0
+    c0 = max(CAL.block_step_cost(layers, lo, hi, 16, hi == len(layers), reps=3)
+             for lo, hi in zip([0] + start, start + [len(layers)]))
+    cuts, costs = CAL.twin_balanced_cuts(layers, 3, 16, start=start, reps=3)
+    assert len(cuts) == 2 and 0 < cuts[0] < cuts[1] < len(layers)
+    assert len(costs) == 3 and all(c > 0 for c in costs)
+    assert max(costs) <= c0 * 1.05
+
+
 def test_device_straggler_changes_timing_not_values():
     torch = torch_mod()
     layers = small_resnet(in_shape=(3, 8, 8))
