@@ -7,6 +7,7 @@ dense bf16 figure in MEASURED_PEAKS.json (burst). Prints one JSON object per (sh
 summary line; `--json out.json` also writes them to a file.
 
     python tools/conv_tc.py [--batch 256] [--reps 20] [--json gpurun_out/conv_tc.json]
+    python tools/conv_tc.py --shapes cifar --batch 128      # ResNet-56 stage convs
 """
 
 from __future__ import annotations
@@ -36,6 +37,14 @@ R50 = [
     ("s4.1x1down", 7, 2048, 512, 1, 1),
 ]
 
+# ResNet-56 / ResNet-110 (BASELINE configs[1], [2]: CIFAR-shaped, batch 128) 3x3 stage convs;
+# c1.3x3 FPROP is bench.py's roofline kernel (stage-1 halo tiles + fused BN statistics)
+CIFAR = [
+    ("c1.3x3", 32, 16, 16, 3, 1),
+    ("c2.3x3", 16, 32, 32, 3, 1),
+    ("c3.3x3", 8, 64, 64, 3, 1),
+]
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -44,6 +53,7 @@ def main():
     ap.add_argument("--json", default="")
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cudnn", action="store_true")
+    ap.add_argument("--shapes", default="r50", choices=["r50", "cifar"])
     args = ap.parse_args()
 
     import torch
@@ -63,7 +73,7 @@ def main():
     st = torch.cuda.current_stream()
     torch.backends.cudnn.benchmark = True
     rows = []
-    for name, H, Cc, K, R, stride in R50:
+    for name, H, Cc, K, R, stride in (CIFAR if args.shapes == "cifar" else R50):
         if args.only and args.only not in name:
             continue
         nimg = args.batch
@@ -139,7 +149,10 @@ def main():
             sv = C.c_void_p(st.cuda_stream)
             t = timed(lambda: L.check(lib.dsp_igemm(mode, L.DSP_DTYPE_BF16, C.byref(a), sp, sv)))
             row = {"shape": name, "mode": mname, "M": a.M, "N": a.N, "Kd": a.Kd, "gflop": flops / 1e9,
-                   "us": t * 1e6, "tflops": flops / t / 1e12, "frac": flops / t / 1e12 / peak}
+                   "us": t * 1e6, "tflops": flops / t / 1e12, "frac": flops / t / 1e12 / peak,
+                   # bf16 operand + result bytes (X, W|dY, Y|dX|fp32 split-K partials): the HBM-bound view
+                   "gbs": (2 * (x.numel() + w.numel() + dy.numel()) + (4 * part.numel()
+                           if mode == L.DSP_IGEMM_WGRAD else 0)) / t / 1e9}
             if not args.no_cudnn:
                 tc = timed(cudnn[mname])
                 row["cudnn_us"] = tc * 1e6
@@ -147,7 +160,7 @@ def main():
             rows.append(row)
             print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in row.items()}), flush=True)
     tot = sum(r["gflop"] for r in rows)
-    summ = {"summary": "resnet50 convs", "batch": args.batch, "peak_tflops": peak,
+    summ = {"summary": ("cifar" if args.shapes == "cifar" else "resnet50") + " convs", "batch": args.batch, "peak_tflops": peak,
             "tflops_all": tot / sum(r["us"] for r in rows) * 1e3,
             "frac_all": tot / sum(r["us"] for r in rows) * 1e3 / peak}
     if not args.no_cudnn:
