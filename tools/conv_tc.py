@@ -54,6 +54,11 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--shapes", default="r50", choices=["r50", "cifar"])
+    ap.add_argument("--fprop-stats", default="finalize", choices=["finalize", "partials", "none"],
+                    help="FPROP epilogue: BN partials + fused finalize (the step's form), partials only, or none")
+    ap.add_argument("--fin-dbg", type=int, default=0,
+                    help="diagnostic: ticket debug bits (1 = skip the pre-ticket fence, 2 = skip the atomic); "
+                         "results are not valid with these set")
     args = ap.parse_args()
 
     import torch
@@ -110,6 +115,11 @@ def main():
                 a.stats, a.stat_out, a.gamma, a.beta, a.sem = (stats.data_ptr(), stat_out.data_ptr(),
                                                                gamma.data_ptr(), beta.data_ptr(), sem.data_ptr())
                 a.n_valid = K
+                a.out_f32 = args.fin_dbg << 8
+                if args.fprop_stats != "finalize":
+                    a.sem, a.stat_out = None, None
+                if args.fprop_stats == "none":
+                    a.stats = None
             elif mode == L.DSP_IGEMM_DGRAD:
                 a.M, a.N, a.Kd = nimg * H * H, Cc, R * R * K
                 a.A, a.B, a.D, a.ldd = dy.data_ptr(), w.data_ptr(), dx.data_ptr(), Cc
@@ -160,7 +170,8 @@ def main():
             rows.append(row)
             print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in row.items()}), flush=True)
     tot = sum(r["gflop"] for r in rows)
-    summ = {"summary": ("cifar" if args.shapes == "cifar" else "resnet50") + " convs", "batch": args.batch, "peak_tflops": peak,
+    summ = {"summary": ("cifar" if args.shapes == "cifar" else "resnet50") + " convs", "batch": args.batch,
+            "peak_tflops": peak, "fprop_stats": args.fprop_stats,
             "tflops_all": tot / sum(r["us"] for r in rows) * 1e3,
             "frac_all": tot / sum(r["us"] for r in rows) * 1e3 / peak}
     if not args.no_cudnn:
