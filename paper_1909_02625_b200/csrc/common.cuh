@@ -19,6 +19,12 @@ namespace dsp {
 
 typedef __nv_bfloat16 bf16;
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------- mbarrier
 // Last-CTA ticket for fused grid reductions. Every thread of the CTA calls it after
 // writing its partials; returns true (CTA-uniformly) in the CTA that arrives last, with
@@ -26,14 +32,21 @@ typedef __nv_bfloat16 bf16;
 // ld.global.cg). One thread fences at gpu scope (release before the ticket, acquire
 // after it), the bar.syncs extend the ordering to the rest of the CTA; a per-thread
 // __threadfence() (MEMBAR.SC.GPU in every warp) cost 5-7 us per launch here.
-__device__ __forceinline__ bool last_cta_ticket(int* sem, int total, int* flag_smem, int dbg = 0) {
+// Diagnostics only: dbg bits 1/2/4 skip the release fence / the atomic / the acquire fence
+// (results invalid); ts (trace builds) receives globaltimer stamps [0] after the release
+// fence, [1] after the atomic returned, [2] after the acquire fence (winner only).
+__device__ __forceinline__ bool last_cta_ticket(int* sem, int total, int* flag_smem, int dbg = 0,
+                                                int64_t* ts = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     int old = 0;
     if (!(dbg & 1)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (ts != nullptr) ts[0] = (int64_t)globaltimer_ns();
     if (!(dbg & 2)) asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(sem) : "memory");
+    if (ts != nullptr) ts[1] = (int64_t)globaltimer_ns();
     const int last = old == total - 1;
-    if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (last && !(dbg & 4)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (ts != nullptr && last) ts[2] = (int64_t)globaltimer_ns();
     *flag_smem = last;
   }
   __syncthreads();
@@ -95,11 +108,6 @@ __host__ __device__ constexpr int part_sums_window(int NTH, int NS) { return NS 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

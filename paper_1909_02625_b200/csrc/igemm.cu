@@ -1154,7 +1154,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
     // n-tile t finalizes its BN columns, so wide outputs finalize on nt CTAs in parallel
     const int t_own = (int)(blockIdx.x % nt);
     int* const sem_t = a.sem + t_own;
-    if (last_cta_ticket(sem_t, (int)gridDim.x / nt, &last_cta_s, (a.out_f32 >> 8) & 3)) {
+    if (last_cta_ticket(sem_t, (int)gridDim.x / nt, &last_cta_s, (a.out_f32 >> 8) & 7,
+                        ctat != nullptr ? a.trace + 192 + 8 * 1024 + 4 * blockIdx.x : nullptr)) {
       const int cbeg = t_own * BN, cend = min(N, cbeg + BN);
       if (kTrace && a.trace != nullptr && tid == 0) a.trace[186] = (int64_t)globaltimer_ns();
       const int nvalid = a.n_valid > 0 ? a.n_valid : N;

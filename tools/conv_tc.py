@@ -57,7 +57,7 @@ def main():
     ap.add_argument("--fprop-stats", default="finalize", choices=["finalize", "partials", "none"],
                     help="FPROP epilogue: BN partials + fused finalize (the step's form), partials only, or none")
     ap.add_argument("--fin-dbg", type=int, default=0,
-                    help="diagnostic: ticket debug bits (1 = skip the pre-ticket fence, 2 = skip the atomic); "
+                    help="diagnostic: ticket debug bits (1 = skip the pre-ticket fence, 2 = skip the atomic, 4 = skip the winner's acquire fence); "
                          "results are not valid with these set")
     args = ap.parse_args()
 

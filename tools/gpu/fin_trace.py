@@ -3,7 +3,8 @@
 Needs a library built with -DIG_TRACE_BUILD (tools/gpu/fin_trace.sh builds one under /tmp and
 puts it first on sys.path). Per CTA: ctat[1] start, ctat[2] epilogue done (ticket taken next),
 ctat[4] finalize done, ctat[3] TMEM dealloc (end); trace[186..188]: the finalizing CTA's ticket
-won / first window loaded / finalize written. Prints one JSON line per shape.
+won / first window loaded / finalize written; trace[192 + 8192 + 4b ..]: CTA b's ticket internals
+(release fence done, atomic returned, acquire fence done). Prints one JSON line per shape.
 """
 
 import ctypes as C
@@ -31,7 +32,7 @@ def main():
         stat_out = torch.empty(4 * K, device="cuda")
         gamma, beta = torch.ones(K, device="cuda"), torch.zeros(K, device="cuda")
         sem = torch.zeros(64, dtype=torch.int32, device="cuda")
-        trace = torch.zeros(192 + 8 * 1024, dtype=torch.int64, device="cuda")
+        trace = torch.zeros(192 + 12 * 1024, dtype=torch.int64, device="cuda")
         a = L.IgemmArgs()
         a.geom = g
         a.M, a.N, a.Kd = nimg * H * H, K, 9 * Cc
@@ -49,13 +50,19 @@ def main():
             t = trace.cpu().tolist()
             ct = [t[192 + 8 * b: 200 + 8 * b] for b in range(1024) if t[192 + 8 * b + 1] != 0]
             t0 = min(c[1] for c in ct)
+            tk = [t[192 + 8 * 1024 + 4 * b: 196 + 8 * 1024 + 4 * b] for b in range(1024) if t[192 + 8 * b + 1] != 0]
             r = {"ctas": len(ct), "last_start_us": (max(c[1] for c in ct) - t0) / 1e3,
                  "work_done_max_us": (max(c[2] for c in ct) - t0) / 1e3,
                  "work_done_median_us": (sorted(c[2] for c in ct)[len(ct) // 2] - t0) / 1e3,
                  "ticket_us": (t[186] - t0) / 1e3 if t[186] else None,
                  "first_window_us": (t[187] - t0) / 1e3 if t[187] else None,
                  "finalized_us": (t[188] - t0) / 1e3 if t[188] else None,
-                 "end_max_us": (max(c[3] for c in ct) - t0) / 1e3}
+                 "end_max_us": (max(c[3] for c in ct) - t0) / 1e3,
+                 # ticket internals (all CTAs): release fence done / atomic returned; winner's acquire fence
+                 "rel_fence_max_us": (max(k[0] for k in tk) - t0) / 1e3,
+                 "atom_ret_median_us": (sorted(k[1] for k in tk)[len(tk) // 2] - t0) / 1e3,
+                 "atom_ret_max_us": (max(k[1] for k in tk) - t0) / 1e3,
+                 "acq_fence_us": (max(k[2] for k in tk) - t0) / 1e3 if max(k[2] for k in tk) else None}
             res.append(r)
         print(json.dumps({"shape": name, "runs": res[2:]}), flush=True)
 
