@@ -78,6 +78,10 @@ struct MmaTraits<float> {
 #ifndef IG_REG_BLOCKS  // register budget as if this many CTAs shared an SM (headroom for other streams)
 #define IG_REG_BLOCKS 3
 #endif
+// rows in flight per thread in the fused finalize's partial-row load (trace experiments vary it)
+#ifndef IG_FIN_DEPTH
+#define IG_FIN_DEPTH 4
+#endif
 #ifndef IG_MAX_CTAS_PER_SM
 #define IG_MAX_CTAS_PER_SM 2
 #endif
@@ -1199,7 +1203,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
         const int win = part_sums_window(NTH, NS);
         for (int w0 = cbeg; w0 < cend; w0 += win) {
           const int cols = min(win, cend - w0);
-          part_sums_load<4, NTH>(a.stats, G, N, NS, w0, cols, BN, nt, fin4);
+          part_sums_load<IG_FIN_DEPTH, NTH>(a.stats, G, N, NS, w0, cols, BN, nt, fin4);
           __syncthreads();
           if (kTrace && a.trace != nullptr && tid == 0 && w0 == cbeg) a.trace[187] = (int64_t)globaltimer_ns();
           for (int cc = tid; cc < cols; cc += IG_THREADS) {
