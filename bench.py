@@ -1,16 +1,20 @@
 #!/usr/bin/env python
 """bench.py -- DSP training throughput on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1]): ResNet-56, synthetic CIFAR-10-shaped
-batches of 128, DSP with K blocks (K=4 for N<=4 GPUs, K=8 for N=8), queue
-config p_k=1, m_k=2(K-1-k), SUM momentum beta=0.9 s=1, lr 0.1,
-weight decay 5e-4, bf16 storage / fp32 accumulate on tcgen05 tensor cores.
-One "step" = one DSP iteration of every block (fresh forward, recompute,
-backward, update) = one batch through the pipeline.
+Headline workload (the largest BASELINE config that fits one GPU, configs[4]): ResNet-50,
+synthetic ImageNet-shaped 224x224x3 batches of 256, DSP with K=4 blocks (K=8 at 8 GPUs), queue
+config p_k=1, m_k=2(K-1-k), SUM momentum beta=0.9 s=1, lr 0.1, weight decay 5e-4,
+bf16 storage / fp32 accumulate on tcgen05 tensor cores.  One "step" = one DSP iteration of every
+block (fresh forward, recompute, backward, update) = one batch through the pipeline.  The same
+line carries the metric's other parts: the K=1 plain-BP baseline on the same model and batch
+(``k1_bp``), the per-conv tensor-pipe fraction of peak (``conv_tensor_pipe``) and configs[1]
+(ResNet-56, K=4, B=128) as a second workload (``resnet56``).
 
   python bench.py [--gpus N --steps K --warmup W]       # this repo's B200 engine
   python bench.py --impl reference [...]                  # the CPU oracle (reference algorithm)
+  python bench.py --model resnet56                        # configs[1] as the headline instead
 
+--gpus N without torchrun re-launches itself under torch.distributed.run (one rank per GPU).
 Prints ONE JSON line on rank 0. See DESIGN.md §5 for every field.
 """
 
@@ -70,11 +74,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=0, help="default: the config's batch (128 / 256)")
-    ap.add_argument("--model", default="resnet56", choices=sorted(MODELS))
+    ap.add_argument("--model", default="resnet50", choices=sorted(MODELS))
     ap.add_argument("--k", type=int, default=0, help="DSP blocks (default 4, or 8 when --gpus 8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cuts", default="", help="block boundaries (layer indices), default FLOP-balanced")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip k1_bp / conv_tensor_pipe / the resnet56 line")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     return ap.parse_args()
 
 
@@ -117,13 +123,18 @@ def workload(args):
     return layers, bounds, cfg
 
 
-def config_dict(args, K, world):
-    m = MODELS[args.model]
-    return {"workload": m["desc"].format(K=K, B=args.batch), "baseline_config": m["cfg"],
-            "model": args.model if args.model == "resnet50" else f"{args.model}-cifar", "global_batch": args.batch, "k_blocks": K,
-            "queues": "p_k=1, m_k=2(K-1-k)", "optimizer": opt_desc(args),
+def config_dict_for(model: str, K: int, batch: int, world: int, opt: str = "") -> dict:
+    m = MODELS[model]
+    return {"workload": m["desc"].format(K=K, B=batch), "baseline_config": m["cfg"],
+            "model": model if model == "resnet50" else f"{model}-cifar", "global_batch": batch, "k_blocks": K,
+            "queues": "p_k=1, m_k=2(K-1-k)",
+            "optimizer": opt or f"SUM momentum beta={SUM_OPT['beta']} s={SUM_OPT['s']}, lr {SUM_OPT['lr']}, wd 5e-4",
             "parallelism": f"dsp-pipeline k{K} over {world} gpu(s)",
             "l2": "L2 flushed (256 MiB write) between timed steps; step working set > L2"}
+
+
+def config_dict(args, K, world):
+    return config_dict_for(args.model, K, args.batch, world, opt_desc(args))
 
 
 # ------------------------------------------------------------------ clocks
@@ -297,7 +308,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": 1000.0 * dt / steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, K, 1),
+            "config": {**config_dict(args, K, 1), "global_batch": sub, "workload_global_batch": args.batch,
+                       "sample": f"each timed step runs the DSP step on a {sub}-sample sub-batch of the workload's "
+                                 f"{args.batch}; samples/s counts the {sub} samples"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"oracle/dsp_ref.py float64 DSP step (reference algorithm, CPU restatement), "
                                        f"ResNet-{DEPTH} K={K}, {steps} timed steps of a {sub}-sample sub-batch "
@@ -308,11 +321,12 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ B200 arm
-def ncu_traffic():
+def ncu_traffic(model: str = "resnet56"):
     """DRAM bytes (read + write) per launch of the roofline kernel from the committed
-    ncu --set full capture (profiles/ncu_roofline.json), or None."""
+    ncu --set full capture (profiles/ncu_roofline[_resnet50].json), or None."""
+    name = "ncu_roofline_resnet50.json" if model == "resnet50" else "ncu_roofline.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_roofline.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             d = json.load(f)
         return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
     except Exception:
@@ -384,7 +398,8 @@ def kernel_roofline(torch, peaks, batch, live_us, spec=None):
         peak = peaks.get(peak_key, peaks.get("bf16_tflops", 2250.0))
         achieved = flops / t / 1e12
         return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": spec["kernel"], "algorithmic_flops_per_launch": flops,
+                "traffic": ncu_traffic("resnet50"), "algorithmic_bytes_per_launch": algo, "kernel": spec["kernel"],
+                "algorithmic_flops_per_launch": flops,
                 "launch_us": t * 1e6, "timing": timing, "isolated_launch_us": t_iso * 1e6,
                 "isolated_achieved": flops / t_iso / 1e12,
                 "isolated_frac": flops / t_iso / 1e12 / peaks.get("bf16_tflops", 2250.0),
@@ -401,92 +416,91 @@ def kernel_roofline(torch, peaks, batch, live_us, spec=None):
             "peak_source": f"MEASURED_PEAKS.json {peak_key}" if peak_key in peaks else "fallback 6650 GB/s"}
 
 
-def run_b200(args):
+def workload_of(model: str, K: int, cuts: str = ""):
+    """(layers, boundaries, queue config) of a BASELINE model at K blocks (FLOP-balanced cuts)."""
+    import paper_1909_02625_b200 as P
+
+    m = MODELS[model]
+    if model == "resnet50":
+        layers = P.resnet50_layers(m["classes"], m["in_shape"])
+    elif model == "resnet164":
+        layers = P.resnet_cifar_bottleneck_layers(m["depth"], m["classes"])
+    else:
+        layers = P.resnet_cifar_layers(m["depth"], m["classes"])
+    bounds = [int(v) for v in cuts.split(",")] if cuts else (P.flop_balanced_boundaries(layers, K) if K > 1 else [])
+    return layers, bounds, P.default_queue_config(K)
+
+
+def measure(model: str, K: int, batch: int, steps: int, warmup: int, dev, world: int, cuts: str = "",
+            probe=None, e2e: bool = True, clock: bool = False, precision: str = "bf16", opt=None):
+    """Device-timed DSP steps of one workload through TrainEngine(backend="b200") on a device-resident
+    synthetic pool (L2 flushed between steps, CUDA events on the engine stream, max over ranks), then
+    optionally the live roofline probe pass and the end-to-end pass with host buffers."""
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
     import paper_1909_02625_b200 as P
     from paper_1909_02625_b200 import _lib as L
-    from paper_1909_02625_b200.data import cycle, synthetic_batches, to_device_batches
+    from paper_1909_02625_b200.data import cycle, device_synthetic_batches, synthetic_batches
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
     lib = L.load()
-    K = blocks_for(args)
-    layers, bounds, cfg = workload(args)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-
-    npool = 16 if IN_SHAPE[1] <= 32 else 4  # ImageNet-shaped batches: 154 MB each on the host
-    host_pool = synthetic_batches(npool, args.batch, IN_SHAPE, CLASSES, seed=0)
-    model = P.build_model(layers, bounds)
-    P.init_params(model, 0)
+    m = MODELS[model]
+    in_shape, classes = m["in_shape"], m["classes"]
+    layers, bounds, cfg = workload_of(model, K, cuts)
+    o = opt or SUM_OPT
+    npool = 16 if in_shape[1] <= 32 else 4  # ImageNet-shaped batches: 154 MB each on the host
+    model_ = P.build_model(layers, bounds)
+    P.init_params(model_, 0)
     stream = torch.cuda.current_stream(dev)
     # device-resident pool generated on the GPU (csrc/synth.cu): bitwise the packed host pool
-    from paper_1909_02625_b200.data import device_synthetic_batches
-
-    o = opt_of(args)
-    dev_pool = device_synthetic_batches(npool, args.batch, IN_SHAPE, CLASSES, seed=0, device=dev, stream=stream)
-    eng = P.TrainEngine(model, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(o["lr"]), rule=o["rule"],
-                        beta=o["beta"], s=o["s"], weight_decay=5e-4, device=dev)
+    dev_pool = device_synthetic_batches(npool, batch, in_shape, classes, seed=0, device=dev, stream=stream,
+                                        precision=precision)
+    eng = P.TrainEngine(model_, cfg, cycle([(b, b.labels) for b in dev_pool]), P.LrSchedule(o["lr"]), rule=o["rule"],
+                        beta=o["beta"], s=o["s"], weight_decay=5e-4, device=dev, precision=precision)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # live timing of the roofline kernel inside the step (CUDA event pairs recorded around
-    # every stage-1 FPROP launch on its block stream; captured into each step graph)
-    import ctypes as C
-
-    probe_pairs = 64
-    probe_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * probe_pairs)]
-    for ev in probe_ev:
-        ev.record(stream)  # materialise the handles
-    torch.cuda.synchronize()
-    handles = (C.c_void_p * (2 * probe_pairs))(*[C.c_void_p(ev.cuda_event) for ev in probe_ev])
-    spec = roofline_spec(args.model, args.batch)
-
     # warm up through the zero-prefill horizon and one capture of every step-graph phase
-    warm = max(3, args.warmup, eng._graph_horizon() + getattr(eng.rt, "R", 0) + 1)
+    warm = max(3, warmup, eng._graph_horizon() + getattr(eng.rt, "R", 0) + 1)
     for _ in range(warm):
         eng.run(1)
     torch.cuda.synchronize()
     barrier()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     launches0 = eng.rt.kernels_executed()
-    with NvmlClockSampler(dev.index) as clk:
-        for i in range(args.steps):
+    with NvmlClockSampler(dev.index) if clock else _Null() as clk:
+        for i in range(steps):
             flush.zero_()  # evict L2 between timed steps (outside the timed window)
             starts[i].record(stream)
             eng.run(1)
             ends[i].record(stream)
         torch.cuda.synchronize()
     launches = eng.rt.kernels_executed() - launches0
+    out = {"warm": warm, "launches": int(launches), "clocks": clk.summary() if clock else None}
 
-    # ---- roofline kernel, live: the same steps again with event pairs around every stage-1
-    # FPROP launch on its block stream (re-captured into each phase graph). A separate pass so
+    # ---- roofline kernel, live: the same steps again with event pairs around every launch of the
+    # roofline conv on its block stream (re-captured into each phase graph). A separate pass so
     # the probe's event nodes never touch the timed steps above.
     live_us = []
-    if world == 1:
-        lib.dsp_probe_arm(L.DSP_IGEMM_FPROP | (spec["Kd"] << 8), spec["K"], spec["M"], handles, probe_pairs)
+    if probe is not None and world == 1:
+        probe_pairs = 64
+        probe_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * probe_pairs)]
+        for ev in probe_ev:
+            ev.record(stream)  # materialise the handles
+        torch.cuda.synchronize()
+        handles = (C.c_void_p * (2 * probe_pairs))(*[C.c_void_p(ev.cuda_event) for ev in probe_ev])
+        lib.dsp_probe_arm(L.DSP_IGEMM_FPROP | (probe["Kd"] << 8), probe["K"], probe["M"], handles, probe_pairs)
         for g in eng.rt.graphs.values():
             lib.dsp_graph_destroy(g[3])
         eng.rt.graphs.clear()
         probed = 0
-        for i in range(getattr(eng.rt, "R", 0) + 1 + args.steps):
+        for i in range(getattr(eng.rt, "R", 0) + 1 + steps):
             flush.zero_()
             lib.dsp_probe_reset()
             eng.run(1)
@@ -496,37 +510,42 @@ def run_b200(args):
                 live_us += [probe_ev[2 * j].elapsed_time(probe_ev[2 * j + 1]) * 1000.0 for j in range(probed)]
         lib.dsp_probe_arm(0, 0, 0, None, 0)
         torch.cuda.synchronize()
+    out["live_us"] = live_us
     barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(step_ms))
-    t = torch.tensor([total_ms], device=dev)
+    step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+    t = torch.tensor([float(sum(step_ms))], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = args.batch * args.steps / (total_ms / 1000.0)
-    loss_ok = True
-    log = eng.log
+    out["ms_per_step"] = total_ms / steps
+    out["step_ms_median"] = statistics.median(step_ms)
+    out["value"] = batch * steps / (total_ms / 1000.0)
+    out["loss_finite"] = True
+    log = eng.log  # raises NonFiniteError if a step went non-finite (tensor.py:34-37)
     if (K - 1) in eng.local:
-        losses = [lv for _, lv in log.losses()]
-        loss_ok = all(np.isfinite(losses))
+        out["loss_finite"] = bool(all(np.isfinite([lv for _, lv in log.losses()])))
+    del eng, model_, dev_pool
+    torch.cuda.empty_cache()
 
     # ---- end to end through the public API with HOST buffers. One GPU: the engine-level
     # C-ABI (dsp_run via NativeEngine) -- every step copies its batch host->device (pinned)
     # and its loss / grad-norm row device->host inside the timed region. N GPUs: the
     # Python-orchestrated TrainEngine on host batches with a per-step loss read.
-    e2e = None
-    if not args.no_e2e:
+    out["e2e"] = None
+    if e2e:
+        host_pool = synthetic_batches(npool, batch, in_shape, classes, seed=0)
         model2 = P.build_model(layers, bounds)
         P.init_params(model2, 0)
         if world == 1:
             from paper_1909_02625_b200.native import NativeEngine
 
-            eng2 = NativeEngine(model2, cfg, args.batch, P.LrSchedule(o["lr"]), rule=o["rule"], beta=o["beta"],
-                                s=o["s"], weight_decay=5e-4, device=dev.index)
+            eng2 = NativeEngine(model2, cfg, batch, P.LrSchedule(o["lr"]), rule=o["rule"], beta=o["beta"],
+                                s=o["s"], weight_decay=5e-4, device=dev.index, precision=precision)
             xs = np.stack([np.asarray(x, dtype=np.float32) for x, _ in host_pool])
             ls = np.stack([np.asarray(lab, dtype=np.int64) for _, lab in host_pool])
+            del host_pool
             warm2 = max(warm, eng2.horizon + eng2.ring + 1)  # every graph phase captured before timing
-            sel = np.arange(warm2 + args.steps) % len(host_pool)
+            sel = np.arange(warm2 + steps) % len(xs)
             xw, lw = xs[sel[:warm2]], ls[sel[:warm2]]
             xt, lt = np.ascontiguousarray(xs[sel[warm2:]]), np.ascontiguousarray(ls[sel[warm2:]])
             eng2.run_batches(xw, lw)
@@ -540,14 +559,14 @@ def run_b200(args):
                    "and async D2H of the step's loss/grad-norm row; graphs replayed natively")
         else:
             eng2 = P.TrainEngine(model2, cfg, cycle(host_pool), P.LrSchedule(o["lr"]), rule=o["rule"],
-                                 beta=o["beta"], s=o["s"], weight_decay=5e-4, device=dev)
+                                 beta=o["beta"], s=o["s"], weight_decay=5e-4, device=dev, precision=precision)
             for _ in range(warm):
                 eng2.run(1)
                 eng2.last_loss()
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
-            for _ in range(args.steps):
+            for _ in range(steps):
                 eng2.run(1)
                 eng2.last_loss()  # device->host read of the step's result
             torch.cuda.synchronize()
@@ -555,32 +574,182 @@ def run_b200(args):
             tt = torch.tensor([el], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             el = float(tt.item())
-            h2d = args.batch * int(np.prod(IN_SHAPE)) * 4 + args.batch * 8 if 0 in eng2.local else 0
+            h2d = batch * int(np.prod(in_shape)) * 4 + batch * 8 if 0 in eng2.local else 0
             d2h = 4 if (K - 1) in eng2.local else 0
             how = "host wall clock incl. pinned H2D + per-step loss D2H (Python engine, one rank per GPU)"
-        e2e = {"value": args.batch * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "timing": how}
+        out["e2e"] = {"value": batch * steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "timing": how}
         del eng2, model2
+        torch.cuda.empty_cache()
+    return out
 
-    roof = kernel_roofline(torch, peaks, args.batch, live_us, spec) if rank == 0 else None
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+# shapes of the per-conv tensor-pipe summary: ResNet-50's 3x3 stage convs (the tensor-bound ones)
+TC_SHAPES = [("s1.3x3", 56, 64, 64), ("s2.3x3", 28, 128, 128), ("s3.3x3", 14, 256, 256), ("s4.3x3", 7, 512, 512)]
+
+
+def conv_tensor_pipe(torch, peaks, batch: int):
+    """Per-conv fraction of the bf16 tensor peak: FLOP/s of isolated event-timed launches through
+    dsp_igemm (FPROP with the fused BN statistics + finalize, DGRAD, WGRAD with split-K) on
+    buffers rotated past L2, divided by MEASURED_PEAKS bf16_tflops.  The ncu counter view of the
+    same kernels (sm__pipe_tensor_cycles_active) is committed under profiles/."""
+    import ctypes as C
+
+    from paper_1909_02625_b200 import _lib as L
+
+    lib = L.load()
+    st = torch.cuda.current_stream()
+    peak = peaks.get("bf16_tflops", 2250.0)
+    out = {}
+    for name, H, Cc, K in TC_SHAPES:
+        M = batch * H * H
+        Kd = 9 * Cc
+        nbuf = max(2, int(2 * L2_BYTES // (M * Cc * 2)) + 1)
+        xs = [torch.randn(M * Cc, device="cuda").bfloat16() for _ in range(nbuf)]
+        dys = [torch.randn(M * K, device="cuda").bfloat16() for _ in range(nbuf)]
+        outs = [torch.empty(M * max(K, Cc), device="cuda", dtype=torch.bfloat16) for _ in range(nbuf)]
+        w = (torch.randn(K * Kd, device="cuda") * 0.05).bfloat16()
+        w_t = w.view(K, 9, Cc).permute(2, 1, 0).contiguous()
+        gamma, beta = torch.ones(K, device="cuda"), torch.zeros(K, device="cuda")
+        stats = torch.empty(L.IGEMM_MAX_CTAS * 3 * K, device="cuda")
+        stat_out = torch.empty(4 * K, device="cuda")
+        sem = torch.zeros(64, dtype=torch.int32, device="cuda")
+        g = L.ConvGeom(batch, H, H, Cc, H, H, K, 3, 3, 1, 1)
+        # WGRAD split-K as the block executor sizes it (block.cu wgrad_splits: ~148 CTAs)
+        nkb = (M + 63) // 64
+        mt, nt = (Kd + 127) // 128, (K + 255) // 256
+        splits = max(1, min(148 // max(1, mt * nt), nkb))
+        kbps = (nkb + splits - 1) // splits
+        splits = (nkb + kbps - 1) // kbps
+        part = torch.empty(splits * Kd * K, device="cuda")
+
+        def launch(mode, i):
+            a = L.IgemmArgs()
+            a.geom = g
+            if mode == L.DSP_IGEMM_FPROP:
+                a.M, a.N, a.Kd = M, K, Kd
+                a.A, a.B, a.D, a.ldd = xs[i].data_ptr(), w.data_ptr(), outs[i].data_ptr(), K
+                a.stats, a.stat_out, a.gamma, a.beta, a.sem = (stats.data_ptr(), stat_out.data_ptr(), gamma.data_ptr(),
+                                                               beta.data_ptr(), sem.data_ptr())
+                a.n_valid = K
+            elif mode == L.DSP_IGEMM_DGRAD:
+                a.M, a.N, a.Kd = M, Cc, 9 * K
+                a.A, a.B, a.D, a.ldd = dys[i].data_ptr(), w.data_ptr(), outs[i].data_ptr(), Cc
+                a.B_t = w_t.data_ptr()
+                a.n_valid = Cc
+            else:
+                a.M, a.N, a.Kd = Kd, K, M
+                a.A, a.B, a.D = xs[i].data_ptr(), dys[i].data_ptr(), part.data_ptr()
+                a.kb_per_split = kbps
+            L.check(lib.dsp_igemm(mode, L.DSP_DTYPE_BF16, C.byref(a), splits if mode == L.DSP_IGEMM_WGRAD else 1,
+                                  C.c_void_p(st.cuda_stream)))
+
+        row = {}
+        for mname, mode in (("fprop", L.DSP_IGEMM_FPROP), ("dgrad", L.DSP_IGEMM_DGRAD), ("wgrad", L.DSP_IGEMM_WGRAD)):
+            for i in range(nbuf):
+                launch(mode, i)
+            torch.cuda.synchronize()
+            reps = max(4 * nbuf, 12)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for i in range(reps):
+                launch(mode, i % nbuf)
+            e1.record(st)
+            e1.synchronize()
+            us = e0.elapsed_time(e1) * 1000.0 / reps
+            tflops = 2.0 * M * K * Kd / (us * 1e-6) / 1e12
+            row[mname] = {"us": round(us, 2), "tflops": round(tflops, 1), "frac": round(tflops / peak, 4)}
+        out[name] = row
+        del xs, dys, outs, part
+        torch.cuda.empty_cache()
+    fr = [r[m]["frac"] for r in out.values() for m in r]
+    return {"convs": out, "mean_frac": round(float(np.mean(fr)), 4), "peak_tflops": peak,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+            "timing": f"isolated dsp_igemm launches, CUDA events, buffers rotated past L2, B={batch}",
+            "ncu": "profiles/r02_conv_tensor_pipe.md"}
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N without a torchrun environment: re-exec this script under torch.distributed.run."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    K = blocks_for(args)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    spec = roofline_spec(args.model, args.batch)
+    main_run = measure(args.model, K, args.batch, args.steps, args.warmup, dev, world, cuts=args.cuts,
+                       probe=spec, e2e=not args.no_e2e, clock=True, precision=args.precision, opt=opt_of(args))
+    extras = {}
+    if not args.no_extras:
+        # the metric's "vs BP": K = 1 (p = (0,), m = (0,)) is plain backprop, bitwise
+        # (tests/test_pipeline.py:152-168), on the same model and batch, one rank
+        if world == 1:
+            bp = measure(args.model, 1, args.batch, args.steps, args.warmup, dev, 1, e2e=False,
+                         precision=args.precision, opt=opt_of(args))
+            extras["k1_bp"] = {"value": bp["value"], "unit": UNIT, "ms_per_step": bp["ms_per_step"],
+                               "dsp_over_bp": main_run["value"] / bp["value"],
+                               "config": "same model / batch / optimizer, K=1 (one block, plain BP)"}
+            extras["conv_tensor_pipe"] = conv_tensor_pipe(torch, peaks, MODELS["resnet50"]["batch"])
+        if args.model != "resnet56":
+            r56 = measure("resnet56", 8 if world >= 8 else 4, MODELS["resnet56"]["batch"], args.steps, args.warmup, dev,
+                          world, e2e=not args.no_e2e, precision=args.precision)
+            extras["resnet56"] = {"value": r56["value"], "unit": UNIT, "ms_per_step": r56["ms_per_step"],
+                                  "e2e": r56["e2e"], "config": config_dict_for("resnet56", 8 if world >= 8 else 4,
+                                                                              MODELS["resnet56"]["batch"], world)}
+    roof = kernel_roofline(torch, peaks, args.batch, main_run["live_us"], spec) if rank == 0 else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             sub = 32 if IN_SHAPE[1] <= 32 else 2
             v, dt, cpu_s = cpu_oracle_steps(args, 3 if sub > 2 else 1, 1, sub)
             cpu = {"value": v, "unit": UNIT, "cores": threads_used(), "kind": "port",
-                   "sample": f"oracle/dsp_ref.py float64 DSP step (CPU restatement of the reference), ResNet-{DEPTH} "
+                   "sample": f"oracle/dsp_ref.py float64 DSP step (CPU restatement of the reference), {args.model} "
                              f"K={K}, {3 if sub > 2 else 1} timed step(s) of a {sub}-sample sub-batch after 1 warmup "
                              f"({dt:.1f} s)"}
         except Exception as exc:  # the baseline must never sink the bench line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc!r}"}
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": warm, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": config_dict(args, K, world), "e2e": e2e, "gpu_launches": int(launches),
-                "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "step_ms_median": statistics.median(step_ms), "loss_finite": bool(loss_ok)}
+        line = {"metric": METRIC, "value": main_run["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": main_run["warm"], "ms_per_step": main_run["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+                "config": config_dict(args, K, world), "e2e": main_run["e2e"], "gpu_launches": main_run["launches"],
+                "roofline": roof, "cpu_baseline": cpu, "clocks": main_run["clocks"],
+                "step_ms_median": main_run["step_ms_median"], "loss_finite": main_run["loss_finite"], **extras}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -590,6 +759,8 @@ def run_b200(args):
 def main():
     args = parse()
     select_model(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -37,7 +37,7 @@ extern "C" {
 
 /* ------------------------------------------------------------ enums */
 #define DSP_DTYPE_BF16 0 /* bf16 storage, kind::f16 tensor-core MMA, fp32 accumulate */
-#define DSP_DTYPE_F32 1  /* fp32 storage, kind::tf32 tensor-core MMA, fp32 accumulate */
+#define DSP_DTYPE_F32 1  /* fp32 storage, 3xTF32 on kind::tf32 tensor cores (fp32-faithful), fp32 accumulate */
 
 #define DSP_IGEMM_FPROP 0
 #define DSP_IGEMM_DGRAD 1
@@ -91,7 +91,9 @@ typedef struct {
   const void* B;           /* FPROP/DGRAD: packed weights [K][R][S][C]; WGRAD: dY */
   void* D;                 /* FPROP/DGRAD: output [M][ldd]; WGRAD: fp32 partials [splits][M][N] */
   int32_t ldd;
-  int32_t out_f32;         /* FPROP/DGRAD: store fp32 instead of the storage dtype */
+  int32_t out_f32;         /* FPROP/DGRAD: 1 = store fp32 instead of the storage dtype (0 or 1; other values are
+                              rejected -- builds with -DIG_TRACE_BUILD read diagnostic switches from the
+                              upper bits) */
   const void* residual;    /* optional [M][ldd] added in the epilogue */
   const float* bias;       /* optional [N] added in the epilogue */
   float* stats;            /* optional BatchNorm partials, one row per CTA: [DSP_IGEMM_MAX_CTAS][2][N]
@@ -210,9 +212,23 @@ int dsp_update_adam_f32(int64_t n, float* x, const float* grad, float* m, float*
  * last block, which uses dlogits).  grad_in: padded dX or NULL to skip the
  * input gradient (block 0).  Writes the flat fp32 parameter gradient. */
 int dsp_block_backward(dsp_block_t* blk, const void* upstream, void* grad_in, void* stream);
-/* Update the bound params from the bound grads and re-pack the weight shadow. */
+/* Update the bound params from the bound grads and re-pack the weight shadow, in ONE launch (a
+ * tile table covers the parameter vector: each weight tile is updated, written to the storage-
+ * dtype shadow and, through shared memory, to its transposed DGRAD copy; the grad-norm partials
+ * are summed by the last CTA into *grad_sq_out). apply = 0: grad norm only (a discarded warmup
+ * update, pipeline.py:594). A non-finite gradient (after weight decay) in an applied update sets
+ * the block's sticky non-finite flag (dsp_block_nonfinite). */
 int dsp_block_update(dsp_block_t* blk, int rule, float* ys, double lr, double slr, double beta, double wd,
                      int apply, float* grad_sq_out, void* stream);
+
+/* Sticky non-finite flags of a block -- the device side of the reference's NonFiniteError
+ * (tensor.py:34-37 / 101-111, optim.py:53 / 89), checked at sync points instead of raising in the
+ * middle of an asynchronous step: bit 0 = dsp_block_loss produced a non-finite loss, bit 1 = an
+ * applied dsp_block_update met a non-finite gradient. One 4-byte device->host copy on `stream` and
+ * a stream synchronize; clear != 0 resets the flags. */
+#define DSP_NONFINITE_LOSS 1
+#define DSP_NONFINITE_GRAD 2
+int dsp_block_nonfinite(dsp_block_t* blk, int clear, int* flags_out, void* stream);
 
 /* Adam variant of dsp_block_update: state = DSP_ADAM_STATE_BYTES(param_count) bytes of device
  * memory laid out as described at DSP_ADAM_STATE_BYTES (the step counter advances on apply). */
@@ -258,7 +274,7 @@ typedef struct {
   int32_t m[DSP_MAX_BLOCKS];      /* staleness per block (m[K-1] >= 0) */
   int32_t warmup;                 /* DSP_WARMUP_* */
   int32_t batch;                  /* B */
-  int32_t dtype;                  /* DSP_DTYPE_BF16 */
+  int32_t dtype;                  /* DSP_DTYPE_BF16 (bf16 storage) or DSP_DTYPE_F32 (fp32 storage, 3xTF32) */
   int32_t in_c, in_h, in_w;       /* one sample of the host batches, (C,H,W) flattened C-major */
   int32_t num_classes;            /* labels must lie in [0, num_classes) */
   int32_t n_layers[DSP_MAX_BLOCKS];
@@ -295,7 +311,9 @@ int dsp_set_adam(dsp_engine_t* eng, double beta1, double beta2, double eps);
 /* n_steps DSP steps. x: host float32 [n_steps][B][C*H*W], labels: host int64
  * [n_steps][B] -- batch n of this call is the data stream's next batch. Each
  * step copies its batch host->device and its loss / grad-norm row device->host
- * (pinned, asynchronous); returns after the last step completed. */
+ * (pinned, asynchronous); returns after the last step completed, with
+ * DSP_E_NONFINITE if any block's non-finite flag is set (dsp_block_nonfinite;
+ * the reference's NonFiniteError). */
 int dsp_run(dsp_engine_t* eng, int n_steps, const float* x, const int64_t* labels);
 /* Records of all steps so far, sorted by (step, block); *n = how many (<= cap written). */
 int dsp_read_log(dsp_engine_t* eng, dsp_log_record_t* recs, size_t cap, size_t* n);

@@ -150,7 +150,8 @@ def bn_bwd(g, cache, gamma):
 
 
 # ------------------------------------------------------------ storage emulation
-# "f64": pure float64 (the reference's precision).  "bf16": round every tensor
+# "f64": pure float64 (the reference's precision).  "f32": round every stored tensor to float32
+# (the device's fp32 parity mode; with acc="f32" also the conv GEMMs).  "bf16": round every tensor
 # the device stores in bf16 at exactly the device's storage points (conv
 # outputs, BN/ReLU outputs, unit outputs, activation gradients, the bf16
 # weight shadow) so that ReLU masks match the device; sums stay float64.
@@ -173,8 +174,17 @@ def bf16_round(x):
     return r.view(np.float32).astype(np.float64)
 
 
+def f32_round(x):
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
 def q(x):
-    return bf16_round(x) if STORAGE["mode"] == "bf16" else x
+    mode = STORAGE["mode"]
+    if mode == "bf16":
+        return bf16_round(x)
+    if mode == "f32":
+        return f32_round(x)
+    return x
 
 
 # ------------------------------------------------------------ layer fwd / bwd

@@ -751,11 +751,11 @@ def stale_gradient(model: Model, fwd, bwd, x, labels, loss_and_grad=softmax_xent
 
 
 class storage:
-    """Context manager selecting the oracle's storage emulation ("f64" or "bf16") and the conv
-    accumulation precision ("f64", or "f32" for the noise-floor measurement of cnn._mm)."""
+    """Context manager selecting the oracle's storage emulation ("f64", "f32" or "bf16") and the
+    conv accumulation precision ("f64", or "f32" for the noise-floor measurement of cnn._mm)."""
 
     def __init__(self, mode: str, acc: str = "f64"):
-        if mode not in ("f64", "bf16") or acc not in ("f64", "f32"):
+        if mode not in ("f64", "f32", "bf16") or acc not in ("f64", "f32"):
             raise ValueError((mode, acc))
         self.mode, self.acc = mode, acc
 

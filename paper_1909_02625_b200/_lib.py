@@ -20,7 +20,27 @@ DSP_E_CUDA = 2
 DSP_E_STATE = 3
 DSP_E_NONFINITE = 4
 DSP_GRAPH_NODE_PRIORITY = 1
+DSP_NONFINITE_LOSS = 1
+DSP_NONFINITE_GRAD = 2
 DSP_DTYPE_F32 = 1
+# engine precisions (storage dtype + tensor-core arithmetic):
+#   "bf16": bf16 activations / weight shadow, kind::f16 MMA -- the performance mode;
+#   "fp32": fp32 activations / weight shadow, 3xTF32 on kind::tf32 (each operand split into a
+#           tf32 hi part and an fp32 remainder, three MMAs) -- fp32-faithful, the parity mode.
+# Accumulation, BatchNorm statistics, master weights and optimizer state are fp32 in both.
+PRECISIONS = {"bf16": DSP_DTYPE_BF16, "fp32": DSP_DTYPE_F32}
+
+
+def storage_dtype(precision: str) -> int:
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
+    return PRECISIONS[precision]
+
+
+def torch_storage(dtype_code: int):
+    import torch
+
+    return torch.float32 if dtype_code == DSP_DTYPE_F32 else torch.bfloat16
 
 DSP_IGEMM_FPROP = 0
 DSP_IGEMM_DGRAD = 1
@@ -142,6 +162,7 @@ _SIGNATURES = {
     "dsp_set_adam": (C.c_int, [_P, C.c_double, C.c_double, C.c_double]),
     "dsp_block_update": (C.c_int, [_P, C.c_int, _P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
                                    _P, _P]),
+    "dsp_block_nonfinite": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _P]),
     "dsp_pack_input": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "dsp_unpack_output": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "dsp_last_error": (C.c_char_p, []),
@@ -201,7 +222,12 @@ def load(require_symbols: bool = True):
 def check(rc: int) -> None:
     if rc != 0:
         msg = load().dsp_last_error()
-        raise DspError(rc, msg.decode() if msg else "unknown")
+        msg = msg.decode() if msg else "unknown"
+        if rc == DSP_E_NONFINITE:  # the reference's NonFiniteError (tensor.py:34-37, optim.py:53 / 89)
+            from .optim import NonFiniteError
+
+            raise NonFiniteError(msg)
+        raise DspError(rc, msg)
 
 
 def lib():

@@ -68,8 +68,11 @@ extern "C" int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int 
   const dsp_conv_geom_t& g = args->geom;
   if (g.C % epc || g.K % epc) return set_error(DSP_E_INVALID, "dsp_igemm: channels C=%d K=%d not multiples of %d", g.C, g.K, epc);
   if (args->M <= 0 || args->N <= 0 || args->Kd <= 0) return set_error(DSP_E_INVALID, "dsp_igemm: empty GEMM");
-  if (dtype == DSP_DTYPE_F32 && mode != DSP_IGEMM_FPROP)
-    return set_error(DSP_E_INVALID, "dsp_igemm: fp32/tf32 storage supports FPROP only (MN-major tf32 operands unsupported)");
+#ifndef IG_TRACE_BUILD
+  // (trace builds pass ablation / fence-diagnostic switches in the upper bits, igemm_kern.cuh)
+  if (args->out_f32 != 0 && args->out_f32 != 1)
+    return set_error(DSP_E_INVALID, "dsp_igemm: out_f32 must be 0 or 1, got %d", args->out_f32);
+#endif
   if (mode == DSP_IGEMM_WGRAD && (splits <= 0 || args->kb_per_split <= 0))
     return set_error(DSP_E_INVALID, "dsp_igemm: WGRAD needs splits and kb_per_split");
   if (args->bnb_count != 0) {

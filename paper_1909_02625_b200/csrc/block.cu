@@ -67,9 +67,10 @@ struct dsp_block {
   size_t ws_bytes = 0;
   size_t S[4] = {0, 0, 0, 0};
   size_t G[2] = {0, 0};
-  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0, sem = 0;
-  size_t packed = 0, ptable = 0;
+  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0, sem = 0, usem = 0, nf = 0;
+  size_t packed = 0, ptable = 0, utable = 0;
   std::vector<dsp::PackEntry> packs;
+  std::vector<dsp::UpdTile> utiles;  // fused update + repack tile table (elementwise.cu update_pack)
   int pack_max = 0;
   size_t dlogits = 0;
   int classes = 0, classes_pad = 0;
@@ -147,6 +148,76 @@ inline P* at(dsp_block* b, size_t off) {
 
 // packed storage-dtype weights this block's convs read (its own, or a forward twin's primary's)
 inline const uint8_t* packed_base(const dsp_block* b) { return b->wsrc ? b->wsrc : b->ws + b->packed; }
+
+// Tile table of the fused update + repack (kernels.cuh UpdTile): every weight tensor in 32 x 32
+// tiles carrying its shadow destinations (conv: [co][tap][ci] same orientation + the per-tap
+// transposed DGRAD copy [ci][tap][co]; dense W[in][out]: its [out][in] shadow, transposed),
+// then every remaining parameter (BatchNorm gamma / beta, biases) in flat runs of <= 1024.
+// Each parameter is covered exactly once (checked).
+int build_update_tiles(dsp_block* b) {
+  std::vector<char> cov((size_t)std::max<int64_t>(b->param_count, 1), 0);
+  auto mark = [&](int64_t i) {
+    if (i < 0 || i >= b->param_count || cov[(size_t)i]) return false;
+    cov[(size_t)i] = 1;
+    return true;
+  };
+  for (const PackEntry& e : b->packs) {
+    if (e.dense_src == 2) continue;  // folded into its conv's tiles below
+    if (e.dense_src == 0) {
+      int64_t dst_t = -1;
+      for (const PackEntry& t : b->packs)
+        if (t.dense_src == 2 && t.src_off == e.src_off) dst_t = t.dst_off;
+      for (int tap = 0; tap < e.rs; ++tap)
+        for (int co0 = 0; co0 < e.co; co0 += 32)
+          for (int ci0 = 0; ci0 < e.ci; ci0 += 32) {
+            UpdTile u{};
+            u.rows = std::min(32, e.co - co0);
+            u.cols = std::min(32, e.ci - ci0);
+            u.src = e.src_off + ((int64_t)co0 * e.rs + tap) * e.ci + ci0;
+            u.src_rs = e.rs * e.ci;
+            u.dst_a = e.dst_off + ((int64_t)co0 * e.rs + tap) * e.cip + ci0;
+            u.dst_a_rs = e.rs * e.cip;
+            u.dst_b = dst_t < 0 ? -1 : dst_t + ((int64_t)ci0 * e.rs + tap) * e.cop + co0;
+            u.dst_b_cs = e.rs * e.cop;
+            for (int r = 0; r < u.rows; ++r)
+              for (int c = 0; c < u.cols; ++c)
+                if (!mark(u.src + (int64_t)r * u.src_rs + c)) return set_error(DSP_E_INVALID, "update tiles overlap");
+            b->utiles.push_back(u);
+          }
+    } else {  // dense W[in = ci][out = co] -> shadow [co][cip]
+      for (int i0 = 0; i0 < e.ci; i0 += 32)
+        for (int o0 = 0; o0 < e.co; o0 += 32) {
+          UpdTile u{};
+          u.rows = std::min(32, e.ci - i0);
+          u.cols = std::min(32, e.co - o0);
+          u.src = e.src_off + (int64_t)i0 * e.co + o0;
+          u.src_rs = e.co;
+          u.dst_a = -1;
+          u.dst_b = e.dst_off + (int64_t)o0 * e.cip + i0;
+          u.dst_b_cs = e.cip;
+          for (int r = 0; r < u.rows; ++r)
+            for (int c = 0; c < u.cols; ++c)
+              if (!mark(u.src + (int64_t)r * u.src_rs + c)) return set_error(DSP_E_INVALID, "update tiles overlap");
+          b->utiles.push_back(u);
+        }
+    }
+  }
+  for (int64_t i = 0; i < b->param_count;) {
+    if (cov[(size_t)i]) {
+      ++i;
+      continue;
+    }
+    int64_t j = i;
+    while (j < b->param_count && !cov[(size_t)j] && j - i < 1024) cov[(size_t)j++] = 1;
+    UpdTile u{};
+    u.src = i;
+    u.cols = (int)(j - i);
+    u.dst_a = u.dst_b = -1;
+    b->utiles.push_back(u);
+    i = j;
+  }
+  return DSP_OK;
+}
 
 // ------------------------------------------------------------------ kernels per conv
 int conv_fprop(dsp_block* b, const ConvP& c, const void* x, cudaStream_t st) {
@@ -447,12 +518,13 @@ using namespace dsp;
 extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, int batch, int dtype, int is_last,
                                 dsp_block_t** out) {
   if (!layers || n_layers <= 0 || batch <= 0 || !out) return set_error(DSP_E_INVALID, "dsp_block_create: bad args");
-  if (dtype != DSP_DTYPE_BF16) return set_error(DSP_E_INVALID, "dsp_block_create: only bf16 storage is supported");
+  if (dtype != DSP_DTYPE_BF16 && dtype != DSP_DTYPE_F32)
+    return set_error(DSP_E_INVALID, "dsp_block_create: dtype %d is neither DSP_DTYPE_BF16 nor DSP_DTYPE_F32", dtype);
   dsp_block* b = new dsp_block();
   b->B = batch;
   b->dtype = dtype;
   b->is_last = is_last;
-  b->esz = 2;
+  b->esz = dtype == DSP_DTYPE_F32 ? 4 : 2;
   Planner pl;
   const int B = batch;
   // running shape (real channels, h, w)
@@ -625,9 +697,17 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
   b->bpart = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
   b->bpart2 = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
   b->wpart = pl.take((size_t)std::max<int64_t>(max_wpart, 1) * 4);
-  b->upart = pl.take((size_t)update_grid(std::max<int64_t>(b->param_count, 1)) * 8);
+  if (build_update_tiles(b) != DSP_OK) {
+    delete b;
+    return DSP_E_INVALID;
+  }
+  b->upart = pl.take((size_t)std::max(update_grid(std::max<int64_t>(b->param_count, 1)),
+                                      update_pack_grid((int)b->utiles.size())) * 8);
+  b->usem = pl.take(256);  // update grad-norm ticket (zeroed at bind, left zero)
+  b->nf = pl.take(256);    // sticky non-finite flags (dsp_block_nonfinite)
   b->packed = pl.take((size_t)std::max<int64_t>(pack_elems, 1) * b->esz);
   b->ptable = pl.take(sizeof(PackEntry) * std::max<size_t>(b->packs.size(), 1));
+  b->utable = pl.take(sizeof(UpdTile) * std::max<size_t>(b->utiles.size(), 1));
   for (auto& p : b->packs) b->pack_max = std::max(b->pack_max, p.cop * p.rs * p.cip);
   b->ws_bytes = pl.off;
   *out = b;
@@ -666,7 +746,10 @@ extern "C" int dsp_block_bind(dsp_block_t* b, void* workspace, float* params, fl
   if (!b->packs.empty())
     DSP_CUDA(cudaMemcpyAsync(b->ws + b->ptable, b->packs.data(), sizeof(PackEntry) * b->packs.size(),
                              cudaMemcpyHostToDevice, st));
-  DSP_CUDA(cudaStreamSynchronize(st));  // the pack table source is a host vector
+  if (!b->utiles.empty())
+    DSP_CUDA(cudaMemcpyAsync(b->ws + b->utable, b->utiles.data(), sizeof(UpdTile) * b->utiles.size(),
+                             cudaMemcpyHostToDevice, st));
+  DSP_CUDA(cudaStreamSynchronize(st));  // the table sources are host vectors
   return dsp_block_pack(b, stream);
 }
 
@@ -705,7 +788,7 @@ extern "C" int dsp_block_loss(dsp_block_t* b, const int64_t* labels, float* loss
   if (!labels || !loss) return set_error(DSP_E_INVALID, "dsp_block_loss: null pointer");
   const LayerP& l = b->L.back();
   DSP_CUDA(softmax_xent(b->dtype, at<float>(b, l.out), l.out_cp, b->B, b->classes, labels, b->ws + b->dlogits, loss,
-                        (cudaStream_t)stream));
+                        at<int>(b, b->nf), (cudaStream_t)stream));
   return DSP_OK;
 }
 
@@ -754,15 +837,11 @@ extern "C" int dsp_block_update(dsp_block_t* b, int rule, float* ys, double lr, 
     if (grad_sq_out) DSP_CUDA(cudaMemsetAsync(grad_sq_out, 0, sizeof(float), st));
     return DSP_OK;
   }
-  float* part = at<float>(b, b->upart);
-  if (apply) {
-    DSP_CUDA(update_f32(rule, n, b->params, b->grads, ys, (float)lr, (float)slr, (float)beta, (float)wd, part, st));
-  } else {
-    // grad norm only (discarded warmup update, pipeline.py:594)
-    DSP_CUDA(sumsq_f32(n, b->grads, part, st));
-  }
-  if (grad_sq_out) DSP_CUDA(sum_partials_f32(part, update_grid(n), grad_sq_out, st));
-  if (apply) DSP_TRY(dsp_block_pack(b, stream));
+  // one launch: update + weight-shadow repack + grad norm (or, for a discarded warmup update,
+  // pipeline.py:594, the grad norm alone)
+  DSP_CUDA(update_pack(b->dtype, rule, apply, at<UpdTile>(b, b->utable), (int)b->utiles.size(), b->params, b->grads,
+                       ys, b->ws + b->packed, (float)lr, (float)slr, (float)beta, (float)wd, at<float>(b, b->upart),
+                       at<int>(b, b->usem), grad_sq_out, at<int>(b, b->nf), st));
   return DSP_OK;
 }
 
@@ -804,5 +883,17 @@ extern "C" int dsp_block_share_weights(dsp_block_t* twin, const dsp_block_t* pri
                      "dsp_block_share_weights: twin must be planned from the same program and bound to the "
                      "primary's params");
   twin->wsrc = primary->ws + primary->packed;
+  return DSP_OK;
+}
+
+extern "C" int dsp_block_nonfinite(dsp_block_t* b, int clear, int* flags_out, void* stream) {
+  if (!b || !b->ws) return set_error(DSP_E_STATE, "dsp_block_nonfinite: block not bound");
+  if (!flags_out) return set_error(DSP_E_INVALID, "dsp_block_nonfinite: null output");
+  cudaStream_t st = (cudaStream_t)stream;
+  int v = 0;
+  DSP_CUDA(cudaMemcpyAsync(&v, b->ws + b->nf, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DSP_CUDA(cudaStreamSynchronize(st));
+  if (clear && v) DSP_CUDA(cudaMemsetAsync(b->ws + b->nf, 0, sizeof(int), st));
+  *flags_out = v;
   return DSP_OK;
 }

@@ -13,6 +13,8 @@
 
 #include <math.h>
 
+#include <algorithm>
+
 namespace dsp {
 
 namespace {
@@ -707,7 +709,7 @@ __global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict
 // ------------------------------------------------------------------ loss
 template <typename T>
 __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, int C, const int64_t* __restrict__ labels,
-                               T* __restrict__ dlogits, float* __restrict__ loss) {
+                               T* __restrict__ dlogits, float* __restrict__ loss, int* __restrict__ nf) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   extern __shared__ float row_loss[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -738,7 +740,9 @@ __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, 
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int b = 0; b < B; ++b) s += (double)row_loss[b];
-    *loss = (float)(s / (double)B);
+    const float l = (float)(s / (double)B);
+    *loss = l;
+    if (nf != nullptr && !isfinite(l)) atomicOr(nf, 1);  // NonFiniteError (tensor.py:101-111)
   }
 }
 
@@ -821,6 +825,144 @@ __global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__
 }
 
 // ------------------------------------------------------------------ optimizer
+// One parameter of the SGD / SUM step (optim.py:48-99 with the coupled weight decay of
+// pipeline.py:591-593), IEEE ops without FMA contraction; accumulates grad^2 (pre-WD) into sq.
+template <int RULE, bool WD>
+__device__ __forceinline__ float upd1(float xv, float g0, float& ysv, float lr, float slr, float beta, float wd,
+                                      float& sq, bool& bad) {
+  sq = __fadd_rn(sq, __fmul_rn(g0, g0));
+  const float g = WD ? __fadd_rn(g0, __fmul_rn(wd, xv)) : g0;
+  bad |= !isfinite(g);
+  if (RULE == DSP_RULE_SGD) return __fsub_rn(xv, __fmul_rn(lr, g));
+  const float y = __fsub_rn(xv, __fmul_rn(lr, g));
+  const float ysn = __fsub_rn(xv, __fmul_rn(slr, g));
+  const float xn = (beta == 0.f) ? y : __fadd_rn(y, __fmul_rn(beta, __fsub_rn(ysn, ysv)));
+  ysv = ysn;
+  return xn;
+}
+
+// 4 consecutive parameters [i, i + n4) (n4 <= 4) of the flat vector, updated in place; the new
+// values are returned in out[] (APPLY) and the grad^2 added to sq. 16-byte accesses when aligned.
+template <int RULE, bool WD, bool APPLY>
+__device__ __forceinline__ void upd4(int64_t i, int n4, float* __restrict__ x, const float* __restrict__ grad,
+                                     float* __restrict__ ys, float lr, float slr, float beta, float wd, float& sq,
+                                     bool& bad, float (&out)[4]) {
+  if (n4 == 4 && (i & 3) == 0) {
+    const float4 g = *reinterpret_cast<const float4*>(grad + i);
+    if (!APPLY) {
+      sq = __fadd_rn(sq, __fmul_rn(g.x, g.x));
+      sq = __fadd_rn(sq, __fmul_rn(g.y, g.y));
+      sq = __fadd_rn(sq, __fmul_rn(g.z, g.z));
+      sq = __fadd_rn(sq, __fmul_rn(g.w, g.w));
+      return;
+    }
+    const float4 xv = *reinterpret_cast<const float4*>(x + i);
+    float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (RULE == DSP_RULE_SUM) yv = *reinterpret_cast<const float4*>(ys + i);
+    out[0] = upd1<RULE, WD>(xv.x, g.x, yv.x, lr, slr, beta, wd, sq, bad);
+    out[1] = upd1<RULE, WD>(xv.y, g.y, yv.y, lr, slr, beta, wd, sq, bad);
+    out[2] = upd1<RULE, WD>(xv.z, g.z, yv.z, lr, slr, beta, wd, sq, bad);
+    out[3] = upd1<RULE, WD>(xv.w, g.w, yv.w, lr, slr, beta, wd, sq, bad);
+    *reinterpret_cast<float4*>(x + i) = make_float4(out[0], out[1], out[2], out[3]);
+    if (RULE == DSP_RULE_SUM) *reinterpret_cast<float4*>(ys + i) = yv;
+    return;
+  }
+  for (int j = 0; j < n4; ++j) {
+    const float g0 = grad[i + j];
+    if (!APPLY) {
+      sq = __fadd_rn(sq, __fmul_rn(g0, g0));
+      continue;
+    }
+    float yv = RULE == DSP_RULE_SUM ? ys[i + j] : 0.f;
+    out[j] = upd1<RULE, WD>(x[i + j], g0, yv, lr, slr, beta, wd, sq, bad);
+    x[i + j] = out[j];
+    if (RULE == DSP_RULE_SUM) ys[i + j] = yv;
+  }
+}
+
+// 4 consecutive storage-dtype values (8 bytes bf16 / 16 bytes fp32 when aligned)
+template <typename T>
+__device__ __forceinline__ void st4(T* p, int n4, const float (&v)[4]) {
+  if (n4 == 4 && (reinterpret_cast<uintptr_t>(p) & (4 * sizeof(T) - 1)) == 0) {
+    if constexpr (sizeof(T) == 2) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+      uint2 raw;
+      raw.x = *reinterpret_cast<uint32_t*>(&a);
+      raw.y = *reinterpret_cast<uint32_t*>(&b);
+      *reinterpret_cast<uint2*>(p) = raw;
+    } else {
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    return;
+  }
+  for (int j = 0; j < n4; ++j) p[j] = from_f<T>(v[j]);
+}
+
+// Fused optimizer step + weight-shadow repack over a tile table (kernels.cuh UpdTile).
+// 256 threads; a matrix tile: thread (r = tid / 8, c0 = 4 * (tid % 8)) updates 4 parameters of
+// row r, writes them to the same-orientation shadow, stages them in smem, and after a barrier
+// writes the transposed shadow 4 rows at a time (both shadow writes 8-byte chunks along rows).
+// The grad^2 partials of the CTAs are summed in fixed order by the last CTA (ticket).
+template <typename T, int RULE, bool WD, bool APPLY>
+__global__ void __launch_bounds__(kThreads) update_pack_k(const UpdTile* __restrict__ tiles, int n_tiles,
+                                                          float* __restrict__ x, const float* __restrict__ grad,
+                                                          float* __restrict__ ys, T* __restrict__ packed, float lr,
+                                                          float slr, float beta, float wd, float* __restrict__ part,
+                                                          int* sem, float* __restrict__ grad_sq_out,
+                                                          int* __restrict__ nf) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  __shared__ float stage[32][33];
+  __shared__ float red[kThreads];
+  __shared__ int last_s;
+  const int tid = threadIdx.x;
+  float sq = 0.f;
+  bool bad = false;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const UpdTile d = tiles[t];
+    float out[4] = {0.f, 0.f, 0.f, 0.f};
+    if (d.rows == 0) {  // flat tile
+      const int c = tid * 4;
+      if (c < d.cols) upd4<RULE, WD, APPLY>(d.src + c, min(4, d.cols - c), x, grad, ys, lr, slr, beta, wd, sq, bad, out);
+      continue;
+    }
+    const int r = tid >> 3, c0 = (tid & 7) * 4;
+    const int n4 = r < d.rows ? max(0, min(4, d.cols - c0)) : 0;
+    if (n4 > 0) {
+      upd4<RULE, WD, APPLY>(d.src + (int64_t)r * d.src_rs + c0, n4, x, grad, ys, lr, slr, beta, wd, sq, bad, out);
+      if (APPLY && d.dst_a >= 0) st4<T>(packed + d.dst_a + (int64_t)r * d.dst_a_rs + c0, n4, out);
+    }
+    if (APPLY && d.dst_b >= 0) {
+      for (int j = 0; j < n4; ++j) stage[r][c0 + j] = out[j];
+      __syncthreads();
+      const int c = tid >> 3, r0 = (tid & 7) * 4;  // transposed: column c, rows r0..r0+3
+      const int m4 = c < d.cols ? max(0, min(4, d.rows - r0)) : 0;
+      if (m4 > 0) {
+        float v[4];
+        for (int j = 0; j < 4; ++j) v[j] = j < m4 ? stage[r0 + j][c] : 0.f;
+        st4<T>(packed + d.dst_b + (int64_t)c * d.dst_b_cs + r0, m4, v);
+      }
+      __syncthreads();
+    }
+  }
+  red[tid] = sq;
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (APPLY && nf != nullptr && __syncthreads_or(bad) && tid == 0) atomicOr(nf, 2);  // optim.py:53, 89
+  if (grad_sq_out == nullptr) return;
+  if (tid == 0) part[blockIdx.x] = red[0];
+  if (last_cta_ticket(sem, (int)gridDim.x, &last_s)) {
+    if (tid == 0) {
+      double s = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) s += (double)__ldcg(&part[b]);
+      *grad_sq_out = (float)s;
+      *sem = 0;
+    }
+  }
+}
+
 template <int RULE, bool WD>
 __global__ void update_f32_k(int64_t n, float* __restrict__ x, const float* __restrict__ grad, float* __restrict__ ys,
                              float lr, float slr, float beta, float wd, float* __restrict__ part) {
@@ -1185,10 +1327,10 @@ cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void*
 }
 
 cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, const int64_t* labels, void* dlogits,
-                         float* loss, cudaStream_t st) {
+                         float* loss, int* nf, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    launch_k(softmax_xent_k<T>, 1, 512, B * sizeof(float), st, logits, ld, B, C, labels, (T*)dlogits, loss);
+    launch_k(softmax_xent_k<T>, 1, 512, B * sizeof(float), st, logits, ld, B, C, labels, (T*)dlogits, loss, nf);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -1213,6 +1355,27 @@ cudaError_t pack_weights(int dtype, const float* params, void* packed, const Pac
 }
 
 int update_grid(int64_t n) { return grid_for(n, kThreads, 148 * 4); }
+
+int update_pack_grid(int n_tiles) { return std::max(1, std::min(n_tiles, 148 * 8)); }
+
+cudaError_t update_pack(int dtype, int rule, int apply, const UpdTile* tiles, int n_tiles, float* x, const float* grad,
+                        float* ys, void* packed, float lr, float slr, float beta, float wd, float* part, int* sem,
+                        float* grad_sq_out, int* nf, cudaStream_t st) {
+  if (n_tiles <= 0) return cudaSuccess;
+  const int g = update_pack_grid(n_tiles);
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    T* pk = static_cast<T*>(packed);
+    auto go = [&](auto kern) {
+      launch_k(kern, g, kThreads, 0, st, tiles, n_tiles, x, grad, ys, pk, lr, slr, beta, wd, part, sem, grad_sq_out, nf);
+    };
+    const bool w = wd != 0.f;
+    if (!apply) go(update_pack_k<T, DSP_RULE_SGD, false, false>);
+    else if (rule == DSP_RULE_SGD) w ? go(update_pack_k<T, DSP_RULE_SGD, true, true>) : go(update_pack_k<T, DSP_RULE_SGD, false, true>);
+    else w ? go(update_pack_k<T, DSP_RULE_SUM, true, true>) : go(update_pack_k<T, DSP_RULE_SUM, false, true>);
+    return note_launch(), cudaGetLastError();
+  });
+}
 
 cudaError_t update_f32(int rule, int64_t n, float* x, const float* grad, float* ys, float lr, float slr, float beta,
                        float wd, float* part, cudaStream_t st) {

@@ -123,7 +123,8 @@ int validate(const dsp_config_t& c) {
     return set_error(DSP_E_INVALID, "dsp_create: unknown warmup policy %d", c.warmup);
   if (c.batch <= 0 || c.in_c <= 0 || c.in_h <= 0 || c.in_w <= 0 || c.num_classes <= 0 || !c.layers)
     return set_error(DSP_E_INVALID, "dsp_create: bad batch / input shape / classes / layers");
-  if (c.dtype != DSP_DTYPE_BF16) return set_error(DSP_E_INVALID, "dsp_create: only bf16 storage is supported");
+  if (c.dtype != DSP_DTYPE_BF16 && c.dtype != DSP_DTYPE_F32)
+    return set_error(DSP_E_INVALID, "dsp_create: dtype %d is neither DSP_DTYPE_BF16 nor DSP_DTYPE_F32", c.dtype);
   for (int k = 0; k < K; ++k)
     if (c.n_layers[k] <= 0) return set_error(DSP_E_INVALID, "dsp_create: block %d has no layers", k);
   return DSP_OK;
@@ -189,6 +190,21 @@ int issue_block(dsp_engine* e, int k, int64_t n, cudaStream_t st) {
                                  apply_update(e, k, n) ? 1 : 0, loss_slot + 1, st);
   return dsp_block_update(e->blk[k], e->rule, e->ys[k], lr, e->s * lr, e->beta, e->wd, apply_update(e, k, n) ? 1 : 0,
                           loss_slot + 1, st);
+}
+
+// NonFiniteError (tensor.py:34-37, optim.py:53 / 89) at the sync point ending dsp_run
+int check_nonfinite(dsp_engine* e) {
+  for (int k = 0; k < e->K; ++k) {
+    int f = 0;
+    DSP_TRY(dsp_block_nonfinite(e->blk[k], 0, &f, e->stream));
+    if (f & DSP_NONFINITE_LOSS)
+      return set_error(DSP_E_NONFINITE, "non-finite values in softmax_xent (block %d, by step %lld)", k,
+                       (long long)e->steps - 1);
+    if (f & DSP_NONFINITE_GRAD)
+      return set_error(DSP_E_NONFINITE, "non-finite gradient in %s (block %d, by step %lld)",
+                       e->rule == DSP_RULE_SGD ? "sgd_step" : "sum_step", k, (long long)e->steps - 1);
+  }
+  return DSP_OK;
 }
 
 int issue_step(dsp_engine* e, int64_t n, bool forked) {
@@ -318,7 +334,7 @@ extern "C" int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out) {
   }
   if (cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming) != cudaSuccess) return fail(DSP_E_CUDA);
   const int R = e->R;
-  const size_t esz = 2;
+  const size_t esz = cfg->dtype == DSP_DTYPE_F32 ? 4 : 2;
   int rc = DSP_OK;
   for (int k = 0; k < K && rc == DSP_OK; ++k) {
     if (k < K - 1) {
@@ -466,7 +482,7 @@ extern "C" int dsp_run(dsp_engine_t* e, int n_steps, const float* x, const int64
   }
   ENG_CUDA(cudaStreamSynchronize(e->stream));
   ENG_CUDA(cudaStreamSynchronize(e->copy_stream));
-  return DSP_OK;
+  return check_nonfinite(e);
 }
 
 extern "C" int64_t dsp_steps_done(dsp_engine_t* e) { return e ? e->steps : -1; }

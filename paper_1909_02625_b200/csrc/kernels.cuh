@@ -64,8 +64,9 @@ cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void*
 
 // softmax_xent (tensor.py:86-111) on fp32 logits [B][ld] (C real classes):
 // dlogits (storage dtype, pads zero) and the mean loss into *loss (device).
+// nf (optional): sticky flags, bit 0 set when the loss is not finite (tensor.py:101-111).
 cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, const int64_t* labels,
-                         void* dlogits, float* loss, cudaStream_t st);
+                         void* dlogits, float* loss, int* nf, cudaStream_t st);
 
 // Split-K WGRAD partials [splits][Mw][N] -> flat fp32 weight gradient.
 //  conv  (dense_layout=0): grad[(co*RS + tap)*ci_real + ci] for Mw = RS*Cp rows (tap*Cp + ci)
@@ -82,6 +83,32 @@ struct PackEntry {
 };                                           //   per tap [cip][rs][cop] (DGRAD K-major weights)
 cudaError_t pack_weights(int dtype, const float* params, void* packed, const PackEntry* entries_dev, int n_entries,
                          int max_elems, cudaStream_t st);
+
+// Fused per-block optimizer step + weight-shadow repack (one launch per block update): a
+// tile table covers the block's flat parameter vector exactly once. Matrix tiles are <= 32 x 32
+// sub-matrices of one weight tensor (conv W[co][tap][ci] at one tap, dense W[in][out]) whose
+// updated values also go to the storage-dtype shadow, in the same orientation (dst_a, row
+// stride dst_a_rs) and/or transposed (element (r, c) -> dst_b + c * dst_b_cs + r); flat tiles
+// (BatchNorm gamma / beta, biases) are <= 1024 consecutive parameters.
+struct UpdTile {
+  int64_t src;       // first parameter (flat index)
+  int64_t dst_a;     // same-orientation shadow destination (elements into the packed buffer), -1: none
+  int64_t dst_b;     // transposed shadow destination, -1: none
+  int32_t rows;      // matrix tile rows (0: flat tile)
+  int32_t cols;      // matrix tile columns, or the flat tile's length
+  int32_t src_rs;    // parameter row stride
+  int32_t dst_a_rs;  // same-orientation row stride
+  int32_t dst_b_cs;  // transposed column stride
+  int32_t pad_;
+};
+int update_pack_grid(int n_tiles);
+// apply = 0: only the grad-norm (a discarded warmup update, pipeline.py:594).  part: >=
+// update_pack_grid(n_tiles) floats; sem: a device int, 0 on entry (left 0); grad_sq_out: sum of
+// grad^2 (pre-WD, pipeline.py:602), written by the last CTA in fixed order; nf: sticky flags, bit 1
+// set when an applied update meets a non-finite gradient (optim.py:53, 89).
+cudaError_t update_pack(int dtype, int rule, int apply, const UpdTile* tiles_dev, int n_tiles, float* x,
+                        const float* grad, float* ys, void* packed, float lr, float slr, float beta, float wd,
+                        float* part, int* sem, float* grad_sq_out, int* nf, cudaStream_t st);
 
 // Optimizer step over a flat vector (optim.py:48-109, pipeline.py:591-596).
 int update_grid(int64_t n);

@@ -84,7 +84,8 @@ def synthetic_batches(n_batches: int, batch: int, in_shape, num_classes: int, se
 
 @dataclass
 class DeviceBatch:
-    """A batch already resident on the device: packed bf16 NHWC activations + int64 labels."""
+    """A batch already resident on the device: packed NHWC activations (the engine's storage
+    dtype) + int64 labels."""
 
     act: object
     labels: object
@@ -94,8 +95,9 @@ class DeviceBatch:
         return (int(self.labels.shape[0]),)
 
 
-def to_device_batches(batches, in_shape, device=None, stream=None):
+def to_device_batches(batches, in_shape, device=None, stream=None, precision: str = "bf16"):
     """Pack host batches once into device-resident DeviceBatch objects."""
+    from . import _lib as L
     from .runtime import pack_input, require_cuda, torch_mod
 
     torch = torch_mod()
@@ -103,7 +105,7 @@ def to_device_batches(batches, in_shape, device=None, stream=None):
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     out = []
     for x, lab in batches:
-        act = pack_input(np.asarray(x), tuple(in_shape), dev, st)
+        act = pack_input(np.asarray(x), tuple(in_shape), dev, st, dtype=L.storage_dtype(precision))
         with torch.cuda.stream(st):
             labd = torch.from_numpy(np.asarray(lab, dtype=np.int64)).to(dev)
         out.append(DeviceBatch(act, labd))
@@ -112,9 +114,9 @@ def to_device_batches(batches, in_shape, device=None, stream=None):
 
 
 def device_synthetic_batches(n_batches: int, batch: int, in_shape, num_classes: int, seed: int = 0, device=None,
-                             stream=None):
+                             stream=None, precision: str = "bf16"):
     """``to_device_batches(synthetic_batches(...))`` generated on the device (csrc/synth.cu): the
-    counter-based stream is evaluated per element straight into packed bf16 slots, no host
+    counter-based stream is evaluated per element straight into packed storage-dtype slots, no host
     arrays and no H2D copies."""
     import ctypes as C
 
@@ -127,12 +129,13 @@ def device_synthetic_batches(n_batches: int, batch: int, in_shape, num_classes: 
     c, h, w = (tuple(in_shape) + (1, 1))[:3] if len(in_shape) < 3 else tuple(in_shape)
     cp = (c + 7) // 8 * 8
     lib = L.load()
+    dt = L.storage_dtype(precision)
     out = []
     for i in range(n_batches):
         with torch.cuda.stream(st):
-            act = torch.empty(batch * h * w * cp, dtype=torch.bfloat16, device=dev)
+            act = torch.empty(batch * h * w * cp, dtype=L.torch_storage(dt), device=dev)
             lab = torch.empty(batch, dtype=torch.int64, device=dev)
-        L.check(lib.dsp_synth_batch(seed & ((1 << 64) - 1), i, batch, c, h, w, cp, num_classes, L.DSP_DTYPE_BF16,
+        L.check(lib.dsp_synth_batch(seed & ((1 << 64) - 1), i, batch, c, h, w, cp, num_classes, dt,
                                     ptr(act), C.cast(ptr(lab), C.POINTER(C.c_int64)), stream_ptr(st)))
         out.append(DeviceBatch(act, lab))
     return out

@@ -49,21 +49,19 @@ class DeviationSample:
 class DeviceOperators:
     """bp_gradient / stale_gradient / grad_deviation on device block executors."""
 
-    def __init__(self, model, batch: int, device=None, stream=None):
+    def __init__(self, model, batch: int, device=None, stream=None, dtype: int = 0):
         torch = torch_mod()
         self.torch = torch
         self.model = model
         self.K = model.k
         self.B = batch
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
-        self.blocks = [DeviceBlock(blk, batch, is_last=(k == self.K - 1), device=device, stream=self.stream)
-                       for k, blk in enumerate(model.blocks)]
+        self.blocks = [DeviceBlock(blk, batch, is_last=(k == self.K - 1), device=device, stream=self.stream,
+                                   dtype=dtype) for k, blk in enumerate(model.blocks)]
         self.n = [blk.param_count for blk in model.blocks]
         with torch.cuda.stream(self.stream):
-            self.inputs = [None] + [torch.empty(db.in_elems, dtype=torch.bfloat16, device=db.device)
-                                    for db in self.blocks[1:]]
-            self.gins = [None] + [torch.empty(db.in_elems, dtype=torch.bfloat16, device=db.device)
-                                  for db in self.blocks[1:]]
+            self.inputs = [None] + [db.new_activation(db.in_elems) for db in self.blocks[1:]]
+            self.gins = [None] + [db.new_activation(db.in_elems) for db in self.blocks[1:]]
             self.loss = torch.zeros(1, device=self.blocks[0].device)
 
     def _load(self, params):
@@ -144,12 +142,12 @@ class DeviationTracker:
     (forward-time parameters) and when it backward-processes it (backward-time parameters,
     runtime gradient, upstream norm); the last block's backward covers both."""
 
-    def __init__(self, every: int, model, batch: int, device=None, stream=None):
+    def __init__(self, every: int, model, batch: int, device=None, stream=None, dtype: int = 0):
         if every <= 0:
             raise ValueError("sampling interval must be positive")
         self.every = every
         self.K = model.k
-        self.ops = DeviceOperators(model, batch, device=device, stream=stream)
+        self.ops = DeviceOperators(model, batch, device=device, stream=stream, dtype=dtype)
         self.torch = self.ops.torch
         self._pending = {}
         self._rows = []

@@ -72,9 +72,13 @@ class B200Runtime:
     LOG_CHUNK = 4096
 
     def __init__(self, model, local, batch: int, rule: str = "sgd", beta: float = 0.0, s: float = 1.0,
-                 weight_decay: float = 0.0, device=None, config=None, use_graphs: bool = True):
+                 weight_decay: float = 0.0, device=None, config=None, use_graphs: bool = True,
+                 precision: str = "bf16"):
         torch = torch_mod()
         self.torch = torch
+        self.precision = precision
+        self.dtype_code = L.storage_dtype(precision)
+        self.act_dtype = L.torch_storage(self.dtype_code)
         self.device = require_cuda(device)
         self.stream = torch.cuda.current_stream(self.device)
         self.model = model
@@ -92,7 +96,8 @@ class B200Runtime:
         self.adam = OptimizerState(rule="adam")  # Adam hyper-parameters (extension; defaults of the oracle)
         for k in self.local:
             blk = model.blocks[k]
-            db = DeviceBlock(blk, batch, is_last=(k == self.K - 1), device=self.device, stream=self.stream)
+            db = DeviceBlock(blk, batch, is_last=(k == self.K - 1), device=self.device, stream=self.stream,
+                             dtype=self.dtype_code)
             blk.dev = db
             self.dev[k] = db
             if rule == "sum":
@@ -146,7 +151,7 @@ class B200Runtime:
     # ---------------------------------------------------------------- buffers
     def _empty(self, n, dtype=None, zero=False):
         torch = self.torch
-        dtype = dtype or torch.bfloat16
+        dtype = dtype or self.act_dtype
         with torch.cuda.stream(self.stream):
             return (torch.zeros if zero else torch.empty)(max(n, 1), dtype=dtype, device=self.device)
 
@@ -188,6 +193,9 @@ class B200Runtime:
         slot = n % self.R
         act, lab = self.ring_in[slot], self.ring_lab[slot]
         if isinstance(x, DeviceBatch):
+            if x.act.dtype != self.act_dtype:
+                raise ValueError(f"device batch holds {x.act.dtype}, engine precision {self.precision!r} stores "
+                                 f"{self.act_dtype}")
             if self.mode == "eager":
                 self._copy_device_batch(x, slot, self._s(0))
             else:  # graph steps copy the batch in right before the launch
@@ -242,7 +250,7 @@ class B200Runtime:
             xd.copy_(xs.view(-1), non_blocking=True)
             self.ring_lab[slot].copy_(ls, non_blocking=True)
         L.check(L.load().dsp_pack_input(ptr(xd), ptr(self.ring_in[slot]), self.B, c, h, w, _pad8(c),
-                                        L.DSP_DTYPE_BF16, 1, stream_ptr(stream)))
+                                        self.dtype_code, 1, stream_ptr(stream)))
         ev = self._pinned.get(("ev", slot)) or torch.cuda.Event()
         ev.record(stream)
         self._pinned[("ev", slot)] = ev
@@ -460,6 +468,22 @@ class B200Runtime:
 
     def synchronize(self) -> None:
         self.stream.synchronize()
+        self.check_finite()
+
+    def check_finite(self) -> None:
+        """The reference raises NonFiniteError inside the step (tensor.py:34-37, optim.py:53 / 89);
+        the device sets sticky per-block flags (dsp_block_nonfinite) that every sync point checks."""
+        lib = L.load()
+        for k in self.local:
+            f = C.c_int(0)
+            L.check(lib.dsp_block_nonfinite(self.dev[k].h, 0, C.byref(f), stream_ptr(self.stream)))
+            if f.value:
+                from .optim import NonFiniteError
+
+                if f.value & L.DSP_NONFINITE_LOSS:
+                    raise NonFiniteError(f"non-finite values in softmax_xent (block {k})")
+                step = {"sgd": "sgd_step", "sum": "sum_step"}.get(self.rule, "update")
+                raise NonFiniteError(f"non-finite gradient in {step} (block {k})")
 
     def _value(self, h, host_chunks):
         _, n, k, which = h
@@ -467,6 +491,7 @@ class B200Runtime:
         return float(host_chunks[row // self.LOG_CHUNK][((row % self.LOG_CHUNK) * self.K + k) * 2 + which])
 
     def read_scalar(self, h) -> float:
+        self.synchronize()
         _, n, k, which = h
         row = self._row_of_step.get(n)
         if row is None:  # not yet copied into the log: read the live slot
@@ -476,7 +501,7 @@ class B200Runtime:
         return float(c[i:i + 1].item())
 
     def read_scalars(self, pairs):
-        self.stream.synchronize()
+        self.synchronize()
         host = [c.cpu().numpy() for c in self._log]
         return [(None if lh is None else self._value(lh, host), self._value(gh, host)) for lh, gh in pairs]
 
@@ -487,12 +512,14 @@ def eval_forward(model, x: np.ndarray) -> np.ndarray:
     device = require_cuda()
     stream = torch.cuda.current_stream(device)
     B = x.shape[0]
-    h = pack_input(np.asarray(x), model.blocks[0].in_shape, device, stream)
+    bound = [blk.dev for blk in model.blocks if blk.dev is not None]
+    dtype = bound[0].dtype if bound else L.DSP_DTYPE_BF16
+    h = pack_input(np.asarray(x), model.blocks[0].in_shape, device, stream, dtype=dtype)
     K = model.k
     for k, blk in enumerate(model.blocks):
         db = blk.dev
-        if db is None or db.batch != B:
-            db = DeviceBlock(blk, B, is_last=(k == K - 1), device=device, stream=stream)
+        if db is None or db.batch != B or db.dtype != dtype:
+            db = DeviceBlock(blk, B, is_last=(k == K - 1), device=device, stream=stream, dtype=dtype)
         if k < K - 1:
             y = db.new_activation(db.out_elems)
             db.forward(h, y, record=False, stream=stream)

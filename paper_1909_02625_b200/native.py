@@ -23,7 +23,7 @@ from .pipeline import LogRecord, PipelineConfig, TrainLog
 class NativeEngine:
     def __init__(self, model, config: PipelineConfig, batch: int, schedule: LrSchedule, rule: str = "sgd",
                  beta: float = 0.0, s: float = 1.0, weight_decay: float = 0.0, use_graphs: bool = True,
-                 device: int = 0):
+                 device: int = 0, precision: str = "bf16"):
         lib = L.load()
         self.lib = lib
         self.model = model
@@ -40,7 +40,7 @@ class NativeEngine:
             cfg.p[k], cfg.m[k] = config.p[k], config.m[k]
         cfg.warmup = L.DSP_WARMUP_DISCARD if config.warmup == "discard_warmup_updates" else L.DSP_WARMUP_FAITHFUL
         cfg.batch = batch
-        cfg.dtype = L.DSP_DTYPE_BF16
+        cfg.dtype = L.storage_dtype(precision)
         c, h, w = model.blocks[0].in_shape
         cfg.in_c, cfg.in_h, cfg.in_w = c, h, w
         cfg.num_classes = model.output_dim

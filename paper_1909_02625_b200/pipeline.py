@@ -256,7 +256,8 @@ class TrainEngine:
     def __init__(self, model: Model, config: PipelineConfig, data_stream: Iterator, schedule: LrSchedule,
                  rule: str = "sgd", beta: float = 0.0, s: float = 1.0, weight_decay: float = 0.0,
                  backend: str = "b200", deviation_every: int = 0, straggler: RuntimeStraggler | None = None,
-                 watchdog_s: float = 120.0, placement=None, device=None, _runtime=None, _transport=None):
+                 watchdog_s: float = 120.0, placement=None, device=None, precision: str = "bf16", _runtime=None,
+                 _transport=None):
         if config.k != model.k:
             raise ConfigError("k", 0, f"config K={config.k} but model has {model.k} blocks")
         if backend not in BACKENDS:
@@ -303,7 +304,7 @@ class TrainEngine:
             from .engine_b200 import B200Runtime
 
             _runtime = B200Runtime(model, self.local, self.batch_size, rule=rule, beta=beta, s=s, config=config,
-                                   weight_decay=weight_decay, device=device)
+                                   weight_decay=weight_decay, device=device, precision=precision)
         self.rt = _runtime
 
         # queues: a FIFO lives on the consumer's rank (pipeline.py:483-513)
@@ -343,7 +344,7 @@ class TrainEngine:
             from .deviation import DeviationTracker
 
             self.tracker = DeviationTracker(deviation_every, model, self.batch_size, device=self.rt.device,
-                                            stream=self.rt.stream)
+                                            stream=self.rt.stream, dtype=getattr(self.rt, "dtype_code", 0))
             self.rt.eager_concurrent = False  # snapshots are taken on the main stream
 
         self.opt_states = [self.rt.opt_state(k) if k in self.local else None for k in range(K)]
@@ -476,7 +477,13 @@ class TrainEngine:
                 bufs.append((src, self.rt.empty_act_header(), self.rt.empty_act(k + 1)))
             else:
                 bufs.append((src, self.rt.empty_grad_header(), self.rt.empty_grad(k)))
-        self._transport.exchange(sends, bufs)
+        try:
+            self._transport.exchange(sends, bufs, timeout_s=self.watchdog_s)
+        except TimeoutError as exc:  # the reference's watchdog (pipeline.py:644-657)
+            occupancy = {q.name: len(q) for q in self.out_queues if q is not None}
+            occupancy.update({q.name: len(q) for q in self.grad_queues[1:] if q is not None})
+            raise DeadlockError(f"workers stalled after {self.watchdog_s}s; queue occupancy {occupancy} "
+                                f"steps {self.block_steps}") from exc
         for (kind, k, _), (_, hdr, ten) in zip(recvs, bufs):
             if kind == "act":
                 tag, labels = self.rt.parse_act_header(hdr)
@@ -505,7 +512,15 @@ class TrainEngine:
         if fork is not None:
             fork()
         for k in self.local:
-            self._iterate_block(k)
+            if self._transport.world <= 1:
+                self._iterate_block(k)
+                continue
+            try:  # one process per GPU stands in for the reference's worker threads (pipeline.py:658-660)
+                self._iterate_block(k)
+            except (DeadlockError, ProtocolError, ConfigError):
+                raise
+            except Exception as exc:
+                raise RuntimeError(f"worker for block {k} failed") from exc
         join = getattr(self.rt, "join_blocks", None)
         if join is not None:
             join()

@@ -45,17 +45,18 @@ class DeviceBlock:
     """Owns a planned block, its workspace, fp32 params / grads (and the
     optimizer's ys vector when the SUM rule is used)."""
 
-    def __init__(self, block, batch: int, is_last: bool, device=None, stream=None):
+    def __init__(self, block, batch: int, is_last: bool, device=None, stream=None, dtype: int = L.DSP_DTYPE_BF16):
         torch = torch_mod()
         self.device = require_cuda(device)
         self.lib = L.load()
+        self.dtype = dtype
         self.block = block
         self.batch = batch
         self.is_last = is_last
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         descs = block.layer_descs()
         h = C.c_void_p()
-        L.check(self.lib.dsp_block_create(descs, len(descs), batch, L.DSP_DTYPE_BF16, int(is_last), C.byref(h)))
+        L.check(self.lib.dsp_block_create(descs, len(descs), batch, dtype, int(is_last), C.byref(h)))
         self.h = h
         self.ws_bytes = int(self.lib.dsp_block_workspace_bytes(h))
         self.in_elems = int(self.lib.dsp_block_in_elems(h))
@@ -77,10 +78,11 @@ class DeviceBlock:
         torch = torch_mod()
         tw = DeviceBlock.__new__(DeviceBlock)
         tw.device, tw.lib, tw.block, tw.batch, tw.is_last = self.device, self.lib, self.block, self.batch, False
+        tw.dtype = self.dtype
         tw.stream = self.stream
         descs = self.block.layer_descs()
         h = C.c_void_p()
-        L.check(self.lib.dsp_block_create(descs, len(descs), self.batch, L.DSP_DTYPE_BF16, 0, C.byref(h)))
+        L.check(self.lib.dsp_block_create(descs, len(descs), self.batch, self.dtype, 0, C.byref(h)))
         tw.h = h
         tw.ws_bytes = int(self.lib.dsp_block_workspace_bytes(h))
         tw.in_elems, tw.out_elems = self.in_elems, self.out_elems
@@ -115,10 +117,11 @@ class DeviceBlock:
     # ---- step pieces --------------------------------------------------------
     def new_activation(self, n_elems: int, zero: bool = False):
         torch = torch_mod()
+        dt = L.torch_storage(self.dtype)
         with torch.cuda.stream(self.stream):
             if zero:
-                return torch.zeros(n_elems, dtype=torch.bfloat16, device=self.device)
-            return torch.empty(n_elems, dtype=torch.bfloat16, device=self.device)
+                return torch.zeros(n_elems, dtype=dt, device=self.device)
+            return torch.empty(n_elems, dtype=dt, device=self.device)
 
     def forward(self, x, y=None, record: bool = False, stream=None) -> None:
         st = stream_ptr(stream or self.stream)
@@ -143,8 +146,8 @@ class DeviceBlock:
                                                C.c_double(eps), C.c_double(wd), int(apply), ptr(grad_sq_out),
                                                stream_ptr(stream or self.stream)))
 
-def pack_input(x_host: np.ndarray, shape: tuple, device, stream):
-    """Host float batch (B, C*H*W) in (C,H,W) order -> padded NHWC bf16 device packet."""
+def pack_input(x_host: np.ndarray, shape: tuple, device, stream, dtype: int = L.DSP_DTYPE_BF16):
+    """Host float batch (B, C*H*W) in (C,H,W) order -> padded NHWC device packet (storage dtype)."""
     torch = torch_mod()
     lib = L.load()
     B = x_host.shape[0]
@@ -153,13 +156,13 @@ def pack_input(x_host: np.ndarray, shape: tuple, device, stream):
     with torch.cuda.stream(stream):
         src = torch.from_numpy(np.ascontiguousarray(x_host, dtype=np.float32)).pin_memory()
         dev = src.to(device, non_blocking=True)
-        out = torch.empty(B * h * w * cp, dtype=torch.bfloat16, device=device)
-    L.check(lib.dsp_pack_input(ptr(dev), ptr(out), B, c, h, w, cp, L.DSP_DTYPE_BF16, 1, stream_ptr(stream)))
+        out = torch.empty(B * h * w * cp, dtype=L.torch_storage(dtype), device=device)
+    L.check(lib.dsp_pack_input(ptr(dev), ptr(out), B, c, h, w, cp, dtype, 1, stream_ptr(stream)))
     dev.record_stream(stream)
     return out
 
 
-def unpack_output(t, batch: int, shape: tuple, stream) -> np.ndarray:
+def unpack_output(t, batch: int, shape: tuple, stream, dtype: int = L.DSP_DTYPE_BF16) -> np.ndarray:
     """Padded NHWC device tensor -> host float64 (B, C*H*W) in (C,H,W) order."""
     torch = torch_mod()
     lib = L.load()
@@ -167,6 +170,6 @@ def unpack_output(t, batch: int, shape: tuple, stream) -> np.ndarray:
     cp = (c + 7) // 8 * 8
     with torch.cuda.stream(stream):
         out = torch.empty(batch * c * h * w, dtype=torch.float32, device=t.device)
-    L.check(lib.dsp_unpack_output(ptr(t), ptr(out), batch, c, h, w, cp, L.DSP_DTYPE_BF16, 1, stream_ptr(stream)))
+    L.check(lib.dsp_unpack_output(ptr(t), ptr(out), batch, c, h, w, cp, dtype, 1, stream_ptr(stream)))
     stream.synchronize()
     return out.double().cpu().numpy().reshape(batch, c * h * w)

@@ -11,12 +11,14 @@ re-checks the reference's gradient-meets-activation assertion.
 
 from __future__ import annotations
 
+import time
+
 
 class LocalTransport:
     rank = 0
     world = 1
 
-    def exchange(self, sends, recvs) -> None:
+    def exchange(self, sends, recvs, timeout_s=None) -> None:
         if sends or recvs:
             raise RuntimeError("single-process transport cannot exchange packets")
 
@@ -32,11 +34,13 @@ class TorchDistTransport:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def exchange(self, sends, recvs) -> None:
+    def exchange(self, sends, recvs, timeout_s: float | None = None) -> None:
         """sends: [(dst, header, tensor)], recvs: [(src, header_buf, tensor_buf)].
 
         Messages between one (src, dst) pair are matched in list order on both
-        sides; the engine builds both lists edge by edge in ascending order."""
+        sides; the engine builds both lists edge by edge in ascending order.
+        timeout_s: the watchdog (pipeline.py:644-657) -- raise TimeoutError if the
+        requests have not completed by then (a stalled or dead peer)."""
         dist = self.dist
         ops = []
         for dst, hdr, ten in sends:
@@ -47,8 +51,35 @@ class TorchDistTransport:
             ops.append(dist.P2POp(dist.irecv, ten, src, self.group))
         if not ops:
             return
-        for req in dist.batch_isend_irecv(ops):
+        reqs = dist.batch_isend_irecv(ops)
+        if timeout_s is None:
+            for req in reqs:
+                req.wait()
+            return
+        deadline = time.monotonic() + timeout_s
+        if dist.get_backend(self.group) == "gloo":
+            # gloo completes a request inside wait(); its timeout raises (RuntimeError "Timed out")
+            from datetime import timedelta
+
+            for i, req in enumerate(reqs):
+                left = deadline - time.monotonic()
+                try:
+                    req.wait(timeout=timedelta(seconds=max(left, 1e-3)))
+                except RuntimeError as exc:
+                    if time.monotonic() < deadline and "imed out" not in str(exc):
+                        raise
+                    raise TimeoutError(f"{len(reqs) - i} of {len(reqs)} transfers pending after {timeout_s}s") from exc
+            return
+        # NCCL: wait() only orders the current stream after the transfer; poll its completion event
+        pending = list(reqs)
+        for req in pending:
             req.wait()
+        while pending:
+            pending = [r for r in pending if not r.is_completed()]
+            if pending:
+                if time.monotonic() > deadline:
+                    raise TimeoutError(f"{len(pending)} of {len(reqs)} transfers pending after {timeout_s}s")
+                time.sleep(2e-4)
 
 
 def default_transport():

@@ -157,3 +157,53 @@ def test_two_rank_pipeline_bitwise_vs_single_process(placement, layers_name):
     assert recs == want
     for k in range(4):
         assert np.array_equal(params[k], om_ref.blocks[k].params)
+
+
+def _stall_worker(rank, world, port, out_dir):
+    """Rank 1 never reaches the exchange within the watchdog: rank 0 must raise DeadlockError
+    with the reference's message (pipeline.py:644-657), not hang."""
+    import time
+
+    import torch.distributed as dist
+
+    from paper_1909_02625_b200.transport import TorchDistTransport
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    layers = _layers()
+    pool = R.synthetic_batches(5, 6, (12, 1, 1), 4, seed=3)
+    placement = [0, 0, 1, 1]
+    local = [k for k, r in enumerate(placement) if r == rank]
+    cfg = ((1, 1, 1, 0), (6, 4, 2, 0), "faithful_zero_updates")
+    eng, _ = _engine(layers, [2, 4, 6], cfg, pool, 20, placement=placement, transport=TorchDistTransport(),
+                     local=local, rule="sgd", watchdog_s=1.0)
+    if rank == 1:
+        time.sleep(4.0)
+        with open(os.path.join(out_dir, "rank1.txt"), "w") as f:
+            f.write("slept")
+        os._exit(0)  # a dead peer
+    try:
+        eng.run(2)
+        res = "no error"
+    except P.DeadlockError as e:
+        res = "DeadlockError: " + str(e)
+    with open(os.path.join(out_dir, "rank0.txt"), "w") as f:
+        f.write(res)
+    os._exit(0)
+
+
+def test_two_rank_watchdog_raises_deadlock_error():
+    with tempfile.TemporaryDirectory() as d:
+        ctx = mp.get_context("spawn")
+        port = _free_port()
+        procs = [ctx.Process(target=_stall_worker, args=(r, 2, port, d)) for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(60)
+            if p.is_alive():
+                p.kill()
+        res = open(os.path.join(d, "rank0.txt")).read()
+    assert res.startswith("DeadlockError: workers stalled after 1.0s; queue occupancy"), res
+    assert "steps" in res

@@ -224,3 +224,45 @@ def test_forward_twin_is_bitwise_neutral(monkeypatch):
     assert runs[0][0] == runs[1][0]
     for a, b in zip(runs[0][1], runs[1][1]):
         assert np.array_equal(a, b)
+
+
+def _nan_model(layers, boundaries, block, seed=1):
+    pm, _ = twin_models(layers, boundaries, seed=seed)
+    p = pm.blocks[block].params.copy()
+    p[len(p) // 2] = np.nan
+    pm.blocks[block].params = p
+    return pm
+
+
+@pytest.mark.parametrize("block", [0, 1])
+def test_nonfinite_gradient_raises(block):
+    """NonFiniteError (optim.py:53 / 89, tensor.py:101-111): a NaN parameter poisons the step; the
+    device's sticky flag is raised at the next sync point (the log read)."""
+    layers = small_resnet(in_shape=(3, 8, 8))
+    pm = _nan_model(layers, [2], block)
+    pool = R.synthetic_batches(3, 8, (3, 8, 8), 10, seed=1)
+    eng = P.TrainEngine(pm, P.validate_config((1, 0), (2, 0)), R.cycle(pool), P.LrSchedule(0.05), rule="sum",
+                        beta=0.9)
+    eng.run(4)
+    with pytest.raises(P.NonFiniteError, match="non-finite"):
+        _ = eng.log
+
+
+def test_nonfinite_native_engine_raises():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    pm = _nan_model(layers, [2], 1)
+    pool = R.synthetic_batches(3, 8, (3, 8, 8), 10, seed=1)
+    eng = P.NativeEngine(pm, P.validate_config((1, 0), (2, 0)), 8, P.LrSchedule(0.05), rule="sum", beta=0.9)
+    with pytest.raises(P.NonFiniteError, match="non-finite"):
+        eng.run(4, R.cycle(pool))
+
+
+def test_finite_run_does_not_raise():
+    layers = small_resnet(in_shape=(3, 8, 8))
+    pm, _ = twin_models(layers, [2], seed=1)
+    pool = R.synthetic_batches(3, 8, (3, 8, 8), 10, seed=1)
+    eng = P.TrainEngine(pm, P.validate_config((1, 0), (2, 0)), R.cycle(pool), P.LrSchedule(0.05), rule="sum",
+                        beta=0.9)
+    eng.run(6)
+    eng.synchronize()
+    assert all(np.isfinite(r.grad_norm) for r in eng.log.records)

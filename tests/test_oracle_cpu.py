@@ -69,6 +69,39 @@ def test_oracle_cnn_matches_reference_engine_driven_run():
     assert np.array_equal(om.flat_params(), g["final"])
 
 
+def test_oracle_engine_reproduces_baseline_config0_golden():
+    """c1_resnet20_k2.npz = BASELINE configs[0] (ResNet-20 w16, K=2, B=32, SUM 0.9, 24 steps)
+    through the reference TrainEngine driving the oracle CNN math; the oracle's own engine gives
+    the identical schedule and checksum, and the product's layer builder / cuts / init give the
+    same model (so the GPU tests of tests/test_configs_gpu.py compare like with like)."""
+    from oracle.make_golden import CONFIGS, resnet_cifar_oracle_layers
+
+    import paper_1909_02625_b200 as P
+
+    g = _gold("c1_resnet20_k2")
+    c = CONFIGS["c1_resnet20_k2"]
+    lay = resnet_cifar_oracle_layers(R, c["depth"], c["width"], c["classes"])
+    play = P.resnet_cifar_layers(c["depth"], c["classes"], width=c["width"])
+    assert [(s.kind, tuple(s.in_shape), s.out_c, s.stride) for s in lay] == \
+        [(s.kind, tuple(s.in_shape), s.out_c, s.stride) for s in play]
+    assert P.flop_balanced_boundaries(play, 2) == c["boundaries"] == list(g["boundaries"])
+    om = R.build_model(lay, c["boundaries"])
+    R.init_params(om, c["init_seed"])
+    pm = P.build_model(play, c["boundaries"])
+    P.init_params(pm, c["init_seed"])
+    assert np.array_equal(om.flat_params(), pm.flat_params())
+    assert np.linalg.norm(om.flat_params()) == float(g["init_norm"])
+    pool = R.synthetic_batches(c["pool"], c["batch"], (3, 32, 32), c["classes"], seed=c["data_seed"])
+    eng = R.Engine(om, R.validate_config(c["p"], c["m"]), R.cycle(pool), R.LrSchedule(c["lr"], c["decays"]),
+                   rule="sum", beta=c["beta"], s=c["s"], weight_decay=c["wd"])
+    eng.run(c["steps"])
+    assert eng.checksum() == str(g["checksum"])
+    st = int(g["stride"])
+    for k, b in enumerate(om.blocks):
+        assert np.array_equal(b.params[::st], g[f"final_{k}"])
+    assert eng.realized_staleness() == list(g["staleness"])
+
+
 def test_optimizer_and_rng_kats():
     k = _gold("kats")
     xs = k["x0"].copy()
