@@ -33,6 +33,11 @@ inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 struct ConvP {
   dsp_conv_geom_t g;
   int ci_real = 0, co_real = 0;
+  // space-to-depth stem (s2d_r > 0): a stride-2 R x R conv on <= 4 channels runs as the stride-1
+  // ((R+1)/2)^2-tap conv over the 2x2 space-to-depth input (4x the channels, 16-channel TMA boxes
+  // instead of 8, (R+1)^2 / R^2 of the padded MACs); g describes that conv, these the original
+  int s2d_r = 0, s2d_ci = 0, s2d_h = 0, s2d_w = 0, s2d_cpx = 0, s2d_pad = 0;
+  size_t s2d_buf = 0;  // the s2d input (forward, WGRAD) / its gradient (DGRAD) in the workspace
   int64_t w_off = 0, gamma_off = 0, beta_off = 0;  // floats, into block params
   int64_t wpack = 0;                               // elements, into packed weights
   int64_t wpack_t = -1;                            // transposed pack [Cin_p][R][S][Cout_p] (stride-1 convs)
@@ -67,7 +72,7 @@ struct dsp_block {
   size_t ws_bytes = 0;
   size_t S[4] = {0, 0, 0, 0};
   size_t G[2] = {0, 0};
-  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0, sem = 0, usem = 0, nf = 0;
+  size_t fpart = 0, bpart = 0, bpart2 = 0, wpart = 0, upart = 0, sem = 0, usem = 0, nf = 0, lsem = 0, rowloss = 0;
   size_t packed = 0, ptable = 0, utable = 0;
   std::vector<dsp::PackEntry> packs;
   std::vector<dsp::UpdTile> utiles;  // fused update + repack tile table (elementwise.cu update_pack)
@@ -163,7 +168,32 @@ int build_update_tiles(dsp_block* b) {
   };
   for (const PackEntry& e : b->packs) {
     if (e.dense_src == 2) continue;  // folded into its conv's tiles below
-    if (e.dense_src == 0) {
+    if (e.dense_src == 0 && e.s2d_r > 0) {  // space-to-depth stem: per original tap (r, s) = (2a+i, 2b+j)
+      int64_t dst_t = -1;
+      for (const PackEntry& t : b->packs)
+        if (t.dense_src == 2 && t.src_off == e.src_off) dst_t = t.dst_off;
+      const int R = e.s2d_r, rs2 = (R + 1) / 2;
+      for (int tap = 0; tap < R * R; ++tap) {
+        const int r = tap / R, sx = tap % R;
+        const int tp = (r / 2) * rs2 + sx / 2, sub = (r & 1) * 2 + (sx & 1);
+        for (int co0 = 0; co0 < e.co; co0 += 32)
+          for (int ci0 = 0; ci0 < e.ci; ci0 += 32) {
+            UpdTile u{};
+            u.rows = std::min(32, e.co - co0);
+            u.cols = std::min(32, e.ci - ci0);
+            u.src = e.src_off + ((int64_t)co0 * R * R + tap) * e.ci + ci0;
+            u.src_rs = R * R * e.ci;
+            u.dst_a = e.dst_off + ((int64_t)co0 * e.rs + tp) * e.cip + sub * e.ci + ci0;
+            u.dst_a_rs = e.rs * e.cip;
+            u.dst_b = dst_t < 0 ? -1 : dst_t + ((int64_t)(sub * e.ci + ci0) * e.rs + tp) * e.cop + co0;
+            u.dst_b_cs = e.rs * e.cop;
+            for (int rr = 0; rr < u.rows; ++rr)
+              for (int cc = 0; cc < u.cols; ++cc)
+                if (!mark(u.src + (int64_t)rr * u.src_rs + cc)) return set_error(DSP_E_INVALID, "update tiles overlap");
+            b->utiles.push_back(u);
+          }
+      }
+    } else if (e.dense_src == 0) {
       int64_t dst_t = -1;
       for (const PackEntry& t : b->packs)
         if (t.dense_src == 2 && t.src_off == e.src_off) dst_t = t.dst_off;
@@ -254,8 +284,8 @@ int conv_wgrad(dsp_block* b, const ConvP& c, const void* x, const void* dy, cuda
   const int splits = wgrad_splits(c, &kb, b->dtype);
   a.kb_per_split = kb;
   DSP_CUDA(igemm_launch(DSP_IGEMM_WGRAD, b->dtype, a, splits, st));
-  DSP_CUDA(wgrad_reduce(at<float>(b, b->wpart), splits, a.M, a.N, c.g.R * c.g.S, c.g.C, c.ci_real, c.co_real, 0,
-                        b->grads + c.w_off, st));
+  DSP_CUDA(wgrad_reduce(at<float>(b, b->wpart), splits, a.M, a.N, c.g.R * c.g.S, c.g.C, c.s2d_r ? c.s2d_ci : c.ci_real,
+                        c.co_real, c.s2d_r ? 2 : 0, b->grads + c.w_off, st, c.s2d_r));
   return DSP_OK;
 }
 
@@ -376,10 +406,15 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
       DSP_CUDA(avgpool_forward(dt, x, out, b->B, l.in_h * l.in_w, l.in_cp, st));
       return DSP_OK;
     case DSP_LAYER_MAXPOOL:
-      DSP_CUDA(maxpool_forward(dt, x, out, at<int32_t>(b, l.arg), b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
+      DSP_CUDA(maxpool_forward(dt, x, out, at<uint8_t>(b, l.arg), b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
       return DSP_OK;
     case DSP_LAYER_CONV_BN_RELU: {
       const ConvP& c = l.convs[0];
+      if (c.s2d_r) {
+        DSP_CUDA(s2d_pack(dt, x, b->ws + c.s2d_buf, b->B, c.s2d_h, c.s2d_w, c.s2d_ci, c.s2d_cpx, c.g.H, c.g.W, c.g.C,
+                          c.s2d_pad, st));
+        x = b->ws + c.s2d_buf;
+      }
       DSP_TRY(conv_fprop(b, c, x, st));
       DSP_CUDA(bn_apply(dt, b->ws + c.y, at<float>(b, c.stat), nullptr, nullptr, nullptr, out, c.M(), c.g.K, 1, st));
       return DSP_OK;
@@ -452,7 +487,7 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
       return DSP_OK;
     case DSP_LAYER_MAXPOOL:
       if (dx)
-        DSP_CUDA(maxpool_backward(dt, u, at<int32_t>(b, l.arg), dx, b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp,
+        DSP_CUDA(maxpool_backward(dt, u, at<uint8_t>(b, l.arg), dx, b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp,
                                   st));
       return DSP_OK;
     case DSP_LAYER_CONV_BN_RELU: {
@@ -462,6 +497,15 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
         DSP_TRY(bn_backward_apply(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
       else
         DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
+      if (c.s2d_r) {  // WGRAD on the recorded s2d input; DGRAD into its gradient, then back to x's layout
+        DSP_TRY(conv_wgrad(b, c, b->ws + c.s2d_buf, dy, st));
+        if (dx) {
+          DSP_TRY(conv_dgrad(b, c, dy, b->ws + c.s2d_buf, nullptr, st));
+          DSP_CUDA(s2d_unpack(dt, b->ws + c.s2d_buf, dx, b->B, c.s2d_h, c.s2d_w, c.s2d_ci, c.s2d_cpx, c.g.H, c.g.W,
+                              c.g.C, c.s2d_pad, st));
+        }
+        return DSP_OK;
+      }
       DSP_TRY(conv_wgrad(b, c, x, dy, st));
       if (dx) DSP_TRY(conv_dgrad(b, c, dy, dx, nullptr, st, below));
       return DSP_OK;
@@ -565,7 +609,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       l.b_off = d.bias ? d.param_offset + (int64_t)d.in_c * d.out_c : -1;
       l.dense.wpack = pack_elems;
       pack_elems += (int64_t)l.dense.g.K * l.dense.g.C;
-      b->packs.push_back({l.dense.w_off, l.dense.wpack, d.out_c, d.in_c, 1, l.dense.g.K, l.dense.g.C, 1});
+      b->packs.push_back({l.dense.w_off, l.dense.wpack, d.out_c, d.in_c, 1, l.dense.g.K, l.dense.g.C, 1, 0, 0});
       l.logits = is_last && i == n_layers - 1;
       cur_c = d.out_c;
       int kb = 1;
@@ -610,9 +654,38 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       };
       if (kind == DSP_LAYER_CONV_BN_RELU) {
         const int k = d.ksize > 0 ? d.ksize : 3;
-        auto g = add_conv(d.in_h, d.in_w, d.in_c, d.out_c, k, d.stride, k / 2);
-        l.out_h = g.P;
-        l.out_w = g.Q;
+        const int pad = k / 2;
+        static const bool no_s2d = getenv("DSP_B200_NO_S2D") != nullptr;
+        const bool s2d = !no_s2d && d.stride == 2 && k >= 5 && (k & 1) && d.in_c <= 4 && (d.in_h + 2 * pad) % 2 == 0 &&
+                         (d.in_w + 2 * pad) % 2 == 0;
+        if (s2d) {
+          const int rs2 = (k + 1) / 2, hs = (d.in_h + 2 * pad) / 2, ws = (d.in_w + 2 * pad) / 2;
+          ConvP c;
+          make_conv(c, B, hs, ws, 4 * d.in_c, d.out_c, rs2, 1, 0);
+          c.s2d_r = k;
+          c.s2d_ci = d.in_c;
+          c.s2d_h = d.in_h;
+          c.s2d_w = d.in_w;
+          c.s2d_cpx = pad8(d.in_c);
+          c.s2d_pad = pad;
+          c.w_off = off;
+          off += (int64_t)d.out_c * k * k * d.in_c;
+          c.gamma_off = off;
+          off += d.out_c;
+          c.beta_off = off;
+          off += d.out_c;
+          c.wpack = pack_elems;
+          pack_elems += (int64_t)c.g.K * rs2 * rs2 * c.g.C;
+          c.wpack_t = pack_elems;
+          pack_elems += (int64_t)c.g.K * rs2 * rs2 * c.g.C;
+          l.convs.push_back(c);
+          l.out_h = c.g.P;
+          l.out_w = c.g.Q;
+        } else {
+          auto g = add_conv(d.in_h, d.in_w, d.in_c, d.out_c, k, d.stride, pad);
+          l.out_h = g.P;
+          l.out_w = g.Q;
+        }
         l.out_real = d.out_c;
       } else if (kind == DSP_LAYER_BASIC_UNIT) {
         auto g1 = add_conv(d.in_h, d.in_w, d.in_c, d.out_c, 3, d.stride, 1);
@@ -659,7 +732,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
   for (int i = 0; i < n_layers; ++i) {
     LayerP& l = b->L[i];
     l.out = pl.take((size_t)l.out_elems() * (l.logits ? 4 : b->esz));
-    if (l.d.kind == DSP_LAYER_MAXPOOL) l.arg = pl.take((size_t)l.out_elems() * 4);
+    if (l.d.kind == DSP_LAYER_MAXPOOL) l.arg = pl.take((size_t)l.out_elems());  // argmax tap bytes
     for (size_t ci = 0; ci < l.convs.size(); ++ci) {
       ConvP& c = l.convs[ci];
       c.y = pl.take((size_t)c.M() * c.g.K * b->esz);
@@ -671,9 +744,11 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       int kb = 1;
       const int sp = wgrad_splits(c, &kb, dtype);
       max_wpart = std::max<int64_t>(max_wpart, (int64_t)sp * c.g.R * c.g.S * c.g.C * c.g.K);
-      b->packs.push_back({c.w_off, c.wpack, c.co_real, c.ci_real, c.g.R * c.g.S, c.g.K, c.g.C, 0});
+      const int pci = c.s2d_r ? c.s2d_ci : c.ci_real;  // the parameter tensor's input channels
+      b->packs.push_back({c.w_off, c.wpack, c.co_real, pci, c.g.R * c.g.S, c.g.K, c.g.C, 0, c.s2d_r, 0});
       if (c.wpack_t >= 0)
-        b->packs.push_back({c.w_off, c.wpack_t, c.co_real, c.ci_real, c.g.R * c.g.S, c.g.K, c.g.C, 2});
+        b->packs.push_back({c.w_off, c.wpack_t, c.co_real, pci, c.g.R * c.g.S, c.g.K, c.g.C, 2, c.s2d_r, 0});
+      if (c.s2d_r) c.s2d_buf = pl.take((size_t)c.Min() * c.g.C * b->esz);
     }
     if (l.d.kind == DSP_LAYER_BASIC_UNIT || l.d.kind == DSP_LAYER_BOTTLENECK) {
       l.z1 = pl.take((size_t)l.convs[0].M() * l.convs[0].g.K * b->esz);
@@ -705,6 +780,8 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
                                       update_pack_grid((int)b->utiles.size())) * 8);
   b->usem = pl.take(256);  // update grad-norm ticket (zeroed at bind, left zero)
   b->nf = pl.take(256);    // sticky non-finite flags (dsp_block_nonfinite)
+  b->lsem = pl.take(256);  // softmax_xent ticket
+  b->rowloss = pl.take((size_t)B * 4);
   b->packed = pl.take((size_t)std::max<int64_t>(pack_elems, 1) * b->esz);
   b->ptable = pl.take(sizeof(PackEntry) * std::max<size_t>(b->packs.size(), 1));
   b->utable = pl.take(sizeof(UpdTile) * std::max<size_t>(b->utiles.size(), 1));
@@ -788,7 +865,7 @@ extern "C" int dsp_block_loss(dsp_block_t* b, const int64_t* labels, float* loss
   if (!labels || !loss) return set_error(DSP_E_INVALID, "dsp_block_loss: null pointer");
   const LayerP& l = b->L.back();
   DSP_CUDA(softmax_xent(b->dtype, at<float>(b, l.out), l.out_cp, b->B, b->classes, labels, b->ws + b->dlogits, loss,
-                        at<int>(b, b->nf), (cudaStream_t)stream));
+                        at<float>(b, b->rowloss), at<int>(b, b->lsem), at<int>(b, b->nf), (cudaStream_t)stream));
   return DSP_OK;
 }
 
@@ -813,7 +890,8 @@ extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* gr
     // the layer below's top BN statistics ride on this layer's final DGRAD (g = dx * (x > 0))
     BnbFuse fz{};
     const BnbFuse* below = nullptr;
-    if (i > 0 && dx != nullptr && has_top_bn(l) && has_top_bn(b->L[i - 1])) {
+    const bool s2d = l.d.kind == DSP_LAYER_CONV_BN_RELU && l.convs[0].s2d_r;  // its dx is unpacked after DGRAD
+    if (i > 0 && dx != nullptr && !s2d && has_top_bn(l) && has_top_bn(b->L[i - 1])) {
       const LayerP& lb = b->L[i - 1];
       const int nmain = lb.d.kind == DSP_LAYER_BOTTLENECK ? 3 : lb.d.kind == DSP_LAYER_BASIC_UNIT ? 2 : 1;
       fz = BnbFuse{x, &lb.convs[nmain - 1], lb.proj ? &lb.convs[nmain] : nullptr};

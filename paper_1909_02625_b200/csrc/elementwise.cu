@@ -614,7 +614,7 @@ __global__ void avgpool_bwd_k(const T* __restrict__ u, T* __restrict__ dx, int B
 // 3x3 / stride-2 / pad-1 max pooling, one thread per 16-byte channel vector of an output pixel;
 // arg = winning tap (0-8, first maximum in tap order) per element, int32.
 template <typename T>
-__global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int32_t* __restrict__ arg, int B, int H,
+__global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, uint8_t* __restrict__ arg, int B, int H,
                               int W, int P, int Q, int Cp) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
@@ -656,14 +656,21 @@ __global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, int3
       }
     }
     st16(out + i * VE, best);
-    int4* ap = reinterpret_cast<int4*>(arg + i * VE);
+    // argmax tap (0..8) as one byte per element (VE bytes per thread)
+    uint32_t packed[VE / 4];
 #pragma unroll
-    for (int e = 0; e < VE; e += 4) ap[e / 4] = make_int4(ba[e], ba[e + 1], ba[e + 2], ba[e + 3]);
+    for (int e = 0; e < VE; e += 4)
+      packed[e / 4] = (uint32_t)ba[e] | ((uint32_t)ba[e + 1] << 8) | ((uint32_t)ba[e + 2] << 16) | ((uint32_t)ba[e + 3] << 24);
+    if constexpr (VE == 8) {
+      *reinterpret_cast<uint2*>(arg + i * VE) = make_uint2(packed[0], packed[1]);
+    } else {
+      *reinterpret_cast<uint32_t*>(arg + i * VE) = packed[0];
+    }
   }
 }
 
 template <typename T>
-__global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict__ arg, T* __restrict__ dx, int B,
+__global__ void maxpool_bwd_k(const T* __restrict__ u, const uint8_t* __restrict__ arg, T* __restrict__ dx, int B,
                               int H, int W, int P, int Q, int Cp) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
@@ -690,31 +697,77 @@ __global__ void maxpool_bwd_k(const T* __restrict__ u, const int32_t* __restrict
         const int64_t o = (((int64_t)b * P + (pp >> 1)) * Q + (qq >> 1)) * Cp + cv * VE;
         float uv[VE];
         cvt16<T>(ldraw(u + o), uv);
-        const int4* ap = reinterpret_cast<const int4*>(arg + o);
-#pragma unroll
-        for (int e = 0; e < VE; e += 4) {
-          const int4 a4 = ap[e / 4];
-          const int k = r * 3 + s2;
-          if (a4.x == k) acc[e] += uv[e];
-          if (a4.y == k) acc[e + 1] += uv[e + 1];
-          if (a4.z == k) acc[e + 2] += uv[e + 2];
-          if (a4.w == k) acc[e + 3] += uv[e + 3];
+        uint32_t a4[VE / 4];
+        if constexpr (VE == 8) {
+          const uint2 a = *reinterpret_cast<const uint2*>(arg + o);
+          a4[0] = a.x;
+          a4[1] = a.y;
+        } else {
+          a4[0] = *reinterpret_cast<const uint32_t*>(arg + o);
         }
+        const uint32_t k = (uint32_t)(r * 3 + s2);
+#pragma unroll
+        for (int e = 0; e < VE; ++e)
+          if (((a4[e / 4] >> (8 * (e & 3))) & 0xffu) == k) acc[e] += uv[e];
       }
     }
     st16(dx + i * VE, acc);
   }
 }
 
+// ------------------------------------------------------------------ space-to-depth stem
+// One thread per s2d pixel: its cps channels = 4 sub-positions (i, j) x c input channels.
+template <typename T>
+__global__ void s2d_pack_k(const T* __restrict__ x, T* __restrict__ s, int B, int H, int W, int c, int cpx, int Hs,
+                           int Ws, int cps, int pad) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  const int64_t n = (int64_t)B * Hs * Ws;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ws = (int)(i % Ws);
+    const int64_t t = i / Ws;
+    const int hs = (int)(t % Hs);
+    const int b = (int)(t / Hs);
+    T* out = s + i * cps;
+    for (int cs = 0; cs < cps; ++cs) {
+      const int sub = cs / c, k = cs % c;
+      float v = 0.f;
+      if (sub < 4) {
+        const int h = 2 * hs + (sub >> 1) - pad, w = 2 * ws + (sub & 1) - pad;
+        if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) v = to_f<T>(x[(((int64_t)b * H + h) * W + w) * cpx + k]);
+      }
+      out[cs] = from_f<T>(v);
+    }
+  }
+}
+
+template <typename T>
+__global__ void s2d_unpack_k(const T* __restrict__ ds, T* __restrict__ dx, int B, int H, int W, int c, int cpx, int Hs,
+                             int Ws, int cps, int pad) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  const int64_t n = (int64_t)B * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int w = (int)(i % W);
+    const int64_t t = i / W;
+    const int h = (int)(t % H);
+    const int b = (int)(t / H);
+    const int hp = h + pad, wp = w + pad;
+    const T* src = ds + (((int64_t)b * Hs + (hp >> 1)) * Ws + (wp >> 1)) * cps + (((hp & 1) * 2 + (wp & 1)) * c);
+    for (int k = 0; k < cpx; ++k) dx[i * cpx + k] = k < c ? src[k] : from_f<T>(0.f);
+  }
+}
+
 // ------------------------------------------------------------------ loss
 template <typename T>
 __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, int C, const int64_t* __restrict__ labels,
-                               T* __restrict__ dlogits, float* __restrict__ loss, int* __restrict__ nf) {
+                               T* __restrict__ dlogits, float* __restrict__ loss, float* __restrict__ row_loss, int* sem,
+                               int* __restrict__ nf) {
+  // one warp per row (8 rows per CTA); the per-row losses are summed in row order by the last
+  // CTA to finish (ticket), so the mean is deterministic
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
-  extern __shared__ float row_loss[];
+  __shared__ int last_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
-  for (int b = warp; b < B; b += nw) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (b < B) {
     const float* z = logits + (size_t)b * ld;
     float mx = -INFINITY;
     for (int c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
@@ -736,20 +789,20 @@ __global__ void softmax_xent_k(const float* __restrict__ logits, int ld, int B, 
     }
     if (lane == 0) row_loss[b] = -((z[lab] - mx) - logf(den));
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (last_cta_ticket(sem, (int)gridDim.x, &last_s) && threadIdx.x == 0) {
     double s = 0.0;
-    for (int b = 0; b < B; ++b) s += (double)row_loss[b];
+    for (int r = 0; r < B; ++r) s += (double)__ldcg(&row_loss[r]);
     const float l = (float)(s / (double)B);
     *loss = l;
     if (nf != nullptr && !isfinite(l)) atomicOr(nf, 1);  // NonFiniteError (tensor.py:101-111)
+    *sem = 0;
   }
 }
 
 // ------------------------------------------------------------------ split-K reduce / packing
 __global__ void __launch_bounds__(256) wgrad_reduce_k(const float* __restrict__ part, int splits, int Mw, int N,
                                                      int RS, int Cp, int ci_real, int co_real, int dense_layout,
-                                                     float* __restrict__ grad) {
+                                                     float* __restrict__ grad, int s2d_r) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   // CTA = 32 consecutive partial elements (coalesced 128 B per split row) x 8 warps; warp w
   // sums the contiguous split range [w*S/8, (w+1)*S/8), 8 loads in flight, then warp 0 adds
@@ -784,9 +837,15 @@ __global__ void __launch_bounds__(256) wgrad_reduce_k(const float* __restrict__ 
   const int m = (int)(idx / N);
   if (n >= co_real) return;
   int64_t dst;
-  if (dense_layout) {
+  if (dense_layout == 1) {
     if (m >= ci_real) return;
     dst = (int64_t)m * co_real + n;
+  } else if (dense_layout == 2) {  // space-to-depth stem
+    const int cs = m % Cp, tap = m / Cp, rs2 = (s2d_r + 1) / 2;
+    const int sub = cs / ci_real, c = cs % ci_real;
+    const int r = 2 * (tap / rs2) + (sub >> 1), s = 2 * (tap % rs2) + (sub & 1);
+    if (sub >= 4 || tap >= RS || r >= s2d_r || s >= s2d_r) return;
+    dst = (((int64_t)n * s2d_r + r) * s2d_r + s) * ci_real + c;
   } else {
     const int ci = m % Cp, tap = m / Cp;
     if (ci >= ci_real || tap >= RS) return;
@@ -816,7 +875,13 @@ __global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__
       co = (int)(t / e.rs);
     }
     float v = 0.f;
-    if (co < e.co && ci < e.ci) {
+    if (e.s2d_r > 0) {  // space-to-depth stem: s2d tap (a, b), channel (i*2 + j)*ci + c
+      const int rs2 = (e.s2d_r + 1) / 2;
+      const int a = tap / rs2, bb = tap % rs2, sub = ci / e.ci, c = ci % e.ci;
+      const int r = 2 * a + (sub >> 1), s = 2 * bb + (sub & 1);
+      if (co < e.co && sub < 4 && r < e.s2d_r && s < e.s2d_r)
+        v = params[e.src_off + (((int64_t)co * e.s2d_r + r) * e.s2d_r + s) * e.ci + c];
+    } else if (co < e.co && ci < e.ci) {
       v = e.dense_src == 1 ? params[e.src_off + (int64_t)ci * e.co + co]
                       : params[e.src_off + ((int64_t)co * e.rs + tap) * e.ci + ci];
     }
@@ -1304,7 +1369,7 @@ cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, 
   });
 }
 
-cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, int B, int H, int W, int P, int Q,
+cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, int B, int H, int W, int P, int Q,
                             int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
@@ -1315,7 +1380,7 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, i
   });
 }
 
-cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void* dx, int B, int H, int W, int P, int Q,
+cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void* dx, int B, int H, int W, int P, int Q,
                              int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
@@ -1327,19 +1392,19 @@ cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void*
 }
 
 cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, const int64_t* labels, void* dlogits,
-                         float* loss, int* nf, cudaStream_t st) {
+                         float* loss, float* row_loss, int* sem, int* nf, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    launch_k(softmax_xent_k<T>, 1, 512, B * sizeof(float), st, logits, ld, B, C, labels, (T*)dlogits, loss, nf);
+    launch_k(softmax_xent_k<T>, (B + 7) / 8, 256, 0, st, logits, ld, B, C, labels, (T*)dlogits, loss, row_loss, sem, nf);
     return note_launch(), cudaGetLastError();
   });
 }
 
 cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
-                         int dense_layout, float* grad, cudaStream_t st) {
+                         int dense_layout, float* grad, cudaStream_t st, int s2d_r) {
   const int64_t total = (int64_t)Mw * N;
   launch_k(wgrad_reduce_k, (unsigned)((total + 31) / 32), 256, 0, st, part, splits, Mw, N, RS, Cp, ci_real, co_real,
-                                                                  dense_layout, grad);
+                                                                  dense_layout, grad, s2d_r);
   return note_launch(), cudaGetLastError();
 }
 
@@ -1350,6 +1415,26 @@ cudaError_t pack_weights(int dtype, const float* params, void* packed, const Pac
     using T = decltype(t);
     dim3 grid(grid_for(max_elems, kThreads, 256), n_entries);
     launch_k(pack_weights_k<T>, grid, kThreads, 0, st, params, (T*)packed, entries_dev, n_entries);
+    return note_launch(), cudaGetLastError();
+  });
+}
+
+cudaError_t s2d_pack(int dtype, const void* x, void* s, int B, int H, int W, int c, int cpx, int Hs, int Ws, int cps,
+                     int pad, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    launch_k(s2d_pack_k<T>, grid_for((int64_t)B * Hs * Ws), kThreads, 0, st, (const T*)x, (T*)s, B, H, W, c, cpx, Hs, Ws,
+             cps, pad);
+    return note_launch(), cudaGetLastError();
+  });
+}
+
+cudaError_t s2d_unpack(int dtype, const void* ds, void* dx, int B, int H, int W, int c, int cpx, int Hs, int Ws, int cps,
+                       int pad, cudaStream_t st) {
+  return dispatch_dtype(dtype, [&](auto t) {
+    using T = decltype(t);
+    launch_k(s2d_unpack_k<T>, grid_for((int64_t)B * H * W), kThreads, 0, st, (const T*)ds, (T*)dx, B, H, W, c, cpx, Hs,
+             Ws, cps, pad);
     return note_launch(), cudaGetLastError();
   });
 }

@@ -57,22 +57,36 @@ cudaError_t avgpool_forward(int dtype, const void* x, void* out, int B, int HW, 
 cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, int Cp, cudaStream_t st);
 
 // 3x3 stride-2 pad-1 max pool and backward (argmax of the first max in (r,s) order).
-cudaError_t maxpool_forward(int dtype, const void* x, void* out, int32_t* arg, int B, int H, int W, int P, int Q,
+// arg: the argmax tap (0..8) of every output element, one byte each.
+cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, int B, int H, int W, int P, int Q,
                             int Cp, cudaStream_t st);
-cudaError_t maxpool_backward(int dtype, const void* u, const int32_t* arg, void* dx, int B, int H, int W, int P,
+cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void* dx, int B, int H, int W, int P,
                              int Q, int Cp, cudaStream_t st);
+
+// Space-to-depth of a stride-2 stem's input (R x R kernel, padding pad): x [B][H][W][cpx] (c real
+// channels) -> s [B][Hs][Ws][cps], s(n, hs, ws, (i*2 + j)*c + k) = x(n, 2hs+i-pad, 2ws+j-pad, k) (0 off
+// the image / past 4c channels); and the gradient's way back (dx from ds, pad channels 0).
+cudaError_t s2d_pack(int dtype, const void* x, void* s, int B, int H, int W, int c, int cpx, int Hs, int Ws, int cps,
+                     int pad, cudaStream_t st);
+cudaError_t s2d_unpack(int dtype, const void* ds, void* dx, int B, int H, int W, int c, int cpx, int Hs, int Ws, int cps,
+                       int pad, cudaStream_t st);
 
 // softmax_xent (tensor.py:86-111) on fp32 logits [B][ld] (C real classes):
 // dlogits (storage dtype, pads zero) and the mean loss into *loss (device).
-// nf (optional): sticky flags, bit 0 set when the loss is not finite (tensor.py:101-111).
+// One warp per row; row_loss: B floats of scratch; sem: a device int, 0 on entry (left 0), the
+// last CTA sums the row losses in order. nf (optional): sticky flags, bit 0 set when the loss is
+// not finite (tensor.py:101-111).
 cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, const int64_t* labels,
-                         void* dlogits, float* loss, int* nf, cudaStream_t st);
+                         void* dlogits, float* loss, float* row_loss, int* sem, int* nf, cudaStream_t st);
 
 // Split-K WGRAD partials [splits][Mw][N] -> flat fp32 weight gradient.
 //  conv  (dense_layout=0): grad[(co*RS + tap)*ci_real + ci] for Mw = RS*Cp rows (tap*Cp + ci)
 //  dense (dense_layout=1): grad[i*out_real + o]   (reference W[in][out] layout)
+// dense_layout 2: the space-to-depth stem (RS = its (R'+1)/2 squared taps, Cp its padded 4*ci_real channels,
+// s2d_r = the original kernel size R'): grad[(co*R' + 2a+i)*R' + 2b+j][c] for s2d (tap (a,b), channel
+// (i*2+j)*ci_real + c).
 cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
-                         int dense_layout, float* grad, cudaStream_t st);
+                         int dense_layout, float* grad, cudaStream_t st, int s2d_r = 0);
 
 // Weight shadow packing: fp32 params -> storage dtype [cop][RS][cip] (zero pads).
 // dense_src=1: source is the reference W[in=ci][out=co] layout (transposed on the fly).
@@ -80,7 +94,12 @@ struct PackEntry {
   int64_t src_off;   // into params (floats)
   int64_t dst_off;   // into the packed buffer (elements)
   int32_t co, ci, rs, cop, cip, dense_src;  // dense_src: 0 conv [cop][rs][cip], 1 dense, 2 conv transposed
-};                                           //   per tap [cip][rs][cop] (DGRAD K-major weights)
+                                             //   per tap [cip][rs][cop] (DGRAD K-major weights)
+  // space-to-depth stem (s2d_r = the original kernel size R, 0 otherwise): the packed tensor is the
+  // ((R+1)/2)^2-tap, 4*ci-channel kernel of the stride-1 conv over the 2x2 space-to-depth input;
+  // s2d tap (a, b), channel ((i*2 + j)*ci + c) holds W[co][2a+i][2b+j][c] (0 past R or ci)
+  int32_t s2d_r, pad_;
+};
 cudaError_t pack_weights(int dtype, const float* params, void* packed, const PackEntry* entries_dev, int n_entries,
                          int max_elems, cudaStream_t st);
 
