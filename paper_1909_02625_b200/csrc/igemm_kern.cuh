@@ -974,6 +974,184 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
       // each warp: CPW 16-column chunks of its half; wide tiles load 32 TMEM columns per wait
       constexpr int CPW = BN / 16 / (NEPI / 4);
       constexpr int LDW = (BN >= 128 && CPW % 2 == 0) ? 2 : 1;
+      // Fast path: a full bf16 FPROP tile of the wide (slab) epilogue without bias / residual (the
+      // ResNet-50 convs): each 32-column chunk is packed with cvt.rn.bf16x2, staged as one 32-row x
+      // 64-byte slab per warp (16-byte chunks XOR-swizzled by row pair: conflict-free), stored four
+      // lanes per row, and its BN statistics come from the staged bf16 pairs -- ~150 instead of ~565
+      // warp instructions per 32 x 32 chunk (ncu source counters, profiles/r02_epilogue.md).
+      bool fast = false, fastd = false;
+      if constexpr (MODE == DSP_IGEMM_FPROP && CPW % 2 == 0 && sizeof(T) == 2) {
+        fast = dw && !s2 && a.bias == nullptr && a.residual == nullptr && m0 + IG_BM <= M &&
+               n0 + BN <= (a.n_valid > 0 ? a.n_valid : N);
+      }
+      if constexpr (MODE == DSP_IGEMM_DGRAD && CPW % 2 == 0 && sizeof(T) == 2) {
+        fastd = dw && !s2 && !zacc && a.bias == nullptr && m0 + IG_BM <= M && n0 + BN <= (a.n_valid > 0 ? a.n_valid : N);
+      }
+      if (fastd) {
+        // DGRAD fast path (same slab scheme): optional residual add (lane = row, its four 16-byte
+        // loads issued before the accumulator wait) and the fused BatchNorm-backward statistics
+        // of the BN(s) below, g = stored dX * (mask > 0): lane = (column pair, row parity) reads
+        // dX from the slab and mask / y straight from global -- two rows of 64 contiguous bytes per
+        // warp load -- with all 16 rows' loads in flight before they are used.
+        const int rbase = m0 + q * 32;
+        const int nbt = a.bnb_count;
+#pragma unroll 1
+        for (int c2 = 0; c2 < CPW; c2 += 2) {
+          const int col0 = (half * CPW + c2) * 16;
+          uint4 rr[4];
+          if (a.residual != nullptr) {
+            const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.residual) +
+                                                             (size_t)(rbase + lane) * a.ldd + n0 + col0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rr[k] = __ldg(rp + k);
+          }
+          float vb[32];
+          tmem_ld32(tl + col0, vb);
+          if (a.residual != nullptr) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t w4[4] = {rr[k].x, rr[k].y, rr[k].z, rr[k].w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                vb[8 * k + 2 * j] += __uint_as_float(w4[j] << 16);
+                vb[8 * k + 2 * j + 1] += __uint_as_float(w4[j] & 0xffff0000u);
+              }
+            }
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk[j]) : "f"(vb[2 * j + 1]), "f"(vb[2 * j]));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t ad = sDW + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(pk[4 * k]), "r"(pk[4 * k + 1]),
+                         "r"(pk[4 * k + 2]), "r"(pk[4 * k + 3])
+                         : "memory");
+          }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int r = (lane >> 2) + 8 * it, k = lane & 3;
+            uint4 raw;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                         : "r"(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)));
+            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k * 8) = raw;
+          }
+          if (want_stats) {
+            const int cp = lane & 15, rh = lane >> 4;
+            const int cl = col0 + 2 * cp;  // tile column of the pair
+            const size_t cofs = (size_t)n0 + cl;
+            const float m0a = bst[0][0][cl], i0a = bst[0][1][cl], m0b = bst[0][0][cl + 1], i0b = bst[0][1][cl + 1];
+            const float m1a = bst[1][0][cl], i1a = bst[1][1][cl], m1b = bst[1][0][cl + 1], i1b = bst[1][1][cl + 1];
+            float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f, s3a = 0.f, s3b = 0.f;
+#pragma unroll 1
+            for (int h8 = 0; h8 < 16; h8 += 8) {  // 8 rows' loads in flight at a time (register cap)
+            uint32_t mk[8], y0[8], y1[8];
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const size_t o = (size_t)(rbase + rh + 2 * (h8 + it)) * a.ldd + cofs;
+              mk[it] = __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb_mask) + o));
+              y0[it] = __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[0].y) + o));
+              y1[it] = nbt > 1 ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[1].y) + o)) : 0u;
+            }
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = rh + 2 * (h8 + it);
+              uint32_t w;
+              asm volatile("ld.shared.b32 %0, [%1];"
+                           : "=r"(w)
+                           : "r"(sDW + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4));
+              const float ga = __uint_as_float(mk[it] << 16) > 0.f ? __uint_as_float(w << 16) : 0.f;
+              const float gb = __uint_as_float(mk[it] & 0xffff0000u) > 0.f ? __uint_as_float(w & 0xffff0000u) : 0.f;
+              s1a += ga;
+              s1b += gb;
+              s2a += ga * ((__uint_as_float(y0[it] << 16) - m0a) * i0a);
+              s2b += gb * ((__uint_as_float(y0[it] & 0xffff0000u) - m0b) * i0b);
+              if (nbt > 1) {
+                s3a += ga * ((__uint_as_float(y1[it] << 16) - m1a) * i1a);
+                s3b += gb * ((__uint_as_float(y1[it] & 0xffff0000u) - m1b) * i1b);
+              }
+            }
+            }
+            s1a += __shfl_xor_sync(0xffffffffu, s1a, 16);
+            s1b += __shfl_xor_sync(0xffffffffu, s1b, 16);
+            s2a += __shfl_xor_sync(0xffffffffu, s2a, 16);
+            s2b += __shfl_xor_sync(0xffffffffu, s2b, 16);
+            s3a += __shfl_xor_sync(0xffffffffu, s3a, 16);
+            s3b += __shfl_xor_sync(0xffffffffu, s3b, 16);
+            if (lane < 16) {
+              red[q][cl][0] += s1a;
+              red[q][cl][1] += s2a;
+              red[q][cl][2] += s3a;
+              red[q][cl + 1][0] += s1b;
+              red[q][cl + 1][1] += s2b;
+              red[q][cl + 1][2] += s3b;
+            }
+          }
+          __syncwarp();
+        }
+      } else if (fast) {
+        const int rbase = m0 + q * 32;
+#pragma unroll 1
+        for (int c2 = 0; c2 < CPW; c2 += 2) {
+          const int col0 = (half * CPW + c2) * 16;  // this chunk: tile columns [col0, col0 + 32)
+          float vb[32];
+          tmem_ld32(tl + col0, vb);
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk[j]) : "f"(vb[2 * j + 1]), "f"(vb[2 * j]));
+          // row `lane`: 4 x 16-byte chunks, chunk k at position k ^ ((lane >> 1) & 3)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t ad = sDW + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(pk[4 * k]), "r"(pk[4 * k + 1]),
+                         "r"(pk[4 * k + 2]), "r"(pk[4 * k + 3])
+                         : "memory");
+          }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {  // 8 rows per pass, 4 lanes (64 contiguous bytes) per row
+            const int r = (lane >> 2) + 8 * it, k = lane & 3;
+            uint4 raw;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                         : "r"(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)));
+            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k * 8) = raw;
+          }
+          if (want_stats) {
+            // lane: column pair cp (tile columns col0 + 2cp, +1) over rows rh, rh + 2, ... (rh = lane >> 4)
+            const int cp = lane & 15, rh = lane >> 4;
+            float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+              const int r = rh + 2 * it;
+              uint32_t w;
+              asm volatile("ld.shared.b32 %0, [%1];"
+                           : "=r"(w)
+                           : "r"(sDW + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4));
+              const float ya = __uint_as_float(w << 16), yb = __uint_as_float(w & 0xffff0000u);
+              s1a += ya;
+              s2a = fmaf(ya, ya, s2a);
+              s1b += yb;
+              s2b = fmaf(yb, yb, s2b);
+            }
+            s1a += __shfl_xor_sync(0xffffffffu, s1a, 16);
+            s1b += __shfl_xor_sync(0xffffffffu, s1b, 16);
+            s2a += __shfl_xor_sync(0xffffffffu, s2a, 16);
+            s2b += __shfl_xor_sync(0xffffffffu, s2b, 16);
+            if (lane < 16) {
+              red[q][col0 + 2 * cp][0] += s1a;
+              red[q][col0 + 2 * cp][1] += s2a;
+              red[q][col0 + 2 * cp + 1][0] += s1b;
+              red[q][col0 + 2 * cp + 1][1] += s2b;
+            }
+          }
+          __syncwarp();  // the slab is rewritten by the next chunk
+        }
+      } else
 #pragma unroll 1
       for (int c2 = 0; c2 < CPW; c2 += LDW) {
         float vb[16 * LDW];

@@ -1,0 +1,71 @@
+"""Run one block's recorded forward + backward (+ update) a few times through the block
+executor, for ncu: realistic launch arguments for a single kernel of the DSP step.
+
+    python tools/block_profile.py --block r50s1 [--reps 3] [--precision bf16]
+    ncu --set full -k regex:igemm -s 20 -c 1 -o gpurun_out/prof python tools/block_profile.py --block r50s1
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import paper_1909_02625_b200 as P  # noqa: E402
+
+BLOCKS = {
+    # ResNet-50 stage-1 unit with identity shortcut (56x56, 256 -> 64 -> 256), B=256
+    "r50s1": (lambda: [P.bottleneck((256, 56, 56), 64, 256, 1)], 256),
+    # ResNet-50 stage-1 first unit (projection shortcut) after the stem + max pool
+    "r50s1proj": (lambda: [P.bottleneck((64, 56, 56), 64, 256, 1)], 256),
+    "r50s3": (lambda: [P.bottleneck((1024, 14, 14), 256, 1024, 1)], 256),
+    "r50stem": (lambda: [P.conv_bn_relu((3, 224, 224), 64, ksize=7, stride=2), P.maxpool((64, 112, 112))], 256),
+    "c1basic": (lambda: [P.basic_unit((16, 32, 32), 16, 1)], 128),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--block", default="r50s1", choices=sorted(BLOCKS))
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    args = ap.parse_args()
+    import torch
+
+    from paper_1909_02625_b200 import _lib as L
+    from paper_1909_02625_b200.runtime import DeviceBlock
+
+    layers, B = BLOCKS[args.block]
+    layers = layers()
+    model = P.build_model(layers, [])
+    P.init_params(model, 0)
+    dt = L.storage_dtype(args.precision)
+    st = torch.cuda.current_stream()
+    db = DeviceBlock(model.blocks[0], B, is_last=False, stream=st, dtype=dt)
+    tdt = L.torch_storage(dt)
+    x = torch.randn(db.in_elems, device="cuda").to(tdt)
+    y = torch.empty(db.out_elems, device="cuda", dtype=tdt)
+    up = (torch.randn(db.out_elems, device="cuda") * 1e-2).to(tdt)
+    gin = torch.empty(db.in_elems, device="cuda", dtype=tdt)
+    ys = db.params.clone()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for r in range(args.reps):
+        if r == args.reps - 1:
+            ev[0].record(st)
+        db.forward(x, y, record=False)
+        db.forward(x, None, record=True)
+        db.backward(up, gin)
+        db.update(L.DSP_RULE_SUM, ys, 1e-3, 1e-3, 0.9, 5e-4, True, None)
+        if r == args.reps - 1:
+            ev[1].record(st)
+    torch.cuda.synchronize()
+    print(f"{args.block}: one fwd + recompute + bwd + update {ev[0].elapsed_time(ev[1]) * 1000:.1f} us")
+
+
+if __name__ == "__main__":
+    main()
