@@ -619,14 +619,14 @@ __global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, uint
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int CV = Cp / VE;
-  const int64_t n = (int64_t)B * P * Q * CV;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cv = (int)(i % CV);
-    int64_t t = i / CV;
-    const int q = (int)(t % Q);
+  const int n = B * P * Q * CV;  // < 2^31 (checked by the launcher): 32-bit index math
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int cv = i % CV;
+    int t = i / CV;
+    const int q = t % Q;
     t /= Q;
-    const int p = (int)(t % P);
-    const int b = (int)(t / P);
+    const int p = t % P;
+    const int b = t / P;
     uint4 raw[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) {  // all nine taps in flight
@@ -675,14 +675,14 @@ __global__ void maxpool_bwd_k(const T* __restrict__ u, const uint8_t* __restrict
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int CV = Cp / VE;
-  const int64_t n = (int64_t)B * H * W * CV;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cv = (int)(i % CV);
-    int64_t t = i / CV;
-    const int w = (int)(t % W);
+  const int n = B * H * W * CV;  // < 2^31 (checked by the launcher): 32-bit index math
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int cv = i % CV;
+    int t = i / CV;
+    const int w = t % W;
     t /= W;
-    const int h = (int)(t % H);
-    const int b = (int)(t / H);
+    const int h = t % H;
+    const int b = t / H;
     float acc[VE];
 #pragma unroll
     for (int e = 0; e < VE; ++e) acc[e] = 0.f;
@@ -717,6 +717,37 @@ __global__ void maxpool_bwd_k(const T* __restrict__ u, const uint8_t* __restrict
 
 // ------------------------------------------------------------------ space-to-depth stem
 // One thread per s2d pixel: its cps channels = 4 sub-positions (i, j) x c input channels.
+// the ResNet-50 stem case: bf16, 8-channel input pixels (one 16-byte load each), 16 s2d channels
+// (two 16-byte stores), 32-bit index math
+__global__ void s2d_pack8_k(const uint4* __restrict__ x, uint4* __restrict__ s, int B, int H, int W, int c, int Hs,
+                            int Ws, int pad) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  const int n = B * Hs * Ws;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int ws = i % Ws, t = i / Ws, hs = t % Hs, b = t / Hs;
+    uint4 in[4];
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+      const int h = 2 * hs + (sub >> 1) - pad, w = 2 * ws + (sub & 1) - pad;
+      in[sub] = ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) ? __ldg(x + ((b * H + h) * W + w))
+                                                                        : make_uint4(0, 0, 0, 0);
+    }
+    uint16_t o[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = 0;
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+      const uint16_t* e = reinterpret_cast<const uint16_t*>(&in[sub]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < c) o[sub * c + k] = e[k];
+    }
+    const uint4* op = reinterpret_cast<const uint4*>(o);
+    s[2 * i] = op[0];
+    s[2 * i + 1] = op[1];
+  }
+}
+
 template <typename T>
 __global__ void s2d_pack_k(const T* __restrict__ x, T* __restrict__ s, int B, int H, int W, int c, int cpx, int Hs,
                            int Ws, int cps, int pad) {
@@ -804,54 +835,69 @@ __global__ void __launch_bounds__(256) wgrad_reduce_k(const float* __restrict__ 
                                                      int RS, int Cp, int ci_real, int co_real, int dense_layout,
                                                      float* __restrict__ grad, int s2d_r) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
-  // CTA = 32 consecutive partial elements (coalesced 128 B per split row) x 8 warps; warp w
-  // sums the contiguous split range [w*S/8, (w+1)*S/8), 8 loads in flight, then warp 0 adds
-  // the 8 warp sums in order (deterministic). Small CTAs on purpose: the step runs the K
-  // blocks' kernels concurrently and a reduce CTA must fit beside two resident conv CTAs
-  // (a 1024-thread version was 5x faster alone and made the whole step 10% slower).
+  // CTA = 128 consecutive partial elements (a float4 per lane: 512 B per split row) x 8 warps;
+  // warp w sums the contiguous split range [w*S/8, (w+1)*S/8) with its loads in flight, then
+  // warp 0 adds the 8 warp sums in order (deterministic). Small CTAs on purpose: the step runs the
+  // K blocks' kernels concurrently and a reduce CTA must fit beside resident conv CTAs.
   constexpr int W = 8;
-  __shared__ float red[W][33];
+  __shared__ float4 red[W][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t total = (int64_t)Mw * N;
-  const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t idx0 = ((int64_t)blockIdx.x * 32 + lane) * 4;  // first of this lane's 4 elements
   const int z0 = (int)((int64_t)splits * w / W), z1 = (int)((int64_t)splits * (w + 1) / W);
-  float acc = 0.f;
-  if (idx < total) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (idx0 < total) {  // total % 4 == 0 (N is a multiple of 8)
     const size_t zs = (size_t)total;
-    const float* p = part + idx;
-    for (int z = z0; z < z1; z += 8) {
-      float v[8];
+    const float* p = part + idx0;
+    for (int z = z0; z < z1; z += 4) {
+      float4 v[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = z + u < z1 ? __ldcg(p + (size_t)(z + u) * zs) : 0.f;
+      for (int u = 0; u < 4; ++u)
+        v[u] = z + u < z1 ? __ldcg(reinterpret_cast<const float4*>(p + (size_t)(z + u) * zs))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc += v[u];
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
     }
   }
   red[w][lane] = acc;
   __syncthreads();
-  if (w != 0 || idx >= total) return;
-  float sum = 0.f;
+  if (w != 0 || idx0 >= total) return;
+  float sum[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int j = 0; j < W; ++j) sum += red[j][lane];
-  const int n = (int)(idx % N);
-  const int m = (int)(idx / N);
-  if (n >= co_real) return;
-  int64_t dst;
-  if (dense_layout == 1) {
-    if (m >= ci_real) return;
-    dst = (int64_t)m * co_real + n;
-  } else if (dense_layout == 2) {  // space-to-depth stem
-    const int cs = m % Cp, tap = m / Cp, rs2 = (s2d_r + 1) / 2;
-    const int sub = cs / ci_real, c = cs % ci_real;
-    const int r = 2 * (tap / rs2) + (sub >> 1), s = 2 * (tap % rs2) + (sub & 1);
-    if (sub >= 4 || tap >= RS || r >= s2d_r || s >= s2d_r) return;
-    dst = (((int64_t)n * s2d_r + r) * s2d_r + s) * ci_real + c;
-  } else {
-    const int ci = m % Cp, tap = m / Cp;
-    if (ci >= ci_real || tap >= RS) return;
-    dst = ((int64_t)n * RS + tap) * ci_real + ci;
+  for (int j = 0; j < W; ++j) {
+    sum[0] += red[j][lane].x;
+    sum[1] += red[j][lane].y;
+    sum[2] += red[j][lane].z;
+    sum[3] += red[j][lane].w;
   }
-  grad[dst] = sum;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int64_t idx = idx0 + e;
+    const int n = (int)(idx % N);
+    const int m = (int)(idx / N);
+    if (n >= co_real) continue;
+    int64_t dst;
+    if (dense_layout == 1) {
+      if (m >= ci_real) continue;
+      dst = (int64_t)m * co_real + n;
+    } else if (dense_layout == 2) {  // space-to-depth stem
+      const int cs = m % Cp, tap = m / Cp, rs2 = (s2d_r + 1) / 2;
+      const int sub = cs / ci_real, c = cs % ci_real;
+      const int r = 2 * (tap / rs2) + (sub >> 1), s = 2 * (tap % rs2) + (sub & 1);
+      if (sub >= 4 || tap >= RS || r >= s2d_r || s >= s2d_r) continue;
+      dst = (((int64_t)n * s2d_r + r) * s2d_r + s) * ci_real + c;
+    } else {
+      const int ci = m % Cp, tap = m / Cp;
+      if (ci >= ci_real || tap >= RS) continue;
+      dst = ((int64_t)n * RS + tap) * ci_real + ci;
+    }
+    grad[dst] = sum[e];
+  }
 }
 
 template <typename T>
@@ -1373,7 +1419,7 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, i
                             int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    if (Cp % V16<T>::N) return cudaErrorInvalidValue;
+    if (Cp % V16<T>::N || (int64_t)B * H * W * Cp >= (1ll << 31)) return cudaErrorInvalidValue;
     launch_k(maxpool_fwd_k<T>, grid_for((int64_t)B * P * Q * Cp / V16<T>::N), kThreads, 0, st, (const T*)x, (T*)out, arg, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
@@ -1384,7 +1430,7 @@ cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void*
                              int Cp, cudaStream_t st) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    if (Cp % V16<T>::N) return cudaErrorInvalidValue;
+    if (Cp % V16<T>::N || (int64_t)B * H * W * Cp >= (1ll << 31)) return cudaErrorInvalidValue;
     launch_k(maxpool_bwd_k<T>, grid_for((int64_t)B * H * W * Cp / V16<T>::N), kThreads, 0, st, (const T*)u, arg, (T*)dx, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
@@ -1403,8 +1449,9 @@ cudaError_t softmax_xent(int dtype, const float* logits, int ld, int B, int C, c
 cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, int Cp, int ci_real, int co_real,
                          int dense_layout, float* grad, cudaStream_t st, int s2d_r) {
   const int64_t total = (int64_t)Mw * N;
-  launch_k(wgrad_reduce_k, (unsigned)((total + 31) / 32), 256, 0, st, part, splits, Mw, N, RS, Cp, ci_real, co_real,
-                                                                  dense_layout, grad, s2d_r);
+  if (N % 4) return cudaErrorInvalidValue;
+  launch_k(wgrad_reduce_k, (unsigned)((total + 127) / 128), 256, 0, st, part, splits, Mw, N, RS, Cp, ci_real, co_real,
+           dense_layout, grad, s2d_r);
   return note_launch(), cudaGetLastError();
 }
 
@@ -1421,6 +1468,11 @@ cudaError_t pack_weights(int dtype, const float* params, void* packed, const Pac
 
 cudaError_t s2d_pack(int dtype, const void* x, void* s, int B, int H, int W, int c, int cpx, int Hs, int Ws, int cps,
                      int pad, cudaStream_t st) {
+  if (dtype == DSP_DTYPE_BF16 && cpx == 8 && cps == 16 && c <= 4 && (int64_t)B * H * W < (1ll << 31)) {
+    launch_k(s2d_pack8_k, grid_for((int64_t)B * Hs * Ws), kThreads, 0, st, (const uint4*)x, (uint4*)s, B, H, W, c, Hs,
+             Ws, pad);
+    return note_launch(), cudaGetLastError();
+  }
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     launch_k(s2d_pack_k<T>, grid_for((int64_t)B * Hs * Ws), kThreads, 0, st, (const T*)x, (T*)s, B, H, W, c, cpx, Hs, Ws,
