@@ -142,6 +142,8 @@ class B200Runtime:
                     self.twins[k] = self.dev[k].make_twin()
                     self._fwd_streams[k] = torch.cuda.Stream(self.device, priority=prio[k])
         self.replayed_kernels = 0  # library kernels executed through graph replays
+        self._recv = {}  # multi-rank receive rings (recv_buffers)
+        self._tagbad = self._empty(1, dtype=torch.int64, zero=True)
 
     def kernels_executed(self) -> int:
         """Library kernels run so far: eager launches (dsp_launch_count, which also counts
@@ -283,6 +285,29 @@ class B200Runtime:
 
     def empty_grad_header(self):
         return self._empty(1, dtype=self.torch.int64)
+
+    # ---- multi-rank receive rings (graph-safe: slot n mod R) and lazy tag checks ------------
+    def recv_buffers(self, kind: str, k: int, n: int):
+        """(header, tensor) slot n mod R of the receive ring for block k's cross-rank input
+        packets (kind "act": header = [tag, labels...]; "grad": header = [tag]). A packet lives at
+        most p_k + m_k (act) / q_k (grad) steps < R, so slots are never overwritten early."""
+        key = (kind, k, n % self.R)
+        buf = self._recv.get(key)
+        if buf is None:
+            torch = self.torch
+            hdr = self._empty(1 + self.B if kind == "act" else 1, dtype=torch.int64, zero=True)
+            buf = (hdr, self._empty(self.in_elems(k), zero=True))
+            self._recv[key] = buf
+        return buf
+
+    def check_tag(self, hdr, tag: int) -> None:
+        """Compare a received header's batch tag with the closed-form one on the device; any
+        mismatch is counted in a device flag that synchronize() turns into ProtocolError."""
+        with self.torch.cuda.stream(self.stream):
+            self._tagbad.add_((hdr[:1] != tag).to(self.torch.int64))
+
+    def tag_errors(self) -> int:
+        return int(self._tagbad.item())
 
     def parse_act_header(self, hdr):
         return int(hdr[0].item()), hdr[1:]

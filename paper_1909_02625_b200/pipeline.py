@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+import os
 import time
 from collections import deque
 from dataclasses import dataclass
@@ -446,12 +447,22 @@ class TrainEngine:
         self.block_steps[k] = n + 1
 
     # ------------------------------------------------------------------ cross-rank exchange
-    def _exchange(self) -> None:
-        """Ship this step's boundary packets to their consumers and receive the
-        packets the neighbours produced this step (consumed >= 1 step later)."""
+    def _exchange(self, n: int | None = None) -> None:
+        """Ship this step's boundary packets to their consumers and receive the packets the
+        neighbours produced this step (consumed >= 1 step later).
+
+        Packets land in the consumer runtime's per-phase receive rings (``recv_buffers``: slot
+        n mod R, the same periodic addresses the step graphs bake in). Their batch tags follow the
+        closed forms of SURVEY Appendix A (fresh tag n - cum_p[k], stale tag n - cum_p[k] - m_k),
+        so the consumer queues the expected tag at once and verifies the received header on the
+        device (``check_tag``), raising ProtocolError at the next sync point -- no per-step
+        device->host read."""
         if self._transport.world <= 1:
             return
         K = self.config.k
+        if n is None:
+            n = self.block_steps[self.local[0]] - 1 if self.local else 0
+        cp, m = self._cum_p, self.config.m
         sends, recvs = [], []
         for k in range(K - 1):
             prod, cons = self.placement[k], self.placement[k + 1]
@@ -461,7 +472,7 @@ class TrainEngine:
                 pkt = self._outbox_act.pop(k)
                 sends.append((cons, self.rt.act_header(pkt.batch_index, pkt.labels), pkt.tensor))
             elif cons == self.rank:
-                recvs.append(("act", k, prod))
+                recvs.append(("act", k, prod, n - cp[k]))
         for k in range(1, K):
             prod, cons = self.placement[k], self.placement[k - 1]
             if prod == cons:
@@ -470,37 +481,55 @@ class TrainEngine:
                 pkt = self._outbox_grad.pop(k)
                 sends.append((cons, self.rt.grad_header(pkt.batch_index), pkt.tensor))
             elif cons == self.rank:
-                recvs.append(("grad", k, prod))
+                recvs.append(("grad", k, prod, n - cp[k] - m[k]))
         bufs = []
-        for kind, k, src in recvs:
-            if kind == "act":
-                bufs.append((src, self.rt.empty_act_header(), self.rt.empty_act(k + 1)))
+        ring = getattr(self.rt, "recv_buffers", None)
+        for kind, k, src, _ in recvs:
+            if ring is not None:
+                hdr, ten = ring(kind, k + 1 if kind == "act" else k, n)
+            elif kind == "act":
+                hdr, ten = self.rt.empty_act_header(), self.rt.empty_act(k + 1)
             else:
-                bufs.append((src, self.rt.empty_grad_header(), self.rt.empty_grad(k)))
+                hdr, ten = self.rt.empty_grad_header(), self.rt.empty_grad(k)
+            bufs.append((src, hdr, ten))
         try:
             self._transport.exchange(sends, bufs, timeout_s=self.watchdog_s)
         except TimeoutError as exc:  # the reference's watchdog (pipeline.py:644-657)
-            occupancy = {q.name: len(q) for q in self.out_queues if q is not None}
-            occupancy.update({q.name: len(q) for q in self.grad_queues[1:] if q is not None})
-            raise DeadlockError(f"workers stalled after {self.watchdog_s}s; queue occupancy {occupancy} "
-                                f"steps {self.block_steps}") from exc
-        for (kind, k, _), (_, hdr, ten) in zip(recvs, bufs):
-            if kind == "act":
+            raise self._deadlock() from exc
+        check = getattr(self.rt, "check_tag", None)
+        for (kind, k, _, tag), (_, hdr, ten) in zip(recvs, bufs):
+            if check is not None:  # device-side comparison, read at the next sync point
+                check(hdr, tag)
+                labels = hdr[1:] if kind == "act" else None
+            elif kind == "act":
                 tag, labels = self.rt.parse_act_header(hdr)
+            else:
+                tag = self.rt.parse_grad_header(hdr)
+            if kind == "act":
                 self.out_queues[k].put(ActivationPacket(tag, ten, labels))
             else:
-                self.grad_queues[k].put(GradPacket(self.rt.parse_grad_header(hdr), ten))
+                self.grad_queues[k].put(GradPacket(tag, ten))
+
+    def _deadlock(self) -> DeadlockError:
+        occupancy = {q.name: len(q) for q in self.out_queues if q is not None}
+        occupancy.update({q.name: len(q) for q in self.grad_queues[1:] if q is not None})
+        return DeadlockError(f"workers stalled after {self.watchdog_s}s; queue occupancy {occupancy} "
+                             f"steps {self.block_steps}")
 
     # ------------------------------------------------------------------ drivers
     def run(self, n_steps: int) -> None:
         if n_steps < 0:
             raise ValueError("n_steps must be non-negative")
-        graphs = (getattr(self.rt, "use_graphs", False) and self._transport.world <= 1 and self.tracker is None
-                  and not isinstance(self.straggler, DeviceStraggler))
+        # multi-rank: the local blocks' step is graph-replayed too; the NCCL exchange follows the
+        # graph launch on the same stream (packets received into periodic per-phase ring slots)
+        graphs = (getattr(self.rt, "use_graphs", False) and self.tracker is None
+                  and not isinstance(self.straggler, DeviceStraggler)
+                  and (self._transport.world <= 1 or os.environ.get("DSP_B200_MULTIRANK_GRAPHS", "1") != "0"))
         for _ in range(n_steps):
             n = self.block_steps[self.local[0]] if self.local else 0
             if graphs and n >= self._graph_horizon():
-                self.rt.graph_step(n, self._step_signature(n), self._issue_step)
+                self.rt.graph_step(n, self._step_signature(n), self._issue_local)
+                self._exchange(n)
             else:
                 self._issue_step()
                 end = getattr(self.rt, "end_step", None)
@@ -508,6 +537,10 @@ class TrainEngine:
                     end(n)
 
     def _issue_step(self) -> None:
+        self._issue_local()
+        self._exchange()
+
+    def _issue_local(self) -> None:
         fork = getattr(self.rt, "fork_blocks", None)
         if fork is not None:
             fork()
@@ -524,7 +557,6 @@ class TrainEngine:
         join = getattr(self.rt, "join_blocks", None)
         if join is not None:
             join()
-        self._exchange()
 
     def _graph_horizon(self) -> int:
         """First step from which every queued packet is a ring slot (zero prefill drained)."""
@@ -542,7 +574,15 @@ class TrainEngine:
         return tuple(sig)
 
     def synchronize(self) -> None:
+        try:
+            self._transport.drain(self.watchdog_s)
+        except TimeoutError as exc:
+            raise self._deadlock() from exc
         self.rt.synchronize()
+        bad = getattr(self.rt, "tag_errors", None)
+        if bad is not None and bad():
+            raise ProtocolError("a received packet's batch tag does not match the closed-form FIFO schedule "
+                                "(gradient batch does not meet activation batch, pipeline.py:567-572)")
 
     def last_loss(self) -> float | None:
         """Loss of the most recent last-block step on this rank (a 4-byte device->host read)."""
@@ -557,6 +597,7 @@ class TrainEngine:
     def _materialize(self) -> None:
         if not self._pending:
             return
+        self.synchronize()
         vals = self.rt.read_scalars([(l, g) for _, l, g in self._pending])
         for (rec, _, _), (lv, gv) in zip(self._pending, vals):
             rec.grad_norm = float(np.sqrt(gv))

@@ -12,6 +12,7 @@ re-checks the reference's gradient-meets-activation assertion.
 from __future__ import annotations
 
 import time
+from collections import deque
 
 
 class LocalTransport:
@@ -21,6 +22,9 @@ class LocalTransport:
     def exchange(self, sends, recvs, timeout_s=None) -> None:
         if sends or recvs:
             raise RuntimeError("single-process transport cannot exchange packets")
+
+    def drain(self, timeout_s=None) -> None:
+        pass
 
 
 class TorchDistTransport:
@@ -33,6 +37,7 @@ class TorchDistTransport:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._inflight = deque()  # NCCL: (issue time, requests) not yet known complete
 
     def exchange(self, sends, recvs, timeout_s: float | None = None) -> None:
         """sends: [(dst, header, tensor)], recvs: [(src, header_buf, tensor_buf)].
@@ -70,16 +75,31 @@ class TorchDistTransport:
                         raise
                     raise TimeoutError(f"{len(reqs) - i} of {len(reqs)} transfers pending after {timeout_s}s") from exc
             return
-        # NCCL: wait() only orders the current stream after the transfer; poll its completion event
-        pending = list(reqs)
-        for req in pending:
+        # NCCL: wait() only orders the current stream after the transfer (the host goes on
+        # enqueueing the next step); the watchdog retires completed batches as later steps are
+        # issued and raises once a batch has been pending for timeout_s
+        for req in reqs:
             req.wait()
-        while pending:
-            pending = [r for r in pending if not r.is_completed()]
-            if pending:
-                if time.monotonic() > deadline:
-                    raise TimeoutError(f"{len(pending)} of {len(reqs)} transfers pending after {timeout_s}s")
-                time.sleep(2e-4)
+        self._inflight.append((time.monotonic(), reqs))
+        self._retire(timeout_s, block=False)
+
+    def _retire(self, timeout_s, block: bool) -> None:
+        while self._inflight:
+            t0, reqs = self._inflight[0]
+            if all(r.is_completed() for r in reqs):
+                self._inflight.popleft()
+                continue
+            waited = time.monotonic() - t0
+            if timeout_s is not None and waited > timeout_s:
+                n = sum(1 for r in reqs if not r.is_completed())
+                raise TimeoutError(f"{n} of {len(reqs)} transfers pending after {timeout_s}s")
+            if not block:
+                return
+            time.sleep(2e-4)
+
+    def drain(self, timeout_s=None) -> None:
+        """Block until every issued transfer completed (sync points), under the watchdog."""
+        self._retire(timeout_s, block=True)
 
 
 def default_transport():

@@ -76,9 +76,11 @@ def test_block_planning_rejects_bad_programs(lib):
     descs[1].in_c = 5
     h = C.c_void_p()
     assert lib.dsp_block_create(descs, 2, 4, L.DSP_DTYPE_BF16, 1, C.byref(h)) == 1
-    # fp32 storage is rejected for blocks (tcgen05 tf32 MN-major operands unsupported)
+    # fp32 storage (3xTF32) plans; an unknown storage dtype is rejected
     descs = P.build_model([P.dense(4, 3)], []).blocks[0].layer_descs()
-    assert lib.dsp_block_create(descs, 1, 4, L.DSP_DTYPE_F32, 1, C.byref(h)) == 1
+    assert lib.dsp_block_create(descs, 1, 4, L.DSP_DTYPE_F32, 1, C.byref(h)) == 0
+    lib.dsp_block_destroy(h)
+    assert lib.dsp_block_create(descs, 1, 4, 7, 1, C.byref(h)) == 1 and b"dtype" in lib.dsp_last_error()
 
 
 def test_engine_without_gpu_fails_loudly():
