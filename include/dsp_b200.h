@@ -260,8 +260,8 @@ int64_t dsp_launch_count(void);
 /* ------------------------------------------------------------ engine level
  * The whole DSP train step behind one handle: the reference's
  * TrainEngine(model, config, data, schedule, rule, beta, s, weight_decay) +
- * run(n) + log (pipeline.py:451-606, 610-620, 664), single GPU, all K blocks
- * on one device. The queue config is validated by the caller exactly as
+ * run(n) + log (pipeline.py:451-606, 610-660, 664): all K blocks on one device,
+ * or one device per block (dsp_config_t.multi_device). The queue config is validated by the caller exactly as
  * validate_config does (pipeline.py:85-128); dsp_create re-checks Eq.(5) and
  * returns DSP_E_INVALID naming the first violated constraint. */
 #define DSP_MAX_BLOCKS 8
@@ -280,7 +280,14 @@ typedef struct {
   int32_t n_layers[DSP_MAX_BLOCKS];
   const dsp_layer_desc_t* layers; /* all blocks' layers back to back; param_offset relative to its block */
   int32_t use_graphs;             /* replay each step as a CUDA graph once the zero prefill has drained */
-  int32_t device;                 /* CUDA device ordinal */
+  int32_t device;                 /* CUDA device ordinal (all blocks, unless multi_device) */
+  /* multi_device = 1: block k runs on device_of_block[k] (one GPU per block is the
+   * reference's one worker per block, pipeline.py:622-660). Rings live on the consumer's device and
+   * the producer's last kernel stores each packet into the peer slot over NVLink (peer access is
+   * enabled along every cross-device FIFO edge); each device replays its own step graph, ordered
+   * after its neighbours' previous step by events. */
+  int32_t multi_device;
+  int32_t device_of_block[DSP_MAX_BLOCKS];
 } dsp_config_t;
 
 typedef struct {

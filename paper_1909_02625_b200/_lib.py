@@ -125,6 +125,7 @@ class EngineConfig(C.Structure):
         ("n_layers", C.c_int32 * DSP_MAX_BLOCKS),
         ("layers", C.POINTER(LayerDesc)),
         ("use_graphs", C.c_int32), ("device", C.c_int32),
+        ("multi_device", C.c_int32), ("device_of_block", C.c_int32 * DSP_MAX_BLOCKS),
     ]
 
 

@@ -1927,9 +1927,13 @@ constexpr int f32_smem() {
 template <typename T, int MODE, int BN>
 cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   using Cfg = IgCfg<BN>;
-  static int attr_state = 0;
-  static int num_sms = 148;
-  if (!attr_state) {
+  // the kernel attributes are per device: set them the first time each device launches
+  constexpr int kMaxDev = 64;
+  static int attr_state[kMaxDev] = {};
+  static int num_sms_dev[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!attr_state[dev]) {
     const int smax = std::max(std::max(std::max(Cfg::SMEM, IgCfg<BN, true>::SMEM), IG_HALO_SMEM_MAX), f32_smem<T, MODE, BN>());
     cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smax);
@@ -1938,11 +1942,12 @@ cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    attr_state = 1;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    num_sms_dev[dev] = sms;
+    attr_state[dev] = 1;
   }
+  const int num_sms = num_sms_dev[dev];
   const int EPC = 16 / (int)sizeof(T);
   const int KS = 8 * EPC;
   const int nkb = (a.Kd + KS - 1) / KS;

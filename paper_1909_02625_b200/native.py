@@ -23,7 +23,9 @@ from .pipeline import LogRecord, PipelineConfig, TrainLog
 class NativeEngine:
     def __init__(self, model, config: PipelineConfig, batch: int, schedule: LrSchedule, rule: str = "sgd",
                  beta: float = 0.0, s: float = 1.0, weight_decay: float = 0.0, use_graphs: bool = True,
-                 device: int = 0, precision: str = "bf16"):
+                 device: int = 0, precision: str = "bf16", devices=None):
+        """devices: optional CUDA ordinal per block (one GPU per block, packets stored into the
+        consumer's ring over NVLink); default: every block on `device`."""
         lib = L.load()
         self.lib = lib
         self.model = model
@@ -56,6 +58,12 @@ class NativeEngine:
         cfg.layers = C.cast(flat, C.POINTER(L.LayerDesc))
         cfg.use_graphs = int(use_graphs)
         cfg.device = device
+        if devices is not None:
+            if len(devices) != K:
+                raise ValueError(f"devices names {len(devices)} devices for {K} blocks")
+            cfg.multi_device = 1
+            for k, d in enumerate(devices):
+                cfg.device_of_block[k] = int(d)
         # ring depth and graph horizon exactly as csrc/engine.cu derives them (steps >= horizon
         # replay per-phase graphs; the first replay of each of the ring phases captures it)
         p, m = config.p, config.m

@@ -130,3 +130,29 @@ def test_label_out_of_range_and_config_errors():
     nm2, _ = twin_models(layers, [2], seed=1)
     with pytest.raises(P.DspError, match="q_positive"):
         NativeEngine(nm2, bad, 4, P.LrSchedule(0.1))
+
+
+def test_device_of_block_config_matches_single_device():
+    """dsp_config_t.multi_device with every block mapped to device 0 runs the per-device graph /
+    event code path; it must give the single-device engine's log and parameters bit for bit (the
+    cross-device case differs only in where the ring slots live -- the consumer's device -- and in
+    the neighbour-step events, which this box cannot exercise with one GPU)."""
+    import torch
+
+    layers = small_resnet(in_shape=(3, 8, 8))
+    cfg = P.default_queue_config(4)
+    pool = R.synthetic_batches(6, 8, (3, 8, 8), 10, seed=1)
+    sched = P.LrSchedule(0.05, ((12, 0.5),))
+    runs = []
+    for devices in (None, [0, 0, 0, 0]):
+        nm, _ = twin_models(layers, [1, 2, 3], seed=3)
+        ne = NativeEngine(nm, cfg, 8, sched, rule="sum", beta=0.9, devices=devices)
+        ne.run(24, R.cycle(pool))
+        runs.append((ne.log.checksum(), [ne.params(k) for k in range(4)]))
+    assert runs[0][0] == runs[1][0]
+    for a, b in zip(runs[0][1], runs[1][1]):
+        assert np.array_equal(a, b)
+    if torch.cuda.device_count() < 2:
+        with pytest.raises(P.DspError, match="device"):
+            nm, _ = twin_models(layers, [1, 2, 3], seed=3)
+            NativeEngine(nm, cfg, 8, sched, devices=[0, 1, 1, 1])
