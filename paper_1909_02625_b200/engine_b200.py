@@ -80,6 +80,18 @@ class B200Runtime:
         self.dtype_code = L.storage_dtype(precision)
         self.act_dtype = L.torch_storage(self.dtype_code)
         self.device = require_cuda(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(self.device):  # the library creates its streams / events on the current device
+            self._init(model, local, batch, rule, beta, s, weight_decay, config, use_graphs)
+
+    def scope(self):
+        """Context making this runtime's device current: every library call that creates CUDA
+        objects (block side streams, events) or launches kernels runs under it."""
+        return self.torch.cuda.device(self.device)
+
+    def _init(self, model, local, batch, rule, beta, s, weight_decay, config, use_graphs):
+        torch = self.torch
         self.stream = torch.cuda.current_stream(self.device)
         self.model = model
         self.B = batch

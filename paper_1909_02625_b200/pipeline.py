@@ -525,16 +525,21 @@ class TrainEngine:
         graphs = (getattr(self.rt, "use_graphs", False) and self.tracker is None
                   and not isinstance(self.straggler, DeviceStraggler)
                   and (self._transport.world <= 1 or os.environ.get("DSP_B200_MULTIRANK_GRAPHS", "1") != "0"))
-        for _ in range(n_steps):
-            n = self.block_steps[self.local[0]] if self.local else 0
-            if graphs and n >= self._graph_horizon():
-                self.rt.graph_step(n, self._step_signature(n), self._issue_local)
-                self._exchange(n)
-            else:
-                self._issue_step()
-                end = getattr(self.rt, "end_step", None)
-                if end is not None:
-                    end(n)
+        scope = getattr(self.rt, "scope", None)
+        with scope() if scope is not None else _nullctx():
+            for _ in range(n_steps):
+                self._run_one(graphs)
+
+    def _run_one(self, graphs: bool) -> None:
+        n = self.block_steps[self.local[0]] if self.local else 0
+        if graphs and n >= self._graph_horizon():
+            self.rt.graph_step(n, self._step_signature(n), self._issue_local)
+            self._exchange(n)
+        else:
+            self._issue_step()
+            end = getattr(self.rt, "end_step", None)
+            if end is not None:
+                end(n)
 
     def _issue_step(self) -> None:
         self._issue_local()
@@ -637,6 +642,14 @@ class TrainEngine:
                 raise ProtocolError(f"block {k} staleness drifted: {sorted(lag)}")
             lags.append(lag.pop())
         return lags
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
 
 
 def model_forward(model: Model, x: np.ndarray) -> np.ndarray:

@@ -42,3 +42,29 @@ def test_auto_boundaries():
                      "model.boundaries": "auto"})
     m = cfg.build_model()
     assert m.k == 4 and m.boundaries == P.flop_balanced_boundaries(P.resnet_cifar_layers(56, 10), 4)
+
+
+SERVICE_CFG = {"pipeline.p": "1,1,0", "pipeline.m": "4,2,0",
+               "model.layers": "dense(12,16), relu, dense(16,12), relu, dense(12,4)", "model.boundaries": "2,4",
+               "data.source": "teacher", "data.teacher_dims": "12,8,4", "data.n_train": "64", "data.batch_size": "16",
+               "optimizer.rule": "sum", "optimizer.lr": "0.05", "train.epochs": "1"}
+
+
+def test_service_front_door_without_gpu():
+    """The reference service's /health, /validate, /train (service.py:98-127) with train.backend = b200:
+    a valid config validates, a bad one is a 400 naming the violated constraint, and /train on a box
+    without a CUDA device is a 503 (no CPU fallback), never a silent CPU run."""
+    import torch
+    from fastapi.testclient import TestClient
+
+    from paper_1909_02625_b200.service import create_app
+
+    c = TestClient(create_app())
+    assert c.get("/health").json()["backend"] == "b200"
+    r = c.post("/validate", json={"config": SERVICE_CFG})
+    assert r.status_code == 200 and r.json()["q"] == [0, 1, 1] and r.json()["max_staleness"] == 4
+    r = c.post("/validate", json={"config": SERVICE_CFG, "overrides": {"pipeline.m": "2,1,0"}})
+    assert r.status_code == 400 and "m[0]-p[0]-m[1] = 2-1-1 = 0" in r.json()["detail"]
+    if not torch.cuda.is_available():
+        r = c.post("/train", json={"config": SERVICE_CFG})
+        assert r.status_code == 503 and "CUDA" in r.json()["detail"]

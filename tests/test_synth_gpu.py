@@ -40,4 +40,20 @@ def test_engine_on_device_data_equals_host_data():
         eng.run(12)
         logs.append(eng.log.checksum())
     assert logs[0] == logs[1]
-    assert R.synthetic_batches is not None  # the oracle's pool is the same definition
+
+
+def test_device_batches_equal_the_oracle_pool():
+    """The device-generated pool (csrc/synth.cu) holds the oracle's synthetic_batches --
+    x ~ SeededRng(seed).normal, labels floor(uniform * C) -- bit for bit after storage rounding."""
+    import torch
+
+    from paper_1909_02625_b200.runtime import unpack_output
+
+    shape = (3, 8, 8)
+    dev = device_synthetic_batches(4, 8, shape, 10, seed=5)
+    ref = R.synthetic_batches(4, 8, shape, 10, seed=5)
+    st = torch.cuda.current_stream()
+    for db, (x, lab) in zip(dev, ref):
+        got = unpack_output(db.act, 8, shape, st)
+        assert np.array_equal(got, R.cnn.bf16_round(x))
+        assert np.array_equal(db.labels.cpu().numpy(), lab)
