@@ -116,7 +116,9 @@ typedef struct {
    * with g = stored dX * (bnb_mask > 0), per column the kernel accumulates sum g
    * and sum g * xhat_t for each of bnb_count (1 or 2) BNs sharing g (stats rows:
    * [CTA][1 + bnb_count][N]); the last CTA finalizes into bnb[t].dgamma / dbeta /
-   * coef, exactly what bn_bwd_stats writes, for channels < bnb_c_real. */
+   * coef, exactly what bn_bwd_stats writes, for channels < bnb_c_real. bnb_mask = NULL (one target
+   * only): the BN's output is relu(y*scale + shift) with no residual, so the mask is recomputed from
+   * bnb[0].y and its stat rows 2-3 (scale, shift) instead of read. */
   const void* bnb_mask;
   int32_t bnb_count;
   int32_t bnb_c_real;

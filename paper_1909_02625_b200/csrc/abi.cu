@@ -78,8 +78,9 @@ extern "C" int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int 
   if (args->bnb_count != 0) {
     if (mode != DSP_IGEMM_DGRAD || args->bnb_count < 0 || args->bnb_count > 2)
       return set_error(DSP_E_INVALID, "dsp_igemm: bnb targets need DGRAD and bnb_count 1 or 2");
-    if (!args->stats || !args->sem || !args->bnb_mask || args->N % 4 || args->out_f32)
-      return set_error(DSP_E_INVALID, "dsp_igemm: bnb needs stats, sem, mask, storage-dtype output and N %% 4 == 0");
+    if (!args->stats || !args->sem || (!args->bnb_mask && args->bnb_count != 1) || args->N % 4 || args->out_f32)
+      return set_error(DSP_E_INVALID,
+                       "dsp_igemm: bnb needs stats, sem, a mask (or one target), storage-dtype output and N %% 4 == 0");
     for (int t = 0; t < args->bnb_count; ++t) {
       const dsp_bnb_target_t& b = args->bnb[t];
       if (!b.y || !b.stat || !b.gamma || !b.dgamma || !b.dbeta || !b.coef)

@@ -352,12 +352,23 @@ int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const voi
   return DSP_OK;
 }
 
+// The ReLU mask of a BN whose output is exactly relu(bn(y)) (stem, intra-unit BNs; not a unit's top
+// BN, which adds the shortcut first): mask_of returns nullptr and the backward kernels recompute
+// the mask from y and the forward's scale / shift instead of reading the stored output -- one
+// tensor read fewer per BN backward pass. DSP_B200_MASK_FROM_Y=0 reads the stored output (A/B).
+const void* mask_of(const void* stored) {
+  static const bool off = getenv("DSP_B200_MASK_FROM_Y") && getenv("DSP_B200_MASK_FROM_Y")[0] == '0';
+  return off ? stored : nullptr;
+}
+
 // Second pass of the BN backward once its statistics (coef, dgamma, dbeta) exist.
+// mask == nullptr: recompute the mask from y (mask_of).
 int bn_backward_apply(dsp_block* b, const void* gsrc, const void* mask, const ConvP& c1, void* dy1, const ConvP* c2,
                       void* dy2, void* g_out, cudaStream_t st) {
   DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, c1.coef), dy1,
                         c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
-                        c2 ? at<float>(b, c2->coef) : nullptr, c2 ? dy2 : nullptr, g_out, c1.M(), c1.g.K, st));
+                        c2 ? at<float>(b, c2->coef) : nullptr, c2 ? dy2 : nullptr, g_out, c1.M(), c1.g.K, st,
+                        mask == nullptr ? 1 : 0));
   return DSP_OK;
 }
 
@@ -369,7 +380,7 @@ int bn_backward_pair(dsp_block* b, const void* gsrc, const void* mask, const Con
   int* sem = at<int32_t>(b, b->sem);
   DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, b->bpart), M, Cp,
                         c1.co_real, b->params + c1.gamma_off, b->grads + c1.gamma_off, b->grads + c1.beta_off,
-                        at<float>(b, c1.coef), sem, st));
+                        at<float>(b, c1.coef), sem, st, mask == nullptr ? 1 : 0));
   if (c2) {
     DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mask, b->ws + c2->y, at<float>(b, c2->stat), at<float>(b, b->bpart2), M, Cp,
                           c2->co_real, b->params + c2->gamma_off, b->grads + c2->gamma_off, b->grads + c2->beta_off,
@@ -494,9 +505,9 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
       const ConvP& c = l.convs[0];
       void* dy = b->ws + b->S[0];
       if (top_done)
-        DSP_TRY(bn_backward_apply(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
+        DSP_TRY(bn_backward_apply(b, u, mask_of(b->ws + l.out), c, dy, nullptr, nullptr, nullptr, st));
       else
-        DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, c, dy, nullptr, nullptr, nullptr, st));
+        DSP_TRY(bn_backward_pair(b, u, mask_of(b->ws + l.out), c, dy, nullptr, nullptr, nullptr, st));
       if (c.s2d_r) {  // WGRAD on the recorded s2d input; DGRAD into its gradient, then back to x's layout
         DSP_TRY(conv_wgrad(b, c, b->ws + c.s2d_buf, dy, st));
         if (dx) {
@@ -534,10 +545,10 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
         // dz_{i}, with the BN-backward statistics of conv i-1 accumulated in the epilogue
         const ConvP& cb = l.convs[i - 1];
         const void* zmask = b->ws + (i == 1 ? l.z1 : l.z2);
-        const BnbFuse fuse{zmask, &cb, nullptr};
+        const BnbFuse fuse{mask_of(zmask), &cb, nullptr};
         DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st, &fuse));
         DSP_TRY(side_join(b, st));  // the WGRAD reading S0 is done before S0 is overwritten
-        DSP_TRY(bn_backward_apply(b, S2, zmask, cb, S0, nullptr, nullptr, nullptr, st));
+        DSP_TRY(bn_backward_apply(b, S2, mask_of(zmask), cb, S0, nullptr, nullptr, nullptr, st));
       }
       const void* res = S1;
       if (cs) {
@@ -894,7 +905,9 @@ extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* gr
     if (i > 0 && dx != nullptr && !s2d && has_top_bn(l) && has_top_bn(b->L[i - 1])) {
       const LayerP& lb = b->L[i - 1];
       const int nmain = lb.d.kind == DSP_LAYER_BOTTLENECK ? 3 : lb.d.kind == DSP_LAYER_BASIC_UNIT ? 2 : 1;
-      fz = BnbFuse{x, &lb.convs[nmain - 1], lb.proj ? &lb.convs[nmain] : nullptr};
+      // a stem below (relu(bn(y)), no shortcut): its mask comes from y too
+      fz = BnbFuse{lb.d.kind == DSP_LAYER_CONV_BN_RELU ? mask_of(x) : x, &lb.convs[nmain - 1],
+                   lb.proj ? &lb.convs[nmain] : nullptr};
       below = &fz;
     }
     DSP_TRY(layer_backward(b, l, x, u, dx, st, below, top_done));

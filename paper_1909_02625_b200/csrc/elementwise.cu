@@ -217,7 +217,7 @@ struct BnBwdFin {  // fused finalize (last CTA) of the BatchNorm-backward reduct
 template <typename T>
 __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                 const float* __restrict__ stat, float* __restrict__ part, int64_t M, int Cp,
-                                int rows_per_chunk, const BnBwdFin fin) {
+                                int rows_per_chunk, const BnBwdFin fin, int relu_y) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   __shared__ float red[kThreads][2 * VE];
@@ -231,11 +231,13 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
   for (int i = 0; i < VE; ++i) s1[i] = s2[i] = 0.f;
   if (tr < TR) {
     const int c0 = cg * VE;
-    float mean[VE], inv[VE];
+    float mean[VE], inv[VE], msc[VE], msh[VE];
 #pragma unroll
     for (int i = 0; i < VE; ++i) {
       mean[i] = y ? stat[c0 + i] : 0.f;
       inv[i] = y ? stat[Cp + c0 + i] : 0.f;
+      msc[i] = relu_y ? stat[2 * Cp + c0 + i] : 0.f;  // mask from y: the forward's relu(y*scale + shift) > 0
+      msh[i] = relu_y ? stat[3 * Cp + c0 + i] : 0.f;
     }
     const int64_t r0 = (int64_t)blockIdx.x * rows_per_chunk;
     const int64_t r1 = min(M, r0 + rows_per_chunk);
@@ -268,6 +270,10 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
         if (y != nullptr) {
           float yy[VE];
           cvt16<T>(ry[u], yy);
+          if (relu_y) {
+#pragma unroll
+            for (int i = 0; i < VE; ++i) g[i] = fmaf(yy[i], msc[i], msh[i]) > 0.f ? g[i] : 0.f;
+          }
 #pragma unroll
           for (int i = 0; i < VE; ++i) {
             s1[i] += g[i];
@@ -362,7 +368,7 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp) {
+                               int64_t nvec, int Cp, int relu_y) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -371,7 +377,7 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
   //   dy = c0 * (g - c1 - (y - mean) * (invstd * c2))
   const int CV = Cp / VE;
   const bool fixc = (blockDim.x % CV) == 0;
-  float k0[VE], k1[VE], km[VE], kq[VE];
+  float k0[VE], k1[VE], km[VE], kq[VE], ms[VE], mh[VE];
   auto coeffs = [&](int c0) {
 #pragma unroll
     for (int i = 0; i < VE; ++i) {
@@ -380,6 +386,8 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
       k1[i] = coef[Cp + c];
       km[i] = stat[c];
       kq[i] = stat[Cp + c] * coef[2 * Cp + c];
+      ms[i] = relu_y ? stat[2 * Cp + c] : 0.f;  // mask from y (relu_y): relu(y*scale + shift) > 0
+      mh[i] = relu_y ? stat[3 * Cp + c] : 0.f;
     }
   };
   if (fixc) coeffs((threadIdx.x % CV) * VE);
@@ -411,10 +419,14 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
 #pragma unroll
         for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
       }
-      if (gout != nullptr) st16(gout + e0, g);
       {
         float yy[VE], o[VE];
         cvt16<T>(ry[u], yy);
+        if (relu_y) {
+#pragma unroll
+          for (int i = 0; i < VE; ++i) g[i] = fmaf(yy[i], ms[i], mh[i]) > 0.f ? g[i] : 0.f;
+        }
+        if (gout != nullptr) st16(gout + e0, g);
 #pragma unroll
         for (int i = 0; i < VE; ++i) o[i] = k0[i] * (g[i] - k1[i] - (yy[i] - km[i]) * kq[i]);
         st16(dy + e0, o);
@@ -440,16 +452,16 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp) {
-  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp);
+                               int64_t nvec, int Cp, int relu_y) {
+  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y);
 }
 template <typename T, int UNR, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) bn_bwd_apply_k_lb(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp) {
-  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp);
+                               int64_t nvec, int Cp, int relu_y) {
+  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y);
 }
 
 // Tensors within one wave (CIFAR shapes, one vector per thread): the plain form -- per-vector
@@ -493,7 +505,7 @@ __global__ void bn_bwd_apply_small_k(const T* __restrict__ gsrc, const T* __rest
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp) {
+                               int64_t nvec, int Cp, int relu_y) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -507,10 +519,15 @@ __global__ void bn_bwd_apply_small_k(const T* __restrict__ gsrc, const T* __rest
 #pragma unroll
       for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
     }
-    if (gout != nullptr) st16(gout + e0, g);
     {
       float yy[VE], o[VE];
       ld16(y + e0, yy);
+      if (relu_y) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i)
+          g[i] = fmaf(yy[i], stat[2 * Cp + c0 + i], stat[3 * Cp + c0 + i]) > 0.f ? g[i] : 0.f;
+      }
+      if (gout != nullptr) st16(gout + e0, g);
 #pragma unroll
       for (int i = 0; i < VE; ++i) {
         const int c = c0 + i;
@@ -1320,21 +1337,21 @@ static int64_t bn_rows_per_chunk(int64_t M, int Cp) {
 }
 
 cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
-                          int64_t M, int Cp, cudaStream_t st) {
+                          int64_t M, int Cp, cudaStream_t st, int relu_y) {
   const int chunks = bn_bwd_chunks(M, Cp);
   const int rows = (int)bn_rows_per_chunk(M, Cp);
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
-                                                    rows, BnBwdFin{});
+             rows, BnBwdFin{}, relu_y);
     return note_launch(), cudaGetLastError();
   });
 }
 
 cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
                          int64_t M, int Cp, int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef,
-                         int* sem, cudaStream_t st) {
+                         int* sem, cudaStream_t st, int relu_y) {
   const int chunks = bn_bwd_chunks(M, Cp);
   const int rows = (int)bn_rows_per_chunk(M, Cp);
   const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sem};
@@ -1342,7 +1359,7 @@ cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const vo
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
-                                                    rows, fin);
+             rows, fin, relu_y);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -1355,7 +1372,7 @@ cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, i
 
 cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
                          const float* coef, void* dy, const void* y_b, const float* stat_b, const float* coef_b,
-                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st) {
+                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st, int relu_y) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
@@ -1365,7 +1382,7 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
     static const int var = getenv("DSP_B200_BNB") ? atoi(getenv("DSP_B200_BNB")) : 13;
     auto go = [&](auto kern) {
       launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef, (T*)dy,
-               (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
+               (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y);
     };
     if (nvec > kWave) {
       if (var == 23) go(bn_bwd_apply_k_lb<T, 2, 3>);
@@ -1376,7 +1393,7 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
     }
     else
       launch_k(bn_bwd_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y,
-               stat, coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp);
+               stat, coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y);
     return note_launch(), cudaGetLastError();
   });
 }

@@ -405,6 +405,12 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           bst[t][0][c] = ok ? a.bnb[t].stat[n0c + c] : 0.f;
           bst[t][1][c] = ok ? a.bnb[t].stat[N + n0c + c] : 0.f;
         }
+      if (a.bnb_mask == nullptr)  // one target, mask from y: its scale / shift in the unused second slot
+        for (int c = lane; c < BN; c += 32) {
+          const bool ok = n0c + c < N;
+          bst[1][0][c] = ok ? a.bnb[0].stat[2 * N + n0c + c] : 0.f;
+          bst[1][1][c] = ok ? a.bnb[0].stat[3 * N + n0c + c] : 0.f;
+        }
     }
   }
   tc_fence_before();
@@ -1052,7 +1058,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const size_t o = (size_t)(rbase + rh + 2 * (h8 + it)) * a.ldd + cofs;
-              mk[it] = __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb_mask) + o));
+              mk[it] = a.bnb_mask != nullptr
+                           ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb_mask) + o)) : 0u;
               y0[it] = __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[0].y) + o));
               y1[it] = nbt > 1 ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[1].y) + o)) : 0u;
             }
@@ -1063,8 +1070,13 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
               asm volatile("ld.shared.b32 %0, [%1];"
                            : "=r"(w)
                            : "r"(sDW + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4));
-              const float ga = __uint_as_float(mk[it] << 16) > 0.f ? __uint_as_float(w << 16) : 0.f;
-              const float gb = __uint_as_float(mk[it] & 0xffff0000u) > 0.f ? __uint_as_float(w & 0xffff0000u) : 0.f;
+              // mask: the stored BN output (> 0), or recomputed from y as relu(y*scale + shift) > 0
+              const bool pa = a.bnb_mask != nullptr ? __uint_as_float(mk[it] << 16) > 0.f
+                                                    : fmaf(__uint_as_float(y0[it] << 16), m1a, i1a) > 0.f;
+              const bool pb = a.bnb_mask != nullptr ? __uint_as_float(mk[it] & 0xffff0000u) > 0.f
+                                                    : fmaf(__uint_as_float(y0[it] & 0xffff0000u), m1b, i1b) > 0.f;
+              const float ga = pa ? __uint_as_float(w << 16) : 0.f;
+              const float gb = pb ? __uint_as_float(w & 0xffff0000u) : 0.f;
               s1a += ga;
               s1b += gb;
               s2a += ga * ((__uint_as_float(y0[it] << 16) - m0a) * i0a);
@@ -1331,15 +1343,18 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
             // g = stored dX * (mask > 0); xhat_t = (y_t - mean_t) * invstd_t of the BN below
             const int cl = cc * 16;  // column within the CTA's n-tile
             float g[16], pr[16];
-            {
+            float yv[16];
+            ld_row16<T>(a.bnb[0].y, mok, mr, a.ldd, nb, N, yv);
+            if (a.bnb_mask != nullptr) {
               float mk[16];
               ld_row16<T>(a.bnb_mask, mok, mr, a.ldd, nb, N, mk);
 #pragma unroll
               for (int e = 0; e < 16; ++e) g[e] = mk[e] > 0.f ? v[e] : 0.f;
+            } else {  // mask from y (one target): relu(y*scale + shift) > 0
+#pragma unroll
+              for (int e = 0; e < 16; ++e) g[e] = fmaf(yv[e], bst[1][0][cl + e], bst[1][1][cl + e]) > 0.f ? v[e] : 0.f;
             }
             const float s1 = colsum16(g, lane);
-            float yv[16];
-            ld_row16<T>(a.bnb[0].y, mok, mr, a.ldd, nb, N, yv);
 #pragma unroll
             for (int e = 0; e < 16; ++e) pr[e] = g[e] * ((yv[e] - bst[0][0][cl + e]) * bst[0][1][cl + e]);
             const float s2 = colsum16(pr, lane);

@@ -29,14 +29,17 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
 // xhat = (y - mean) * invstd (if y != null, else 0).  Writes per-chunk
 // partial (sum g, sum g*xhat) [chunks][2][Cp]; returns the chunk count.
 int bn_bwd_chunks(int64_t M, int Cp);
+// relu_y (mask == nullptr): the ReLU mask is recomputed from y as relu(y*scale + shift) > 0 with the
+// forward's scale / shift (stat rows 2, 3) -- for BNs whose output is exactly relu(bn(y)) (no
+// residual), so the backward never reads the stored BN output.
 cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
-                          float* part, int64_t M, int Cp, cudaStream_t st);
+                          float* part, int64_t M, int Cp, cudaStream_t st, int relu_y = 0);
 // Reduction + finalize in one launch: the last CTA to finish (atomic ticket on
 // *sem, which must be 0 and is left 0) sums the partials in fixed order and
 // writes dgamma/dbeta/coef exactly like bn_bwd_finalize.
 cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
                          int64_t M, int Cp, int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef,
-                         int* sem, cudaStream_t st);
+                         int* sem, cudaStream_t st, int relu_y = 0);
 // Finalize: sum partials -> dgamma/dbeta into the flat grad (if non-null) and
 // coefficients coef[0]=gamma*invstd, coef[1]=sum(g)/M, coef[2]=sum(g*xhat)/M.
 // With gamma == null (bias gradient) only dbeta = sum(g) is produced.
@@ -46,7 +49,7 @@ cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, i
 // sharing g; optional g_out = g.
 cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
                          const float* coef, void* dy, const void* y_b, const float* stat_b, const float* coef_b,
-                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st);
+                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st, int relu_y = 0);
 
 // Dense activations (tensor.py:59-83): out = relu/tanh(x); dx = u * act'(x).
 cudaError_t act_forward(int dtype, int tanh_kind, const void* x, void* out, int64_t n, cudaStream_t st);

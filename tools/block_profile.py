@@ -34,19 +34,28 @@ def main():
     ap.add_argument("--block", default="r50s1", choices=sorted(BLOCKS))
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--r50-block", type=int, default=-1,
+                    help="instead of --block: block k of ResNet-50 cut into K=4 FLOP-balanced blocks (B=256)")
     args = ap.parse_args()
     import torch
 
     from paper_1909_02625_b200 import _lib as L
     from paper_1909_02625_b200.runtime import DeviceBlock
 
-    layers, B = BLOCKS[args.block]
-    layers = layers()
+    if args.r50_block >= 0:
+        full = P.resnet50_layers()
+        cuts = [0] + P.flop_balanced_boundaries(full, 4) + [len(full)]
+        layers, B = full[cuts[args.r50_block]:cuts[args.r50_block + 1]], 256
+        last = args.r50_block == 3
+    else:
+        layers, B = BLOCKS[args.block]
+        layers = layers()
+        last = False
     model = P.build_model(layers, [])
     P.init_params(model, 0)
     dt = L.storage_dtype(args.precision)
     st = torch.cuda.current_stream()
-    db = DeviceBlock(model.blocks[0], B, is_last=False, stream=st, dtype=dt)
+    db = DeviceBlock(model.blocks[0], B, is_last=last, stream=st, dtype=dt)
     tdt = L.torch_storage(dt)
     x = torch.randn(db.in_elems, device="cuda").to(tdt)
     y = torch.empty(db.out_elems, device="cuda", dtype=tdt)
@@ -54,17 +63,24 @@ def main():
     gin = torch.empty(db.in_elems, device="cuda", dtype=tdt)
     ys = db.params.clone()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    labels = torch.zeros(B, dtype=torch.int64, device="cuda")
+    loss = torch.zeros(1, device="cuda")
     for r in range(args.reps):
         if r == args.reps - 1:
             ev[0].record(st)
-        db.forward(x, y, record=False)
+        if not last:
+            db.forward(x, y, record=False)
         db.forward(x, None, record=True)
-        db.backward(up, gin)
+        if last:
+            db.loss(labels, loss)
+        db.backward(None if last else up, gin)
         db.update(L.DSP_RULE_SUM, ys, 1e-3, 1e-3, 0.9, 5e-4, True, None)
         if r == args.reps - 1:
             ev[1].record(st)
     torch.cuda.synchronize()
-    print(f"{args.block}: one fwd + recompute + bwd + update {ev[0].elapsed_time(ev[1]) * 1000:.1f} us")
+    name = f"resnet50 block {args.r50_block}" if args.r50_block >= 0 else args.block
+    print(f"{name}: one fwd + recompute + bwd + update {ev[0].elapsed_time(ev[1]) * 1000:.1f} us "
+          f"({model.blocks[0].param_count} params)")
 
 
 if __name__ == "__main__":
