@@ -126,6 +126,10 @@ typedef struct {
   /* DGRAD (optional): the weights transposed per tap, [Cin_p][R][S][Cout_p] bf16 -- lets
    * stride-1 DGRAD load K-major weight boxes with TMA and use halo tiles like FPROP. */
   const void* B_t;
+  /* DGRAD bnb (optional, bf16, takes precedence over bnb_mask): the mask as bits, one byte per 8
+   * columns of every row ([M][ldd / 8]), bit i = column 8j + i of the BN's output > 0 (what the
+   * forward's BN-apply wrote beside the output). */
+  const uint8_t* bnb_mask_bits;
 } dsp_igemm_args_t;
 
 #define DSP_IGEMM_MAX_CTAS 444

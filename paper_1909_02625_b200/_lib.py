@@ -93,6 +93,7 @@ class IgemmArgs(C.Structure):
         ("bnb_mask", C.c_void_p), ("bnb_count", C.c_int32), ("bnb_c_real", C.c_int32),
         ("bnb", BnbTarget * 2),
         ("B_t", C.c_void_p),
+        ("bnb_mask_bits", C.c_void_p),
     ]
 
 

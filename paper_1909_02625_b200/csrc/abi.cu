@@ -78,7 +78,8 @@ extern "C" int dsp_igemm(int mode, int dtype, const dsp_igemm_args_t* args, int 
   if (args->bnb_count != 0) {
     if (mode != DSP_IGEMM_DGRAD || args->bnb_count < 0 || args->bnb_count > 2)
       return set_error(DSP_E_INVALID, "dsp_igemm: bnb targets need DGRAD and bnb_count 1 or 2");
-    if (!args->stats || !args->sem || (!args->bnb_mask && args->bnb_count != 1) || args->N % 4 || args->out_f32)
+    if (!args->stats || !args->sem || (!args->bnb_mask && !args->bnb_mask_bits && args->bnb_count != 1) ||
+        args->N % 4 || args->out_f32 || (args->bnb_mask_bits && (dtype != DSP_DTYPE_BF16 || args->ldd % 8)))
       return set_error(DSP_E_INVALID,
                        "dsp_igemm: bnb needs stats, sem, a mask (or one target), storage-dtype output and N %% 4 == 0");
     for (int t = 0; t < args->bnb_count; ++t) {

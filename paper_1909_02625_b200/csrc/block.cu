@@ -55,6 +55,7 @@ struct LayerP {
   std::vector<ConvP> convs;
   bool proj = false;
   size_t out = 0, z1 = 0, z2 = 0, arg = 0;
+  size_t mbits = 0;  // residual units (bf16): ReLU mask bits of `out`, one byte per 8 channels (0 = none)
   // dense
   ConvP dense;  // 1x1 conv view of the dense layer
   int64_t b_off = -1;
@@ -311,9 +312,10 @@ int side_join(dsp_block* b, cudaStream_t st) {
 
 // The BatchNorm below a DGRAD output whose backward statistics the DGRAD epilogue computes.
 struct BnbFuse {
-  const void* mask;  // ReLU mask tensor (the BN's stored output)
+  const void* mask;  // ReLU mask tensor (the BN's stored output); nullptr: from y (mask_of)
   const ConvP* c1;   // the BN's conv (its y / stat / coef / gamma, beta grads)
   const ConvP* c2;   // optional second BN sharing g (projection shortcut)
+  const uint8_t* bits = nullptr;  // the mask as bits (a residual unit's output), read instead
 };
 
 void set_bnb_target(dsp_block* b, const ConvP& c, dsp_bnb_target_t& t) {
@@ -342,7 +344,8 @@ int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const voi
   if (fuse != nullptr) {
     a.stats = at<float>(b, b->fpart);
     a.sem = at<int32_t>(b, b->sem);
-    a.bnb_mask = fuse->mask;
+    a.bnb_mask = fuse->bits ? nullptr : fuse->mask;
+    a.bnb_mask_bits = fuse->bits;
     a.bnb_count = fuse->c2 ? 2 : 1;
     a.bnb_c_real = fuse->c1->co_real;
     set_bnb_target(b, *fuse->c1, a.bnb[0]);
@@ -363,30 +366,32 @@ const void* mask_of(const void* stored) {
 
 // Second pass of the BN backward once its statistics (coef, dgamma, dbeta) exist.
 // mask == nullptr: recompute the mask from y (mask_of).
+// mbits (optional): the mask as bits (a residual unit's output, LayerP.mbits) -- read instead of `mask`.
 int bn_backward_apply(dsp_block* b, const void* gsrc, const void* mask, const ConvP& c1, void* dy1, const ConvP* c2,
-                      void* dy2, void* g_out, cudaStream_t st) {
-  DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, c1.coef), dy1,
-                        c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
+                      void* dy2, void* g_out, cudaStream_t st, const uint8_t* mbits = nullptr) {
+  DSP_CUDA(bn_bwd_apply(b->dtype, gsrc, mbits ? nullptr : mask, b->ws + c1.y, at<float>(b, c1.stat),
+                        at<float>(b, c1.coef), dy1, c2 ? b->ws + c2->y : nullptr, c2 ? at<float>(b, c2->stat) : nullptr,
                         c2 ? at<float>(b, c2->coef) : nullptr, c2 ? dy2 : nullptr, g_out, c1.M(), c1.g.K, st,
-                        mask == nullptr ? 1 : 0));
+                        (mask == nullptr && mbits == nullptr) ? 1 : 0, mbits));
   return DSP_OK;
 }
 
 // BN backward for one conv: dy = BNback(g = gsrc*(mask>0)), grads into params layout.
 int bn_backward_pair(dsp_block* b, const void* gsrc, const void* mask, const ConvP& c1, void* dy1, const ConvP* c2,
-                     void* dy2, void* g_out, cudaStream_t st) {
+                     void* dy2, void* g_out, cudaStream_t st, const uint8_t* mbits = nullptr) {
   const int64_t M = c1.M();
   const int Cp = c1.g.K;
   int* sem = at<int32_t>(b, b->sem);
-  DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mask, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, b->bpart), M, Cp,
+  const void* mk = mbits ? nullptr : mask;
+  DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mk, b->ws + c1.y, at<float>(b, c1.stat), at<float>(b, b->bpart), M, Cp,
                         c1.co_real, b->params + c1.gamma_off, b->grads + c1.gamma_off, b->grads + c1.beta_off,
-                        at<float>(b, c1.coef), sem, st, mask == nullptr ? 1 : 0));
+                        at<float>(b, c1.coef), sem, st, (mask == nullptr && mbits == nullptr) ? 1 : 0, mbits));
   if (c2) {
-    DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mask, b->ws + c2->y, at<float>(b, c2->stat), at<float>(b, b->bpart2), M, Cp,
+    DSP_CUDA(bn_bwd_stats(b->dtype, gsrc, mk, b->ws + c2->y, at<float>(b, c2->stat), at<float>(b, b->bpart2), M, Cp,
                           c2->co_real, b->params + c2->gamma_off, b->grads + c2->gamma_off, b->grads + c2->beta_off,
-                          at<float>(b, c2->coef), sem, st));
+                          at<float>(b, c2->coef), sem, st, 0, mbits));
   }
-  return bn_backward_apply(b, gsrc, mask, c1, dy1, c2, dy2, g_out, st);
+  return bn_backward_apply(b, gsrc, mask, c1, dy1, c2, dy2, g_out, st, mbits);
 }
 
 // ------------------------------------------------------------------ layer forward / backward
@@ -444,13 +449,14 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
       }
       const ConvP& cl = l.convs[nmain - 1];
       DSP_TRY(conv_fprop(b, cl, cur, st));
+      uint8_t* mb = l.mbits ? at<uint8_t>(b, l.mbits) : nullptr;
       if (l.proj) {
         const ConvP& cs = l.convs[nmain];
         DSP_TRY(conv_fprop(b, cs, x, st));
         DSP_CUDA(bn_apply(dt, b->ws + cl.y, at<float>(b, cl.stat), nullptr, b->ws + cs.y, at<float>(b, cs.stat), out,
-                          cl.M(), cl.g.K, 1, st));
+                          cl.M(), cl.g.K, 1, st, mb));
       } else {
-        DSP_CUDA(bn_apply(dt, b->ws + cl.y, at<float>(b, cl.stat), x, nullptr, nullptr, out, cl.M(), cl.g.K, 1, st));
+        DSP_CUDA(bn_apply(dt, b->ws + cl.y, at<float>(b, cl.stat), x, nullptr, nullptr, out, cl.M(), cl.g.K, 1, st, mb));
       }
       return DSP_OK;
     }
@@ -532,10 +538,11 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
       const ConvP& cl = l.convs[nmain - 1];
       const ConvP* cs = l.proj ? &l.convs[nmain] : nullptr;
       // top BN(s): g = u * (out > 0); dy_last -> S0, dy_sc -> S1 (proj) or g -> S1 (identity)
+      const uint8_t* mb = l.mbits ? at<uint8_t>(b, l.mbits) : nullptr;
       if (top_done)
-        DSP_TRY(bn_backward_apply(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st));
+        DSP_TRY(bn_backward_apply(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st, mb));
       else
-        DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st));
+        DSP_TRY(bn_backward_pair(b, u, b->ws + l.out, cl, S0, cs, cs ? S1 : nullptr, cs ? nullptr : S1, st, mb));
       // walk the main path down
       for (int i = nmain - 1; i >= 0; --i) {
         const ConvP& c = l.convs[i];
@@ -762,6 +769,8 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
       if (c.s2d_r) c.s2d_buf = pl.take((size_t)c.Min() * c.g.C * b->esz);
     }
     if (l.d.kind == DSP_LAYER_BASIC_UNIT || l.d.kind == DSP_LAYER_BOTTLENECK) {
+      static const bool no_bits = getenv("DSP_B200_MASK_BITS") && getenv("DSP_B200_MASK_BITS")[0] == '0';
+      if (dtype == DSP_DTYPE_BF16 && !no_bits) l.mbits = pl.take((size_t)l.out_elems() / 8);
       l.z1 = pl.take((size_t)l.convs[0].M() * l.convs[0].g.K * b->esz);
       if (l.d.kind == DSP_LAYER_BOTTLENECK) l.z2 = pl.take((size_t)l.convs[1].M() * l.convs[1].g.K * b->esz);
     }
@@ -907,7 +916,7 @@ extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* gr
       const int nmain = lb.d.kind == DSP_LAYER_BOTTLENECK ? 3 : lb.d.kind == DSP_LAYER_BASIC_UNIT ? 2 : 1;
       // a stem below (relu(bn(y)), no shortcut): its mask comes from y too
       fz = BnbFuse{lb.d.kind == DSP_LAYER_CONV_BN_RELU ? mask_of(x) : x, &lb.convs[nmain - 1],
-                   lb.proj ? &lb.convs[nmain] : nullptr};
+                   lb.proj ? &lb.convs[nmain] : nullptr, lb.mbits ? at<uint8_t>(b, lb.mbits) : nullptr};
       below = &fz;
     }
     DSP_TRY(layer_backward(b, l, x, u, dx, st, below, top_done));

@@ -113,10 +113,19 @@ __global__ void bn_finalize_k(const float* __restrict__ part, int tiles, int Cp,
   }
 }
 
+// ReLU mask bits of one 8-element vector (bf16): bit i = the STORED value > 0
+template <typename T>
+__device__ __forceinline__ uint8_t mask_byte(const float (&a)[V16<T>::N]) {
+  uint32_t b = 0;
+#pragma unroll
+  for (int i = 0; i < V16<T>::N; ++i) b |= (to_f<T>(from_f<T>(a[i])) > 0.f ? 1u : 0u) << i;
+  return (uint8_t)b;
+}
+
 template <typename T, int UNR>
 __device__ __forceinline__ void bn_apply_k_body(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
-                           int64_t nvec, int Cp, int relu) {
+                           int64_t nvec, int Cp, int relu, uint8_t* __restrict__ mbits) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -183,6 +192,7 @@ __device__ __forceinline__ void bn_apply_k_body(const T* __restrict__ y, const f
         for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
       }
       st16(out + e0, a);
+      if (mbits != nullptr) mbits[v] = mask_byte<T>(a);  // bf16: one byte per vector
     }
   }
 }
@@ -191,14 +201,14 @@ __device__ __forceinline__ void bn_apply_k_body(const T* __restrict__ y, const f
 template <typename T, int UNR>
 __global__ void bn_apply_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
-                           int64_t nvec, int Cp, int relu) {
-  bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu);
+                           int64_t nvec, int Cp, int relu, uint8_t* __restrict__ mbits) {
+  bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu, mbits);
 }
 template <typename T, int UNR, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) bn_apply_k_lb(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
-                           int64_t nvec, int Cp, int relu) {
-  bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu);
+                           int64_t nvec, int Cp, int relu, uint8_t* __restrict__ mbits) {
+  bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu, mbits);
 }
 
 // ------------------------------------------------------------------ BatchNorm backward
@@ -217,7 +227,8 @@ struct BnBwdFin {  // fused finalize (last CTA) of the BatchNorm-backward reduct
 template <typename T>
 __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                 const float* __restrict__ stat, float* __restrict__ part, int64_t M, int Cp,
-                                int rows_per_chunk, const BnBwdFin fin, int relu_y) {
+                                int rows_per_chunk, const BnBwdFin fin, int relu_y,
+                                const uint8_t* __restrict__ mbits) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   __shared__ float red[kThreads][2 * VE];
@@ -246,13 +257,15 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
     constexpr int RU = 4;
     for (int64_t rb = r0 + tr; rb < r1; rb += (int64_t)TR * RU) {
       uint4 rg[RU], rm[RU], ry[RU];
+      uint32_t rb8[RU];
 #pragma unroll
       for (int u = 0; u < RU; ++u) {
         const int64_t r = rb + (int64_t)u * TR;
         if (r < r1) {
           const int64_t e0 = r * Cp + c0;
           rg[u] = ldraw(gsrc + e0);
-          if (mask != nullptr) rm[u] = ldraw(mask + e0);
+          if (mbits != nullptr) rb8[u] = mbits[e0 / 8];
+          else if (mask != nullptr) rm[u] = ldraw(mask + e0);
           if (y != nullptr) ry[u] = ldraw(y + e0);
         }
       }
@@ -261,7 +274,10 @@ __global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict_
         if (rb + (int64_t)u * TR >= r1) break;
         float g[VE];
         cvt16<T>(rg[u], g);
-        if (mask != nullptr) {
+        if (mbits != nullptr) {
+#pragma unroll
+          for (int i = 0; i < VE; ++i) g[i] = (rb8[u] >> i) & 1u ? g[i] : 0.f;
+        } else if (mask != nullptr) {
           float mk[VE];
           cvt16<T>(rm[u], mk);
 #pragma unroll
@@ -368,7 +384,7 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp, int relu_y) {
+                               int64_t nvec, int Cp, int relu_y, const uint8_t* __restrict__ mbits) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -393,12 +409,14 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
   if (fixc) coeffs((threadIdx.x % CV) * VE);
   for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * UNR) {
     uint4 rg[UNR], rm[UNR], ry[UNR], rb[UNR];
+    uint32_t rb8[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {  // every load of the pass first
       const int64_t v = v0 + u * stride;
       if (v < nvec) {
         rg[u] = ldraw(gsrc + v * VE);
-        if (mask != nullptr) rm[u] = ldraw(mask + v * VE);
+        if (mbits != nullptr) rb8[u] = mbits[v];  // bf16: one mask byte per vector
+        else if (mask != nullptr) rm[u] = ldraw(mask + v * VE);
         ry[u] = ldraw(y + v * VE);
         if (dyb != nullptr) rb[u] = ldraw(yb + v * VE);
       }
@@ -413,7 +431,10 @@ __device__ __forceinline__ void bn_bwd_apply_k_body(const T* __restrict__ gsrc, 
       if (!fixc) coeffs(c0);
       float g[VE];
       cvt16<T>(rg[u], g);
-      if (mask != nullptr) {
+      if (mbits != nullptr) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) g[i] = (rb8[u] >> i) & 1u ? g[i] : 0.f;
+      } else if (mask != nullptr) {
         float mk[VE];
         cvt16<T>(rm[u], mk);
 #pragma unroll
@@ -452,16 +473,16 @@ __global__ void bn_bwd_apply_k(const T* __restrict__ gsrc, const T* __restrict__
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp, int relu_y) {
-  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y);
+                               int64_t nvec, int Cp, int relu_y, const uint8_t* __restrict__ mbits) {
+  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y, mbits);
 }
 template <typename T, int UNR, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) bn_bwd_apply_k_lb(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp, int relu_y) {
-  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y);
+                               int64_t nvec, int Cp, int relu_y, const uint8_t* __restrict__ mbits) {
+  bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y, mbits);
 }
 
 // Tensors within one wave (CIFAR shapes, one vector per thread): the plain form -- per-vector
@@ -470,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, MINB) bn_bwd_apply_k_lb(const T* __r
 template <typename T>
 __global__ void bn_apply_small_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
                            const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out,
-                           int64_t nvec, int Cp, int relu) {
+                           int64_t nvec, int Cp, int relu, uint8_t* __restrict__ mbits) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -497,6 +518,7 @@ __global__ void bn_apply_small_k(const T* __restrict__ y, const float* __restric
       for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
     }
     st16(out + e0, a);
+    if (mbits != nullptr) mbits[v] = mask_byte<T>(a);
   }
 }
 
@@ -505,7 +527,7 @@ __global__ void bn_bwd_apply_small_k(const T* __restrict__ gsrc, const T* __rest
                                const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
                                const T* __restrict__ yb, const float* __restrict__ statb,
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
-                               int64_t nvec, int Cp, int relu_y) {
+                               int64_t nvec, int Cp, int relu_y, const uint8_t* __restrict__ mbits) {
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -513,7 +535,11 @@ __global__ void bn_bwd_apply_small_k(const T* __restrict__ gsrc, const T* __rest
     const int c0 = (int)(e0 % Cp);
     float g[VE];
     ld16(gsrc + e0, g);
-    if (mask != nullptr) {
+    if (mbits != nullptr) {
+      const uint32_t b8 = mbits[v];
+#pragma unroll
+      for (int i = 0; i < VE; ++i) g[i] = (b8 >> i) & 1u ? g[i] : 0.f;
+    } else if (mask != nullptr) {
       float mk[VE];
       ld16(mask + e0, mk);
 #pragma unroll
@@ -1295,10 +1321,11 @@ cudaError_t bn_finalize(const float* part, int tiles, int Cp, int c_real, int64_
 }
 
 cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* res, const void* y2, const float* stat2,
-                     void* out, int64_t M, int Cp, int relu, cudaStream_t st) {
+                     void* out, int64_t M, int Cp, int relu, cudaStream_t st, uint8_t* mbits) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
+    if (mbits != nullptr && V16<T>::N != 8) return cudaErrorInvalidValue;  // mask bytes: 8 channels (bf16)
     // variant (UNR x min CTAs per SM) via DSP_B200_BNA = 10*UNR + MINB (A/B knob). ncu on
     // ResNet-50: the unbounded UNR-4 form took 117 registers -> 2 CTAs/SM, 24% warps active,
     // 44-59% of DRAM peak; one vector per thread per pass at 4 CTAs/SM measured +1.6%
@@ -1306,7 +1333,7 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
     static const int var = getenv("DSP_B200_BNA") ? atoi(getenv("DSP_B200_BNA")) : 13;
     auto go = [&](auto kern) {
       launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
-               nvec, Cp, relu);
+               nvec, Cp, relu, mbits);
     };
     if (nvec > kWave) {
       if (var == 23) go(bn_apply_k_lb<T, 2, 3>);
@@ -1317,7 +1344,7 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
     }
     else
       launch_k(bn_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2,
-               stat2, (T*)out, nvec, Cp, relu);
+               stat2, (T*)out, nvec, Cp, relu, mbits);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -1337,21 +1364,21 @@ static int64_t bn_rows_per_chunk(int64_t M, int Cp) {
 }
 
 cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
-                          int64_t M, int Cp, cudaStream_t st, int relu_y) {
+                          int64_t M, int Cp, cudaStream_t st, int relu_y, const uint8_t* mbits) {
   const int chunks = bn_bwd_chunks(M, Cp);
   const int rows = (int)bn_rows_per_chunk(M, Cp);
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
-             rows, BnBwdFin{}, relu_y);
+             rows, BnBwdFin{}, relu_y, mbits);
     return note_launch(), cudaGetLastError();
   });
 }
 
 cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
                          int64_t M, int Cp, int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef,
-                         int* sem, cudaStream_t st, int relu_y) {
+                         int* sem, cudaStream_t st, int relu_y, const uint8_t* mbits) {
   const int chunks = bn_bwd_chunks(M, Cp);
   const int rows = (int)bn_rows_per_chunk(M, Cp);
   const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sem};
@@ -1359,7 +1386,7 @@ cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const vo
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
-             rows, fin, relu_y);
+             rows, fin, relu_y, mbits);
     return note_launch(), cudaGetLastError();
   });
 }
@@ -1372,7 +1399,8 @@ cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, i
 
 cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
                          const float* coef, void* dy, const void* y_b, const float* stat_b, const float* coef_b,
-                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st, int relu_y) {
+                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st, int relu_y,
+                         const uint8_t* mbits) {
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     const int64_t nvec = M * Cp / V16<T>::N;
@@ -1382,7 +1410,7 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
     static const int var = getenv("DSP_B200_BNB") ? atoi(getenv("DSP_B200_BNB")) : 13;
     auto go = [&](auto kern) {
       launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef, (T*)dy,
-               (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y);
+               (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y, mbits);
     };
     if (nvec > kWave) {
       if (var == 23) go(bn_bwd_apply_k_lb<T, 2, 3>);
@@ -1393,7 +1421,7 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
     }
     else
       launch_k(bn_bwd_apply_small_k<T>, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y,
-               stat, coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y);
+               stat, coef, (T*)dy, (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y, mbits);
     return note_launch(), cudaGetLastError();
   });
 }

@@ -405,7 +405,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           bst[t][0][c] = ok ? a.bnb[t].stat[n0c + c] : 0.f;
           bst[t][1][c] = ok ? a.bnb[t].stat[N + n0c + c] : 0.f;
         }
-      if (a.bnb_mask == nullptr)  // one target, mask from y: its scale / shift in the unused second slot
+      if (a.bnb_mask == nullptr && a.bnb_mask_bits == nullptr)  // one target, mask from y: its scale / shift
+                                                                 // in the unused second slot
         for (int c = lane; c < BN; c += 32) {
           const bool ok = n0c + c < N;
           bst[1][0][c] = ok ? a.bnb[0].stat[2 * N + n0c + c] : 0.f;
@@ -1055,10 +1056,13 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll 1
             for (int h8 = 0; h8 < 16; h8 += 8) {  // 8 rows' loads in flight at a time (register cap)
             uint32_t mk[8], y0[8], y1[8];
+            const bool mbits = a.bnb_mask_bits != nullptr;
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const size_t o = (size_t)(rbase + rh + 2 * (h8 + it)) * a.ldd + cofs;
-              mk[it] = a.bnb_mask != nullptr
+              // mask bits: the byte of the column pair's 8-column group, shifted so bits 0/1 are the pair
+              mk[it] = mbits ? (uint32_t)__ldg(a.bnb_mask_bits + (o >> 3)) >> (o & 7)
+                       : a.bnb_mask != nullptr
                            ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb_mask) + o)) : 0u;
               y0[it] = __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[0].y) + o));
               y1[it] = nbt > 1 ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[1].y) + o)) : 0u;
@@ -1071,10 +1075,12 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                            : "=r"(w)
                            : "r"(sDW + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4));
               // mask: the stored BN output (> 0), or recomputed from y as relu(y*scale + shift) > 0
-              const bool pa = a.bnb_mask != nullptr ? __uint_as_float(mk[it] << 16) > 0.f
-                                                    : fmaf(__uint_as_float(y0[it] << 16), m1a, i1a) > 0.f;
-              const bool pb = a.bnb_mask != nullptr ? __uint_as_float(mk[it] & 0xffff0000u) > 0.f
-                                                    : fmaf(__uint_as_float(y0[it] & 0xffff0000u), m1b, i1b) > 0.f;
+              const bool pa = mbits ? (mk[it] & 1u) != 0u
+                              : a.bnb_mask != nullptr ? __uint_as_float(mk[it] << 16) > 0.f
+                                                      : fmaf(__uint_as_float(y0[it] << 16), m1a, i1a) > 0.f;
+              const bool pb = mbits ? (mk[it] & 2u) != 0u
+                              : a.bnb_mask != nullptr ? __uint_as_float(mk[it] & 0xffff0000u) > 0.f
+                                                      : fmaf(__uint_as_float(y0[it] & 0xffff0000u), m1b, i1b) > 0.f;
               const float ga = pa ? __uint_as_float(w << 16) : 0.f;
               const float gb = pb ? __uint_as_float(w & 0xffff0000u) : 0.f;
               s1a += ga;
@@ -1345,7 +1351,13 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
             float g[16], pr[16];
             float yv[16];
             ld_row16<T>(a.bnb[0].y, mok, mr, a.ldd, nb, N, yv);
-            if (a.bnb_mask != nullptr) {
+            if (a.bnb_mask_bits != nullptr) {  // two mask bytes: columns nb .. nb + 15 of row mr
+              const uint32_t b16 = mok ? (uint32_t)a.bnb_mask_bits[((size_t)mr * a.ldd + nb) >> 3] |
+                                             ((uint32_t)a.bnb_mask_bits[(((size_t)mr * a.ldd + nb) >> 3) + 1] << 8)
+                                       : 0u;
+#pragma unroll
+              for (int e = 0; e < 16; ++e) g[e] = (b16 >> e) & 1u ? v[e] : 0.f;
+            } else if (a.bnb_mask != nullptr) {
               float mk[16];
               ld_row16<T>(a.bnb_mask, mok, mr, a.ldd, nb, N, mk);
 #pragma unroll

@@ -22,8 +22,11 @@ cudaError_t bn_finalize(const float* part, int tiles, int Cp, int c_real, int64_
                         const float* beta, float* stat, cudaStream_t st);
 
 // out = act(y*scale + shift  [+ res]  [+ y2*scale2 + shift2]); act = relu if relu.
+// mbits (optional, bf16): one byte per 8 channels of every row, bit i = stored out > 0 -- the ReLU
+// mask the backward reads instead of the 16-byte output vector.
 cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* res, const void* y2,
-                     const float* stat2, void* out, int64_t M, int Cp, int relu, cudaStream_t st);
+                     const float* stat2, void* out, int64_t M, int Cp, int relu, cudaStream_t st,
+                     uint8_t* mbits = nullptr);
 
 // BatchNorm backward, reduction half: g = gsrc * (mask > 0 if mask);
 // xhat = (y - mean) * invstd (if y != null, else 0).  Writes per-chunk
@@ -33,13 +36,14 @@ int bn_bwd_chunks(int64_t M, int Cp);
 // forward's scale / shift (stat rows 2, 3) -- for BNs whose output is exactly relu(bn(y)) (no
 // residual), so the backward never reads the stored BN output.
 cudaError_t bn_bwd_reduce(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
-                          float* part, int64_t M, int Cp, cudaStream_t st, int relu_y = 0);
+                          float* part, int64_t M, int Cp, cudaStream_t st, int relu_y = 0,
+                          const uint8_t* mbits = nullptr);
 // Reduction + finalize in one launch: the last CTA to finish (atomic ticket on
 // *sem, which must be 0 and is left 0) sums the partials in fixed order and
 // writes dgamma/dbeta/coef exactly like bn_bwd_finalize.
 cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat, float* part,
                          int64_t M, int Cp, int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef,
-                         int* sem, cudaStream_t st, int relu_y = 0);
+                         int* sem, cudaStream_t st, int relu_y = 0, const uint8_t* mbits = nullptr);
 // Finalize: sum partials -> dgamma/dbeta into the flat grad (if non-null) and
 // coefficients coef[0]=gamma*invstd, coef[1]=sum(g)/M, coef[2]=sum(g*xhat)/M.
 // With gamma == null (bias gradient) only dbeta = sum(g) is produced.
@@ -49,7 +53,8 @@ cudaError_t bn_bwd_finalize(const float* part, int chunks, int Cp, int c_real, i
 // sharing g; optional g_out = g.
 cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const void* y, const float* stat,
                          const float* coef, void* dy, const void* y_b, const float* stat_b, const float* coef_b,
-                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st, int relu_y = 0);
+                         void* dy_b, void* g_out, int64_t M, int Cp, cudaStream_t st, int relu_y = 0,
+                         const uint8_t* mbits = nullptr);
 
 // Dense activations (tensor.py:59-83): out = relu/tanh(x); dx = u * act'(x).
 cudaError_t act_forward(int dtype, int tanh_kind, const void* x, void* out, int64_t n, cudaStream_t st);
