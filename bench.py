@@ -621,7 +621,7 @@ def conv_tensor_pipe(torch, peaks, batch: int):
         gamma, beta = torch.ones(K, device="cuda"), torch.zeros(K, device="cuda")
         stats = torch.empty(L.IGEMM_MAX_CTAS * 3 * K, device="cuda")
         stat_out = torch.empty(4 * K, device="cuda")
-        sem = torch.zeros(64, dtype=torch.int32, device="cuda")
+        sem = torch.zeros(L.IGEMM_SEM_INTS, dtype=torch.int32, device="cuda")
         g = L.ConvGeom(batch, H, H, Cc, H, H, K, 3, 3, 1, 1)
         # WGRAD split-K as the block executor sizes it (block.cu wgrad_splits: ~148 CTAs)
         nkb = (M + 63) // 64

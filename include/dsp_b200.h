@@ -103,9 +103,9 @@ typedef struct {
   /* FPROP fused BatchNorm finalize (optional, needs stats): per n-tile of the
    * launch, the last CTA owning it reduces that tile's per-CTA partials in fixed
    * order and writes stat_out[4][N] = mean, invstd, gamma*invstd,
-   * beta - mean*gamma*invstd for its columns (columns >= n_valid get zeros).
-   * sem: device ints, one per n-tile (ceil(N / 128) suffice, 64 max), 0 on entry
-   * (the kernel leaves them 0 again). */
+   * beta - mean*gamma*invstd for its columns (columns >= n_valid get zeros). Large grids
+   * finalize in two levels (groups of 16 CTAs, then the group sums).
+   * sem: DSP_IGEMM_SEM_INTS device ints, 0 on entry (the kernel leaves them 0 again). */
   float* stat_out;
   const float* gamma;
   const float* beta;
@@ -133,6 +133,7 @@ typedef struct {
 } dsp_igemm_args_t;
 
 #define DSP_IGEMM_MAX_CTAS 444
+#define DSP_IGEMM_SEM_INTS 1024 /* ticket ints a fused-finalize launch may use (dsp_igemm_args_t.sem) */
 
 /* Implicit-GEMM conv/dense on tcgen05 tensor cores (igemm.cu).  `splits` is the
  * WGRAD split-K factor (ignored otherwise). */

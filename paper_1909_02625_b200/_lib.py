@@ -98,6 +98,7 @@ class IgemmArgs(C.Structure):
 
 
 IGEMM_MAX_CTAS = 444
+IGEMM_SEM_INTS = 1024  # DSP_IGEMM_SEM_INTS
 
 
 class LayerDesc(C.Structure):

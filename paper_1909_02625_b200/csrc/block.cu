@@ -788,7 +788,7 @@ extern "C" int dsp_block_create(const dsp_layer_desc_t* layers, int n_layers, in
   for (int s = 0; s < 4; ++s) b->S[s] = pl.take((size_t)max_act * b->esz);
   for (int s = 0; s < 2; ++s) b->G[s] = pl.take((size_t)max_act * b->esz);
   b->fpart = pl.take((size_t)std::max<int64_t>(max_fpart, 1) * 4);
-  b->sem = pl.take(256);  // zeroed at bind; fused-finalize kernels leave it zero
+  b->sem = pl.take(4096);  // DSP_IGEMM_SEM_INTS tickets, zeroed at bind; the fused-finalize kernels leave them zero
   b->bpart = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
   b->bpart2 = pl.take((size_t)std::max<int64_t>(max_bpart, 1) * 4);
   b->wpart = pl.take((size_t)std::max<int64_t>(max_wpart, 1) * 4);

@@ -249,6 +249,7 @@ struct IgTma {
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
   // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
   uint32_t fd_d[5], fd_mul[5], fd_shr[5];
+  int fin1;     // 1: single-level BN finalize (DSP_B200_FIN_1LEVEL A/B switch)
 };
 
 static void fastdiv_host(uint32_t d, uint32_t& mul, uint32_t& shr) {
@@ -1427,7 +1428,84 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
     if (tid == 0) ctat[2] = (int64_t)globaltimer_ns();
   }
   const bool fuse_fin = want_stats && a.sem != nullptr && (bnb || a.stat_out != nullptr);
-  if (fuse_fin) {
+  // Two-level finalize: the G/nt CTAs owning an n-tile form groups of FIN_GS; the last CTA of a
+  // group sums its group's partial rows (fixed order, double) into the group leader's row, and the
+  // last group to finish reduces the ngr leader rows and finalizes. The single-CTA form loaded all
+  // G/nt rows at one SM's bandwidth: 6-12 us of every ResNet-50 FPROP (--fprop-stats finalize vs
+  // partials, tools/conv_tc.py). Level-1 tickets live at sem[64 + 32 t + g].
+  constexpr int FIN_GS = 16;
+  const int per_tile = (int)gridDim.x / nt;
+  const int ngr = (per_tile + FIN_GS - 1) / FIN_GS;
+  // Same-box A/B (tools/gpu/ab_fin_conv.sh): pays off for >= 64 partial rows of >= 128 columns
+  // (2-4 us off ResNet-50's s2-s4 3x3 / reduce convs); the extra ticket costs more than it saves
+  // on short rows (CIFAR widths) or few rows (wide 1x1 expansions).
+  const bool two_level = fuse_fin && (N & 3) == 0 && per_tile >= 64 && min(BN, N) >= 128 && ngr <= 32 &&
+                         nt <= 30 && !tm.fin1 && !kTrace;
+  if (two_level) {
+    const int t_own = (int)(blockIdx.x % nt);
+    const int j = (int)(blockIdx.x / nt), gi = j / FIN_GS;
+    const int gsize = min(FIN_GS, per_tile - gi * FIN_GS);
+    const int cbeg = t_own * BN, cend = min(N, cbeg + BN), cols = cend - cbeg;
+    if (last_cta_ticket(a.sem + 64 + 32 * t_own + gi, gsize, &last_cta_s)) {
+      // level 1: rows of CTAs t_own + (gi*FIN_GS + r)*nt, r < gsize -> the leader's row (r = 0)
+      const size_t lead = (size_t)t_own + (size_t)gi * FIN_GS * nt;
+      for (int it = tid; it < NS * cols; it += IG_THREADS) {
+        const int st = it / cols, c = cbeg + it % cols;
+        float v[FIN_GS];
+#pragma unroll
+        for (int r = 0; r < FIN_GS; ++r)
+          v[r] = r < gsize ? __ldcg(&a.stats[((lead + (size_t)r * nt) * NS + st) * N + c]) : 0.f;
+        double acc = 0.0;
+#pragma unroll
+        for (int r = 0; r < FIN_GS; ++r) acc += (double)v[r];
+        a.stats[(lead * NS + st) * N + c] = (float)acc;
+      }
+      if (tid == 0) a.sem[64 + 32 * t_own + gi] = 0;
+      if (last_cta_ticket(a.sem + t_own, ngr, &last_cta_s)) {
+        // level 2: the ngr leader rows, in group order
+        const int nvalid = a.n_valid > 0 ? a.n_valid : N;
+        const double count = (double)a.M;
+        for (int cc = tid; cc < cols; cc += IG_THREADS) {
+          const int c = cbeg + cc;
+          double sv[3] = {0.0, 0.0, 0.0};
+          for (int g2 = 0; g2 < ngr; ++g2) {
+            const size_t row = (size_t)t_own + (size_t)g2 * FIN_GS * nt;
+            for (int st = 0; st < NS; ++st) sv[st] += (double)__ldcg(&a.stats[(row * NS + st) * N + c]);
+          }
+          if (MODE == DSP_IGEMM_FPROP) {
+            float mean = 0.f, inv = 0.f, scale = 0.f, shift = 0.f;
+            if (c < nvalid) {
+              const double mu = sv[0] / count;
+              double var = sv[1] / count - mu * mu;
+              if (var < 0.0) var = 0.0;
+              const double iv = 1.0 / sqrt(var + 1e-5);
+              mean = (float)mu;
+              inv = (float)iv;
+              scale = (float)((double)a.gamma[c] * iv);
+              shift = (float)((double)a.beta[c] - mu * (double)a.gamma[c] * iv);
+            }
+            a.stat_out[c] = mean;
+            a.stat_out[N + c] = inv;
+            a.stat_out[2 * N + c] = scale;
+            a.stat_out[3 * N + c] = shift;
+          } else {
+            for (int t = 0; t + 1 < NS; ++t) {  // DGRAD: target t's sum g * xhat_t is statistic t + 1
+              const dsp_bnb_target_t& tg = a.bnb[t];
+              const bool real = c < a.bnb_c_real;
+              if (real) {
+                tg.dbeta[c] = (float)sv[0];
+                tg.dgamma[c] = (float)sv[t + 1];
+              }
+              tg.coef[c] = real ? tg.gamma[c] * __ldcg(&tg.stat[N + c]) : 0.f;
+              tg.coef[N + c] = real ? (float)(sv[0] / count) : 0.f;
+              tg.coef[2 * N + c] = real ? (float)(sv[t + 1] / count) : 0.f;
+            }
+          }
+        }
+        if (tid == 0) a.sem[t_own] = 0;
+      }
+    }
+  } else if (fuse_fin) {
     // one ticket per n-tile (sem[t], t = blockIdx.x % nt): the last of the G/nt CTAs owning
     // n-tile t finalizes its BN columns, so wide outputs finalize on nt CTAs in parallel
     const int t_own = (int)(blockIdx.x % nt);
@@ -2002,6 +2080,8 @@ cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
       fastdiv_host(divs[i], tm.fd_mul[i], tm.fd_shr[i]);
     }
   }
+  static const bool fin1 = getenv("DSP_B200_FIN_1LEVEL") != nullptr;
+  tm.fin1 = fin1 ? 1 : 0;
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
   int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128
                      : (tm.i2c ? IgCfg<BN, true>::SMEM : Cfg::SMEM);

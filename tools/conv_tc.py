@@ -97,7 +97,7 @@ def main():
         stat_out = torch.empty(4 * K, device="cuda")
         gamma = torch.ones(K, device="cuda")
         beta = torch.zeros(K, device="cuda")
-        sem = torch.zeros(64, dtype=torch.int32, device="cuda")  # one ticket per n-tile
+        sem = torch.zeros(L.IGEMM_SEM_INTS, dtype=torch.int32, device="cuda")  # one ticket per n-tile
         # WGRAD split-K as the block executor sizes it (block.cu wgrad_splits, 148-CTA target)
         Mw, nkb = R * R * Cc, (Mf + 63) // 64
         mt, nt = (Mw + 127) // 128, (K + 255) // 256

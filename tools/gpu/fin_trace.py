@@ -31,7 +31,7 @@ def main():
         stats = torch.empty(L.IGEMM_MAX_CTAS * 2 * K, device="cuda")
         stat_out = torch.empty(4 * K, device="cuda")
         gamma, beta = torch.ones(K, device="cuda"), torch.zeros(K, device="cuda")
-        sem = torch.zeros(64, dtype=torch.int32, device="cuda")
+        sem = torch.zeros(L.IGEMM_SEM_INTS, dtype=torch.int32, device="cuda")
         trace = torch.zeros(192 + 12 * 1024, dtype=torch.int64, device="cuda")
         a = L.IgemmArgs()
         a.geom = g
