@@ -211,6 +211,72 @@ __global__ void __launch_bounds__(kThreads, MINB) bn_apply_k_lb(const T* __restr
   bn_apply_k_body<T, UNR>(y, stat, res, y2, stat2, out, nvec, Cp, relu, mbits);
 }
 
+// Resident-grid form (tensors beyond one wave, channel vectors dividing the block): the projection
+// branch is compile-time (Y2) so the plain unit keeps only its own scale / shift in registers,
+// two vectors per thread per pass, and exactly the resident CTAs (no partial last wave).
+template <typename T, int UNR, int MINB, bool Y2>
+__global__ void __launch_bounds__(kThreads, MINB)
+    bn_apply_rg_k(const T* __restrict__ y, const float* __restrict__ stat, const T* __restrict__ res,
+                  const T* __restrict__ y2, const float* __restrict__ stat2, T* __restrict__ out, int64_t nvec,
+                  int Cp, int relu, uint8_t* __restrict__ mbits) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  constexpr int VE = V16<T>::N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int c0 = (int)(threadIdx.x % (Cp / VE)) * VE;
+  float sc[VE], sh[VE], sc2[Y2 ? VE : 1], sh2[Y2 ? VE : 1];
+#pragma unroll
+  for (int i = 0; i < VE; ++i) {
+    sc[i] = stat[2 * Cp + c0 + i];
+    sh[i] = stat[3 * Cp + c0 + i];
+    if constexpr (Y2) {
+      sc2[i] = stat2[2 * Cp + c0 + i];
+      sh2[i] = stat2[3 * Cp + c0 + i];
+    }
+  }
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * UNR) {
+    uint4 ry[UNR], rr[UNR], r2[Y2 ? UNR : 1];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {  // every load of the pass first
+      const int64_t v = v0 + u * stride;
+      if (v < nvec) {
+        ry[u] = ldraw(y + v * VE);
+        if (res != nullptr) rr[u] = ldraw(res + v * VE);
+        if constexpr (Y2) r2[u] = ldraw(y2 + v * VE);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v >= nvec) break;
+      float a[VE];
+      cvt16<T>(ry[u], a);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) a[i] = a[i] * sc[i] + sh[i];
+      if (res != nullptr) {
+        float r[VE];
+        cvt16<T>(rr[u], r);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) a[i] += r[i];
+      }
+      if constexpr (Y2) {
+        float r[VE];
+        cvt16<T>(r2[u], r);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) a[i] += r[i] * sc2[i] + sh2[i];
+      }
+      if (relu) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) a[i] = fmaxf(a[i], 0.f);
+      }
+      st16(out + v * VE, a);
+      if (mbits != nullptr) mbits[v] = mask_byte<T>(a);
+    }
+  }
+}
+
+template <typename K>
+int resident_ctas(K kern);
+
 // ------------------------------------------------------------------ BatchNorm backward
 // Layout of a reduction CTA: G = Cp/VE channel groups, TR = 256/G row lanes.
 struct BnBwdFin {  // fused finalize (last CTA) of the BatchNorm-backward reduction
@@ -483,6 +549,118 @@ __global__ void __launch_bounds__(kThreads, MINB) bn_bwd_apply_k_lb(const T* __r
                                const float* __restrict__ coefb, T* __restrict__ dyb, T* __restrict__ gout,
                                int64_t nvec, int Cp, int relu_y, const uint8_t* __restrict__ mbits) {
   bn_bwd_apply_k_body<T, UNR>(gsrc, mask, y, stat, coef, dy, yb, statb, coefb, dyb, gout, nvec, Cp, relu_y, mbits);
+}
+
+// Resident-grid form of the BN-backward apply for tensors beyond one wave whose channel vectors
+// divide the block (each thread keeps one channel group for the whole pass): the mask path is a
+// compile-time KIND so only the coefficients it needs occupy registers -- 0: mask bits / mask
+// tensor / none, 1: mask from y (relu(y*scale + shift) > 0), 2: main + projection target
+// (register-resident here; the general form re-loads the projection's five coefficients per
+// element, 1.9 TB/s on ResNet-50's first unit) -- and the grid is exactly the resident CTAs, so
+// there is no partial last wave (1184 CTAs at 3 per SM left a third of a wave idle).
+template <typename T, int UNR, int MINB, int KIND>
+__global__ void __launch_bounds__(kThreads, MINB)
+    bn_bwd_apply_rg_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+                      const float* __restrict__ stat, const float* __restrict__ coef, T* __restrict__ dy,
+                      const T* __restrict__ yb, const float* __restrict__ statb, const float* __restrict__ coefb,
+                      T* __restrict__ dyb, T* __restrict__ gout, int64_t nvec, int Cp, int relu_y,
+                      const uint8_t* __restrict__ mbits) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  constexpr int VE = V16<T>::N;
+  constexpr bool kRy = KIND == 1, kPair = KIND == 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int c0 = (int)(threadIdx.x % (Cp / VE)) * VE;
+  // dy = k0 * (g - k1 - (y - km) * kq) (the general form's arithmetic, kq = invstd * c2)
+  float k0[VE], k1[VE], km[VE], kq[VE];
+  float ms[kRy ? VE : 1], mh[kRy ? VE : 1];
+  float p0[kPair ? VE : 1], p1[kPair ? VE : 1], pm[kPair ? VE : 1], pi[kPair ? VE : 1], p2[kPair ? VE : 1];
+#pragma unroll
+  for (int i = 0; i < VE; ++i) {
+    const int c = c0 + i;
+    k0[i] = coef[c];
+    k1[i] = coef[Cp + c];
+    km[i] = stat[c];
+    kq[i] = stat[Cp + c] * coef[2 * Cp + c];
+    if constexpr (kRy) {
+      ms[i] = stat[2 * Cp + c];
+      mh[i] = stat[3 * Cp + c];
+    }
+    if constexpr (kPair) {
+      p0[i] = coefb[c];
+      p1[i] = coefb[Cp + c];
+      p2[i] = coefb[2 * Cp + c];
+      pm[i] = statb[c];
+      pi[i] = statb[Cp + c];
+    }
+  }
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * UNR) {
+    uint4 rg[UNR], rm[UNR], ry[UNR], rb[kPair ? UNR : 1];
+    uint32_t rb8[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {  // every load of the pass first
+      const int64_t v = v0 + u * stride;
+      if (v < nvec) {
+        rg[u] = ldraw(gsrc + v * VE);
+        if constexpr (!kRy) {
+          if (mbits != nullptr) rb8[u] = mbits[v];
+          else if (mask != nullptr) rm[u] = ldraw(mask + v * VE);
+        }
+        ry[u] = ldraw(y + v * VE);
+        if constexpr (kPair) rb[u] = ldraw(yb + v * VE);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v >= nvec) break;
+      const int64_t e0 = v * VE;
+      float g[VE], yy[VE], o[VE];
+      cvt16<T>(rg[u], g);
+      cvt16<T>(ry[u], yy);
+      if constexpr (kRy) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) g[i] = fmaf(yy[i], ms[i], mh[i]) > 0.f ? g[i] : 0.f;
+      } else if (mbits != nullptr) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) g[i] = (rb8[u] >> i) & 1u ? g[i] : 0.f;
+      } else if (mask != nullptr) {
+        float mk[VE];
+        cvt16<T>(rm[u], mk);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) g[i] = mk[i] > 0.f ? g[i] : 0.f;
+      }
+      if (gout != nullptr) st16(gout + e0, g);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) o[i] = k0[i] * (g[i] - k1[i] - (yy[i] - km[i]) * kq[i]);
+      st16(dy + e0, o);
+      if constexpr (kPair) {
+        cvt16<T>(rb[u], yy);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+          const float xh = (yy[i] - pm[i]) * pi[i];
+          o[i] = p0[i] * (g[i] - p1[i] - xh * p2[i]);
+        }
+        st16(dyb + e0, o);
+      }
+    }
+  }
+}
+
+// CTAs of `kern` resident on the current device at kThreads threads (cached per kernel/device)
+template <typename K>
+int resident_ctas(K kern) {
+  constexpr int kMaxDev = 16;
+  static int cache[kMaxDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) dev = 0;
+  if (cache[dev] == 0) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = std::max(1, per_sm) * std::max(1, sms);
+  }
+  return cache[dev];
 }
 
 // Tensors within one wave (CIFAR shapes, one vector per thread): the plain form -- per-vector
@@ -1330,16 +1508,25 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
     // ResNet-50: the unbounded UNR-4 form took 117 registers -> 2 CTAs/SM, 24% warps active,
     // 44-59% of DRAM peak; one vector per thread per pass at 4 CTAs/SM measured +1.6%
     // (ResNet-50) / +5.3% (ResNet-164) samples/s
-    static const int var = getenv("DSP_B200_BNA") ? atoi(getenv("DSP_B200_BNA")) : 13;
+    static const int var = getenv("DSP_B200_BNA") ? atoi(getenv("DSP_B200_BNA")) : 0;
     auto go = [&](auto kern) {
       launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)y, stat, (const T*)res, (const T*)y2, stat2, (T*)out,
                nvec, Cp, relu, mbits);
     };
-    if (nvec > kWave) {
+    // resident-grid forms by default (DSP_B200_BNA=13 restores the general one)
+    auto go_rg = [&](auto kern) {
+      const int64_t need = (nvec + kThreads - 1) / kThreads;
+      launch_k(kern, (int)std::min<int64_t>(need, resident_ctas(kern)), kThreads, 0, st, (const T*)y, stat,
+               (const T*)res, (const T*)y2, stat2, (T*)out, nvec, Cp, relu, mbits);
+    };
+    if (nvec > kWave && var == 0 && (kThreads % (Cp / V16<T>::N)) == 0) {
+      if (y2 != nullptr) go_rg(bn_apply_rg_k<T, 2, 2, true>);
+      else go_rg(bn_apply_rg_k<T, 2, 4, false>);
+    } else if (nvec > kWave) {
       if (var == 23) go(bn_apply_k_lb<T, 2, 3>);
       else if (var == 24) go(bn_apply_k_lb<T, 2, 4>);
       else if (var == 43) go(bn_apply_k_lb<T, 4, 3>);
-      else if (var == 13) go(bn_apply_k_lb<T, 1, 4>);  // default: 62 regs, 4 CTAs/SM, no spill
+      else if (var == 13 || var == 0) go(bn_apply_k_lb<T, 1, 4>);  // general: 62 regs, 4 CTAs/SM
       else go(bn_apply_k<T, 4>);  // 41: compiler-chosen 117 regs, 2 CTAs/SM
     }
     else
@@ -1407,15 +1594,27 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
     // variant (UNR x min CTAs per SM) via DSP_B200_BNB = 10*UNR + MINB (A/B knob): the
     // unbounded UNR-2 form took 128 registers (2 CTAs/SM); UNR 1 at 3 CTAs/SM measured +0.9%
     // (ResNet-50) / +2.6% (ResNet-164)
-    static const int var = getenv("DSP_B200_BNB") ? atoi(getenv("DSP_B200_BNB")) : 13;
+    static const int var = getenv("DSP_B200_BNB") ? atoi(getenv("DSP_B200_BNB")) : 0;
     auto go = [&](auto kern) {
       launch_k(kern, grid_for(nvec), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef, (T*)dy,
                (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y, mbits);
     };
-    if (nvec > kWave) {
+    // resident-grid forms (DSP_B200_BNB=13 restores the general form)
+    const bool rg = var != 13 && (kThreads % (Cp / V16<T>::N)) == 0 && !(y_b != nullptr && relu_y);
+    auto go_rg = [&](auto kern) {
+      const int64_t need = (nvec + kThreads - 1) / kThreads;
+      const int grid = (int)std::min<int64_t>(need, resident_ctas(kern));
+      launch_k(kern, grid, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, coef, (T*)dy,
+               (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y, mbits);
+    };
+    if (nvec > kWave && rg) {
+      if (y_b != nullptr) go_rg(bn_bwd_apply_rg_k<T, 1, 2, 2>);
+      else if (relu_y) go_rg(bn_bwd_apply_rg_k<T, 2, 2, 1>);
+      else go_rg(bn_bwd_apply_rg_k<T, 2, 2, 0>);
+    } else if (nvec > kWave) {
       if (var == 23) go(bn_bwd_apply_k_lb<T, 2, 3>);
       else if (var == 24) go(bn_bwd_apply_k_lb<T, 2, 4>);
-      else if (var == 13) go(bn_bwd_apply_k_lb<T, 1, 3>);  // default: 80 regs, 3 CTAs/SM, no spill
+      else if (var == 13 || var == 0) go(bn_bwd_apply_k_lb<T, 1, 3>);  // general default: 80 regs, 3 CTAs/SM
       else if (var == 14) go(bn_bwd_apply_k_lb<T, 1, 4>);
       else go(bn_bwd_apply_k<T, 2>);
     }
