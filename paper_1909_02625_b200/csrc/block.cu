@@ -355,6 +355,14 @@ int conv_dgrad(dsp_block* b, const ConvP& c, const void* dy, void* dx, const voi
   return DSP_OK;
 }
 
+// Which BN-backward statistics ride on a DGRAD epilogue (DSP_B200_BNB_FUSE bit mask, A/B knob):
+// bit 0 = a unit's inner BNs (on the conv above's DGRAD), bit 1 = the top BN(s) of the layer below
+// (on this layer's input DGRAD). Unfused, bn_bwd_stats reads the DGRAD output back.
+int bnb_fuse_mask() {
+  static const int m = getenv("DSP_B200_BNB_FUSE") ? atoi(getenv("DSP_B200_BNB_FUSE")) : 3;
+  return m;
+}
+
 // The ReLU mask of a BN whose output is exactly relu(bn(y)) (stem, intra-unit BNs; not a unit's top
 // BN, which adds the shortcut first): mask_of returns nullptr and the backward kernels recompute
 // the mask from y and the forward's scale / shift instead of reading the stored output -- one
@@ -553,9 +561,13 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
         const ConvP& cb = l.convs[i - 1];
         const void* zmask = b->ws + (i == 1 ? l.z1 : l.z2);
         const BnbFuse fuse{mask_of(zmask), &cb, nullptr};
-        DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st, &fuse));
+        const bool fused = (bnb_fuse_mask() & 1) != 0;
+        DSP_TRY(conv_dgrad(b, c, S0, S2, nullptr, st, fused ? &fuse : nullptr));
         DSP_TRY(side_join(b, st));  // the WGRAD reading S0 is done before S0 is overwritten
-        DSP_TRY(bn_backward_apply(b, S2, mask_of(zmask), cb, S0, nullptr, nullptr, nullptr, st));
+        if (fused)
+          DSP_TRY(bn_backward_apply(b, S2, mask_of(zmask), cb, S0, nullptr, nullptr, nullptr, st));
+        else
+          DSP_TRY(bn_backward_pair(b, S2, mask_of(zmask), cb, S0, nullptr, nullptr, nullptr, st));
       }
       const void* res = S1;
       if (cs) {
@@ -911,7 +923,7 @@ extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* gr
     BnbFuse fz{};
     const BnbFuse* below = nullptr;
     const bool s2d = l.d.kind == DSP_LAYER_CONV_BN_RELU && l.convs[0].s2d_r;  // its dx is unpacked after DGRAD
-    if (i > 0 && dx != nullptr && !s2d && has_top_bn(l) && has_top_bn(b->L[i - 1])) {
+    if (i > 0 && dx != nullptr && !s2d && has_top_bn(l) && has_top_bn(b->L[i - 1]) && (bnb_fuse_mask() & 2)) {
       const LayerP& lb = b->L[i - 1];
       const int nmain = lb.d.kind == DSP_LAYER_BOTTLENECK ? 3 : lb.d.kind == DSP_LAYER_BASIC_UNIT ? 2 : 1;
       // a stem below (relu(bn(y)), no shortcut): its mask comes from y too

@@ -290,8 +290,10 @@ struct BnBwdFin {  // fused finalize (last CTA) of the BatchNorm-backward reduct
   int* sem;
 };
 
+// 2 CTAs per SM (= the 296-chunk grid in one wave): unbounded, the compiler took 132 registers ->
+// 1 CTA per SM, two waves, 3.2 TB/s (ncu, profiles/r02_bn_bwd_reduce.md)
 template <typename T>
-__global__ void bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
+__global__ void __launch_bounds__(kThreads, 2) bn_bwd_reduce_k(const T* __restrict__ gsrc, const T* __restrict__ mask, const T* __restrict__ y,
                                 const float* __restrict__ stat, float* __restrict__ part, int64_t M, int Cp,
                                 int rows_per_chunk, const BnBwdFin fin, int relu_y,
                                 const uint8_t* __restrict__ mbits) {

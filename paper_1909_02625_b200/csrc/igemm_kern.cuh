@@ -993,7 +993,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                n0 + BN <= (a.n_valid > 0 ? a.n_valid : N);
       }
       if constexpr (MODE == DSP_IGEMM_DGRAD && CPW % 2 == 0 && sizeof(T) == 2) {
-        fastd = dw && !s2 && !zacc && a.bias == nullptr && m0 + IG_BM <= M && n0 + BN <= (a.n_valid > 0 ? a.n_valid : N);
+        fastd = dw && !s2 && !zacc && a.bias == nullptr && m0 + IG_BM <= M && n0 + BN <= (a.n_valid > 0 ? a.n_valid : N) &&
+                !(want_stats && a.bnb_mask != nullptr && a.bnb_mask_bits == nullptr);
       }
       if (fastd) {
         // DGRAD fast path (same slab scheme): optional residual add (lane = row, its four 16-byte
@@ -1013,6 +1014,14 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll
             for (int k = 0; k < 4; ++k) rr[k] = __ldg(rp + k);
           }
+          // mask bits with 32-aligned rows: lane l loads the chunk's 32-bit mask word of row l (one
+          // coalesced load, issued here so it lands under the TMEM load / staging) and each row's
+          // word is shuffled to the lanes that need it -- instead of 16 one-byte loads per lane (30%
+          // of this epilogue's stall samples, profiles/r02_dgrad_epilogue.md)
+          const bool mword = want_stats && a.bnb_mask_bits != nullptr && (a.ldd & 31) == 0;
+          const uint32_t mw = mword ? __ldg(reinterpret_cast<const uint32_t*>(a.bnb_mask_bits) +
+                                            (((size_t)(rbase + lane) * a.ldd + n0 + col0) >> 5))
+                                    : 0u;
           float vb[32];
           tmem_ld32(tl + col0, vb);
           if (a.residual != nullptr) {
@@ -1038,75 +1047,108 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                          : "memory");
           }
           __syncwarp();
+          // lane = (row r = lane / 4 + 8 it, 16-byte chunk k4): the slab read that feeds the store
+          // also feeds the statistics, with y (and mask) read as the same 16-byte row chunks --
+          // coalesced 64-byte row segments, 4 (8 for two targets) loads per lane per chunk, all in
+          // flight before the slab reads -- and the 8 lanes of a chunk reduced by shuffles in fixed
+          // order (the 2-column-per-lane form issued 4-byte loads in two latency-bound batches)
+          const int k4 = lane & 3;
+          const bool mbits = a.bnb_mask_bits != nullptr;  // else the mask is recomputed from y (fastd)
+          uint4 yr[4];
+          uint32_t mb8[4];
+          auto load_y = [&](const void* y) {
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const size_t o = (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8;
+              yr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(y) + o));
+            }
+          };
+          if (want_stats) {
+            load_y(a.bnb[0].y);
+            if (mbits && !mword) {
+#pragma unroll
+              for (int it = 0; it < 4; ++it)
+                mb8[it] = __ldg(a.bnb_mask_bits +
+                                (((size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8) >> 3));
+            }
+          }
+          // this lane's slab chunk of row r (the stored dX; re-read for the statistics rather than
+          // held in registers across the y loads' latency)
+          auto slab = [&](int it) {
+            const int r = (lane >> 2) + 8 * it;
+            uint4 v;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(sDW + r * 64 + ((k4 ^ ((r >> 1) & 3)) << 4)));
+            return v;
+          };
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
-            const int r = (lane >> 2) + 8 * it, k = lane & 3;
-            uint4 raw;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
-                         : "r"(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)));
-            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k * 8) = raw;
+            const int r = (lane >> 2) + 8 * it;
+            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) =
+                slab(it);
           }
           if (want_stats) {
-            const int cp = lane & 15, rh = lane >> 4;
-            const int cl = col0 + 2 * cp;  // tile column of the pair
-            const size_t cofs = (size_t)n0 + cl;
-            const float m0a = bst[0][0][cl], i0a = bst[0][1][cl], m0b = bst[0][0][cl + 1], i0b = bst[0][1][cl + 1];
-            const float m1a = bst[1][0][cl], i1a = bst[1][1][cl], m1b = bst[1][0][cl + 1], i1b = bst[1][1][cl + 1];
-            float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f, s3a = 0.f, s3b = 0.f;
-#pragma unroll 1
-            for (int h8 = 0; h8 < 16; h8 += 8) {  // 8 rows' loads in flight at a time (register cap)
-            uint32_t mk[8], y0[8], y1[8];
-            const bool mbits = a.bnb_mask_bits != nullptr;
+            const int cl = col0 + k4 * 8;  // tile columns cl .. cl + 7
+            if (mword) {
 #pragma unroll
-            for (int it = 0; it < 8; ++it) {
-              const size_t o = (size_t)(rbase + rh + 2 * (h8 + it)) * a.ldd + cofs;
-              // mask bits: the byte of the column pair's 8-column group, shifted so bits 0/1 are the pair
-              mk[it] = mbits ? (uint32_t)__ldg(a.bnb_mask_bits + (o >> 3)) >> (o & 7)
-                       : a.bnb_mask != nullptr
-                           ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb_mask) + o)) : 0u;
-              y0[it] = __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[0].y) + o));
-              y1[it] = nbt > 1 ? __ldg(reinterpret_cast<const uint32_t*>(reinterpret_cast<const T*>(a.bnb[1].y) + o)) : 0u;
+              for (int it = 0; it < 4; ++it) mb8[it] = __shfl_sync(0xffffffffu, mw, (lane >> 2) + 8 * it) >> (8 * k4);
             }
+            auto bf = [](uint32_t w, int j) { return __uint_as_float((j & 1) ? (w & 0xffff0000u) : (w << 16)); };
+            // g = dX where the mask is on: the unit output's bits, or relu(y*scale + shift) > 0 (y of
+            // target 0, whose scale / shift sit in bst[1] then); gate bits per (row, column)
+            uint32_t on[4];
 #pragma unroll
-            for (int it = 0; it < 8; ++it) {
-              const int r = rh + 2 * (h8 + it);
-              uint32_t w;
-              asm volatile("ld.shared.b32 %0, [%1];"
-                           : "=r"(w)
-                           : "r"(sDW + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4));
-              // mask: the stored BN output (> 0), or recomputed from y as relu(y*scale + shift) > 0
-              const bool pa = mbits ? (mk[it] & 1u) != 0u
-                              : a.bnb_mask != nullptr ? __uint_as_float(mk[it] << 16) > 0.f
-                                                      : fmaf(__uint_as_float(y0[it] << 16), m1a, i1a) > 0.f;
-              const bool pb = mbits ? (mk[it] & 2u) != 0u
-                              : a.bnb_mask != nullptr ? __uint_as_float(mk[it] & 0xffff0000u) > 0.f
-                                                      : fmaf(__uint_as_float(y0[it] & 0xffff0000u), m1b, i1b) > 0.f;
-              const float ga = pa ? __uint_as_float(w << 16) : 0.f;
-              const float gb = pb ? __uint_as_float(w & 0xffff0000u) : 0.f;
-              s1a += ga;
-              s1b += gb;
-              s2a += ga * ((__uint_as_float(y0[it] << 16) - m0a) * i0a);
-              s2b += gb * ((__uint_as_float(y0[it] & 0xffff0000u) - m0b) * i0b);
-              if (nbt > 1) {
-                s3a += ga * ((__uint_as_float(y1[it] << 16) - m1a) * i1a);
-                s3b += gb * ((__uint_as_float(y1[it] & 0xffff0000u) - m1b) * i1b);
+            for (int it = 0; it < 4; ++it) {
+              if (mbits) {
+                on[it] = mb8[it] & 0xffu;
+              } else {
+                const uint32_t yw[4] = {yr[it].x, yr[it].y, yr[it].z, yr[it].w};
+                uint32_t b8 = 0u;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  b8 |= (fmaf(bf(yw[j >> 1], j), bst[1][0][cl + j], bst[1][1][cl + j]) > 0.f ? 1u : 0u) << j;
+                on[it] = b8;
               }
             }
-            }
-            s1a += __shfl_xor_sync(0xffffffffu, s1a, 16);
-            s1b += __shfl_xor_sync(0xffffffffu, s1b, 16);
-            s2a += __shfl_xor_sync(0xffffffffu, s2a, 16);
-            s2b += __shfl_xor_sync(0xffffffffu, s2b, 16);
-            s3a += __shfl_xor_sync(0xffffffffu, s3a, 16);
-            s3b += __shfl_xor_sync(0xffffffffu, s3b, 16);
-            if (lane < 16) {
-              red[q][cl][0] += s1a;
-              red[q][cl][1] += s2a;
-              red[q][cl][2] += s3a;
-              red[q][cl + 1][0] += s1b;
-              red[q][cl + 1][1] += s2b;
-              red[q][cl + 1][2] += s3b;
+            // target t: per column, sum g and sum g * xhat_t over this lane's 4 rows, then over the 8
+            // lanes of the chunk (fixed shuffle order); target 1's y row replaces target 0's in the
+            // same registers as soon as that row is summed
+            for (int t = 0; t < nbt; ++t) {
+              float s1[8], s2[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) s1[j] = s2[j] = 0.f;
+#pragma unroll
+              for (int it = 0; it < 4; ++it) {
+                const uint4 gv = slab(it);
+                const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+                const uint32_t yw[4] = {yr[it].x, yr[it].y, yr[it].z, yr[it].w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float g = ((on[it] >> j) & 1u) ? bf(gw[j >> 1], j) : 0.f;
+                  s1[j] += g;
+                  s2[j] += g * ((bf(yw[j >> 1], j) - bst[t][0][cl + j]) * bst[t][1][cl + j]);
+                }
+                if (t + 1 < nbt) {
+                  const size_t o = (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8;
+                  yr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.bnb[1].y) + o));
+                }
+              }
+#pragma unroll
+              for (int off = 4; off < 32; off <<= 1) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  if (t == 0) s1[j] += __shfl_xor_sync(0xffffffffu, s1[j], off);
+                  s2[j] += __shfl_xor_sync(0xffffffffu, s2[j], off);
+                }
+              }
+              if (lane < 4) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  if (t == 0) red[q][cl + j][0] += s1[j];
+                  red[q][cl + j][1 + t] += s2[j];
+                }
+              }
             }
           }
           __syncwarp();
