@@ -1134,21 +1134,41 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                   yr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.bnb[1].y) + o));
                 }
               }
+              // reduce-scatter over the 8 lanes of the chunk (lane bits 4, 3, 2; fixed tree): each
+              // step keeps the half of the columns selected by the lane bit and adds the partner's
+              // copy of it, so lane (k4, cg = lane >> 2) ends with column cg's sums -- 14 shuffles
+              // instead of a 48-shuffle butterfly, and all 32 lanes update red[] at once
+              const int cg = lane >> 2;
+              float v[8];  // (column, statistic) pairs still held: s1 / s2 of 4, 2, 1 columns
+              {
+                const bool hb = (cg >> 2) & 1;  // off 16: keep columns 4..7 (hb) or 0..3
 #pragma unroll
-              for (int off = 4; off < 32; off <<= 1) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  if (t == 0) s1[j] += __shfl_xor_sync(0xffffffffu, s1[j], off);
-                  s2[j] += __shfl_xor_sync(0xffffffffu, s2[j], off);
+                for (int i = 0; i < 4; ++i) {
+                  const float k1 = hb ? s1[4 + i] : s1[i], o1 = hb ? s1[i] : s1[4 + i];
+                  const float k2 = hb ? s2[4 + i] : s2[i], o2 = hb ? s2[i] : s2[4 + i];
+                  v[2 * i] = k1 + (t == 0 ? __shfl_xor_sync(0xffffffffu, o1, 16) : 0.f);
+                  v[2 * i + 1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 16);
                 }
               }
-              if (lane < 4) {
+              {
+                const bool hb = (cg >> 1) & 1;  // off 8: keep columns 2,3 (hb) or 0,1 of the four
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  if (t == 0) red[q][cl + j][0] += s1[j];
-                  red[q][cl + j][1 + t] += s2[j];
+                for (int i = 0; i < 2; ++i) {
+                  const float k1 = hb ? v[2 * (2 + i)] : v[2 * i], o1 = hb ? v[2 * i] : v[2 * (2 + i)];
+                  const float k2 = hb ? v[2 * (2 + i) + 1] : v[2 * i + 1], o2 = hb ? v[2 * i + 1] : v[2 * (2 + i) + 1];
+                  v[2 * i] = k1 + (t == 0 ? __shfl_xor_sync(0xffffffffu, o1, 8) : 0.f);
+                  v[2 * i + 1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 8);
                 }
               }
+              {
+                const bool hb = cg & 1;  // off 4: keep column 1 (hb) or 0 of the two
+                const float k1 = hb ? v[2] : v[0], o1 = hb ? v[0] : v[2];
+                const float k2 = hb ? v[3] : v[1], o2 = hb ? v[1] : v[3];
+                v[0] = k1 + (t == 0 ? __shfl_xor_sync(0xffffffffu, o1, 4) : 0.f);
+                v[1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 4);
+              }
+              if (t == 0) red[q][cl + cg][0] += v[0];
+              red[q][cl + cg][1 + t] += v[1];
             }
           }
           __syncwarp();
