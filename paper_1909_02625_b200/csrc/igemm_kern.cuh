@@ -1007,12 +1007,17 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll 1
         for (int c2 = 0; c2 < CPW; c2 += 2) {
           const int col0 = (half * CPW + c2) * 16;
+          // residual: loaded coalesced as (row lane / 4 + 8 it, 16-byte chunk lane % 4) -- 8 rows of
+          // 64 contiguous bytes per warp load -- and transposed to lane = row through the slab (a
+          // lane-per-row global load touched 32 lines per instruction: the L1 was the bottleneck,
+          // 87% busy, profiles/r02_dgrad_epilogue.md)
           uint4 rr[4];
           if (a.residual != nullptr) {
-            const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.residual) +
-                                                             (size_t)(rbase + lane) * a.ldd + n0 + col0);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) rr[k] = __ldg(rp + k);
+            for (int it = 0; it < 4; ++it)
+              rr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.residual) +
+                                                            (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 +
+                                                            col0 + (lane & 3) * 8));
           }
           // mask bits with 32-aligned rows: lane l loads the chunk's 32-bit mask word of row l (one
           // coalesced load, issued here so it lands under the TMEM load / staging) and each row's
@@ -1022,6 +1027,23 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           const uint32_t mw = mword ? __ldg(reinterpret_cast<const uint32_t*>(a.bnb_mask_bits) +
                                             (((size_t)(rbase + lane) * a.ldd + n0 + col0) >> 5))
                                     : 0u;
+          if (a.residual != nullptr) {
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int r = (lane >> 2) + 8 * it, k = lane & 3;
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)),
+                           "r"(rr[it].x), "r"(rr[it].y), "r"(rr[it].z), "r"(rr[it].w)
+                           : "memory");
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(rr[k].x), "=r"(rr[k].y), "=r"(rr[k].z), "=r"(rr[k].w)
+                           : "r"(sDW + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4))
+                           : "memory");
+            __syncwarp();  // the slab is rewritten with the output below
+          }
           float vb[32];
           tmem_ld32(tl + col0, vb);
           if (a.residual != nullptr) {
