@@ -1007,17 +1007,19 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll 1
         for (int c2 = 0; c2 < CPW; c2 += 2) {
           const int col0 = (half * CPW + c2) * 16;
-          // residual: loaded coalesced as (row lane / 4 + 8 it, 16-byte chunk lane % 4) -- 8 rows of
-          // 64 contiguous bytes per warp load -- and transposed to lane = row through the slab (a
-          // lane-per-row global load touched 32 lines per instruction: the L1 was the bottleneck,
-          // 87% busy, profiles/r02_dgrad_epilogue.md)
-          uint4 rr[4];
+          // residual: copied coalesced (cp.async, no registers) as (row lane / 4 + 8 it, 16-byte chunk
+          // lane % 4) -- 8 rows of 64 contiguous bytes per warp request -- into the slab, then read
+          // back as lane = row (a lane-per-row global load touched 32 lines per instruction: the L1
+          // was the bottleneck, 87% busy, and register-held prefetches spilled;
+          // profiles/r02_dgrad_epilogue.md)
           if (a.residual != nullptr) {
 #pragma unroll
-            for (int it = 0; it < 4; ++it)
-              rr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.residual) +
-                                                            (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 +
-                                                            col0 + (lane & 3) * 8));
+            for (int it = 0; it < 4; ++it) {
+              const int r = (lane >> 2) + 8 * it, k = lane & 3;
+              cp_async_16_cg(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4),
+                             reinterpret_cast<const T*>(a.residual) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k * 8);
+            }
+            cp_async_commit();
           }
           // mask bits with 32-aligned rows: lane l loads the chunk's 32-bit mask word of row l (one
           // coalesced load, issued here so it lands under the TMEM load / staging) and each row's
@@ -1028,34 +1030,27 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                                             (((size_t)(rbase + lane) * a.ldd + n0 + col0) >> 5))
                                     : 0u;
           if (a.residual != nullptr) {
-#pragma unroll
-            for (int it = 0; it < 4; ++it) {
-              const int r = (lane >> 2) + 8 * it, k = lane & 3;
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)),
-                           "r"(rr[it].x), "r"(rr[it].y), "r"(rr[it].z), "r"(rr[it].w)
-                           : "memory");
-            }
+            cp_async_wait<0>();
             __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(rr[k].x), "=r"(rr[k].y), "=r"(rr[k].z), "=r"(rr[k].w)
-                           : "r"(sDW + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4))
-                           : "memory");
-            __syncwarp();  // the slab is rewritten with the output below
           }
           float vb[32];
           tmem_ld32(tl + col0, vb);
-          if (a.residual != nullptr) {
+          if (a.residual != nullptr) {  // row `lane` of the staged residual, one 16-byte chunk at a time
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint32_t w4[4] = {rr[k].x, rr[k].y, rr[k].z, rr[k].w};
+              uint4 rk;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(rk.x), "=r"(rk.y), "=r"(rk.z), "=r"(rk.w)
+                           : "r"(sDW + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4))
+                           : "memory");
+              const uint32_t w4[4] = {rk.x, rk.y, rk.z, rk.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 vb[8 * k + 2 * j] += __uint_as_float(w4[j] << 16);
                 vb[8 * k + 2 * j + 1] += __uint_as_float(w4[j] & 0xffff0000u);
               }
             }
+            __syncwarp();  // every lane has its residual row before the slab takes the output
           }
           uint32_t pk[16];
 #pragma unroll
