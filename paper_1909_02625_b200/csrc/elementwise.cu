@@ -938,6 +938,124 @@ __global__ void maxpool_bwd_k(const T* __restrict__ u, const uint8_t* __restrict
   }
 }
 
+// bf16 forward on packed pairs: per tap, one bf16x2 greater-than mask per word selects both the
+// new maximum and its tap (two LOP3s) -- the same strict first-maximum-in-tap-order rule as the
+// generic form, which spent ~32 scalar instructions per tap and was issue-bound (66% issue slots,
+// 2.8 TB/s, profiles/r02_maxpool.md)
+__global__ void maxpool_fwd_bf16x2_k(const uint4* __restrict__ x, uint4* __restrict__ out, uint2* __restrict__ arg,
+                                     int B, int H, int W, int P, int Q, int CV) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  const int n = B * P * Q * CV;  // < 2^31 (checked by the launcher)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int cv = i % CV;
+    int t = i / CV;
+    const int q = t % Q;
+    t /= Q;
+    const int p = t % P;
+    const int b = t / P;
+    uint4 raw[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {  // all nine taps in flight
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) raw[k] = __ldg(x + ((b * H + h) * W + w) * CV + cv);
+    }
+    uint32_t best[4] = {0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u}, ba[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) {
+        const uint32_t v[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&v[j]),
+                                         *reinterpret_cast<const __nv_bfloat162*>(&best[j]));
+          best[j] = (v[j] & m) | (best[j] & ~m);
+          ba[j] = ((uint32_t)k * 0x00010001u & m) | (ba[j] & ~m);
+        }
+      }
+    }
+    out[i] = make_uint4(best[0], best[1], best[2], best[3]);
+    arg[i] = make_uint2(__byte_perm(ba[0], ba[1], 0x6420), __byte_perm(ba[2], ba[3], 0x6420));
+  }
+}
+
+// Backward by output quads: thread (b, i, j, channel vector) writes input pixels (2i + di, 2j + dj)
+// from the (up to) four windows (i + di', j + dj') that contain them -- four 16-byte window loads,
+// no divergent tap search, every store a full 16 bytes. Each input pixel sums its windows in the
+// generic form's order (window rows, then columns, descending), so results are bitwise the same.
+template <typename T>
+__global__ void maxpool_bwd_quad_k(const T* __restrict__ u, const uint8_t* __restrict__ arg, T* __restrict__ dx,
+                                   int B, int H, int W, int P, int Q, int Cp) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  constexpr int VE = V16<T>::N;
+  const int CV = Cp / VE;
+  const int n = B * P * Q * CV;  // < 2^31 (checked by the launcher)
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const int cv = idx % CV;
+    int t = idx / CV;
+    const int j = t % Q;
+    t /= Q;
+    const int i = t % P;
+    const int b = t / P;
+    // windows w[di][dj] = (i + di, j + dj): gradient u and argmax taps
+    float uv[2][2][VE];
+    uint32_t tap[2][2][VE / 4];
+#pragma unroll
+    for (int di = 0; di < 2; ++di)
+#pragma unroll
+      for (int dj = 0; dj < 2; ++dj) {
+        const bool ok = i + di < P && j + dj < Q;
+        const int64_t o = (((int64_t)b * P + i + di) * Q + j + dj) * Cp + cv * VE;
+        if (ok) {
+          cvt16<T>(ldraw(u + o), uv[di][dj]);
+          if constexpr (VE == 8) {
+            const uint2 a = *reinterpret_cast<const uint2*>(arg + o);
+            tap[di][dj][0] = a.x;
+            tap[di][dj][1] = a.y;
+          } else {
+            tap[di][dj][0] = *reinterpret_cast<const uint32_t*>(arg + o);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < VE; ++e) uv[di][dj][e] = 0.f;
+#pragma unroll
+          for (int e = 0; e < VE / 4; ++e) tap[di][dj][e] = 0xffffffffu;  // matches no tap
+        }
+      }
+    auto term = [&](float (&acc)[VE], int di, int dj, uint32_t k) {
+#pragma unroll
+      for (int e = 0; e < VE; ++e)
+        if (((tap[di][dj][e / 4] >> (8 * (e & 3))) & 0xffu) == k) acc[e] += uv[di][dj][e];
+    };
+#pragma unroll
+    for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+      for (int dw = 0; dw < 2; ++dw) {
+        const int h = 2 * i + dh, w = 2 * j + dw;
+        if (h >= H || w >= W) continue;
+        float acc[VE];
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc[e] = 0.f;
+        // window rows r ascending = window index descending; likewise columns
+        if (dh == 0 && dw == 0) {
+          term(acc, 0, 0, 4);
+        } else if (dh == 0) {
+          term(acc, 0, 1, 3);
+          term(acc, 0, 0, 5);
+        } else if (dw == 0) {
+          term(acc, 1, 0, 1);
+          term(acc, 0, 0, 7);
+        } else {
+          term(acc, 1, 1, 0);
+          term(acc, 1, 0, 2);
+          term(acc, 0, 1, 6);
+          term(acc, 0, 0, 8);
+        }
+        st16(dx + (((int64_t)b * H + h) * W + w) * Cp + cv * VE, acc);
+      }
+  }
+}
+
 // ------------------------------------------------------------------ space-to-depth stem
 // One thread per s2d pixel: its cps channels = 4 sub-positions (i, j) x c input channels.
 // the ResNet-50 stem case: bf16, 8-channel input pixels (one 16-byte load each), 16 s2d channels
@@ -1666,6 +1784,12 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, i
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp % V16<T>::N || (int64_t)B * H * W * Cp >= (1ll << 31)) return cudaErrorInvalidValue;
+    static const bool generic = getenv("DSP_B200_MAXPOOL_GENERIC") != nullptr;  // A/B knob
+    if (sizeof(T) == 2 && !generic) {
+      launch_k(maxpool_fwd_bf16x2_k, grid_for((int64_t)B * P * Q * Cp / 8), kThreads, 0, st, (const uint4*)x, (uint4*)out,
+               (uint2*)arg, B, H, W, P, Q, Cp / 8);
+      return note_launch(), cudaGetLastError();
+    }
     launch_k(maxpool_fwd_k<T>, grid_for((int64_t)B * P * Q * Cp / V16<T>::N), kThreads, 0, st, (const T*)x, (T*)out, arg, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();
@@ -1677,6 +1801,13 @@ cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void*
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp % V16<T>::N || (int64_t)B * H * W * Cp >= (1ll << 31)) return cudaErrorInvalidValue;
+    static const bool generic = getenv("DSP_B200_MAXPOOL_GENERIC") != nullptr;  // A/B knob
+    // the quad form covers input rows / columns [0, 2P) x [0, 2Q): exactly H x W when 2P >= H, 2Q >= W
+    if (!generic && 2 * P >= H && 2 * Q >= W) {
+      launch_k(maxpool_bwd_quad_k<T>, grid_for((int64_t)B * P * Q * Cp / V16<T>::N), kThreads, 0, st, (const T*)u, arg,
+               (T*)dx, B, H, W, P, Q, Cp);
+      return note_launch(), cudaGetLastError();
+    }
     launch_k(maxpool_bwd_k<T>, grid_for((int64_t)B * H * W * Cp / V16<T>::N), kThreads, 0, st, (const T*)u, arg, (T*)dx, B, H, W, P, Q,
                                                                             Cp);
     return note_launch(), cudaGetLastError();

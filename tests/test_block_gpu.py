@@ -140,6 +140,13 @@ def test_pools_and_head():
     _check(*_run_block(layers, 8, last=True))
 
 
+def test_pools_odd_maxpool_input():
+    """3x3/2 max pool on an odd 13x13 map (7x7 windows; the last window row / column clipped): the
+    quad backward's edge quads and the packed forward's padding taps."""
+    layers = [P.conv_bn_relu((3, 13, 13), 16), P.maxpool((16, 13, 13)), P.avgpool((16, 7, 7)), P.dense(16, 10)]
+    _check(*_run_block(layers, 8, last=True))
+
+
 def test_mlp_kinds():
     layers = [P.dense(12, 16), P.relu(), P.dense(16, 12), P.tanh(), P.dense(12, 4)]
     _check(*_run_block(layers, 16, last=True))
