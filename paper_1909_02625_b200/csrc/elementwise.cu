@@ -1241,6 +1241,51 @@ __global__ void __launch_bounds__(256) wgrad_reduce_k(const float* __restrict__ 
   }
 }
 
+// Tiled form for outputs of >= 148 32x32 tiles (the wide stage-3/4 convs: few splits, millions of
+// weights): CTA = 32 rows (m) x 32 columns (n) of the partials, thread (n, 4 rows) sums the splits
+// in ascending order with 4 splits' loads in flight, and the tile is transposed through shared
+// memory so the [co][tap][ci] stores run along ci (the row-major form wrote 4-byte scattered
+// stores with a stride of RS*ci: 23-41 us per stage-4 reduce).
+__global__ void __launch_bounds__(256) wgrad_reduce_tiled_k(const float* __restrict__ part, int splits, int Mw, int N,
+                                                           int RS, int Cp, int ci_real, int co_real,
+                                                           float* __restrict__ grad) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: rows 4 ty .. 4 ty + 3
+  const int m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+  const size_t zs = (size_t)Mw * N;
+  const int n = n0 + tx;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (n < N) {
+    for (int z = 0; z < splits; z += 4) {
+      float v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int m = m0 + 4 * ty + i;
+          v[u][i] = (z + u < splits && m < Mw) ? __ldcg(part + (size_t)(z + u) * zs + (size_t)m * N + n) : 0.f;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] += v[u][i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tile[4 * ty + i][tx] = acc[i];
+  __syncthreads();
+  // write: lane = row (m -> (tap, ci)), 4 columns (co) per warp
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + tx, nn = n0 + 4 * ty + i;
+    if (m >= Mw || nn >= co_real) continue;
+    const int ci = m % Cp, tap = m / Cp;
+    if (ci >= ci_real || tap >= RS) continue;
+    grad[((int64_t)nn * RS + tap) * ci_real + ci] = tile[tx][4 * ty + i];
+  }
+}
+
 template <typename T>
 __global__ void pack_weights_k(const float* __restrict__ params, T* __restrict__ packed,
                                const PackEntry* __restrict__ ents, int n_entries) {
@@ -1827,6 +1872,13 @@ cudaError_t wgrad_reduce(const float* part, int splits, int Mw, int N, int RS, i
                          int dense_layout, float* grad, cudaStream_t st, int s2d_r) {
   const int64_t total = (int64_t)Mw * N;
   if (N % 4) return cudaErrorInvalidValue;
+  const int64_t tiles = (int64_t)((Mw + 31) / 32) * ((N + 31) / 32);
+  static const bool flat = getenv("DSP_B200_WGRAD_REDUCE_FLAT") != nullptr;  // A/B knob
+  if (dense_layout == 0 && tiles >= 148 && !flat) {
+    launch_k(wgrad_reduce_tiled_k, dim3((Mw + 31) / 32, (N + 31) / 32), 256, 0, st, part, splits, Mw, N, RS, Cp, ci_real,
+             co_real, grad);
+    return note_launch(), cudaGetLastError();
+  }
   launch_k(wgrad_reduce_k, (unsigned)((total + 127) / 128), 256, 0, st, part, splits, Mw, N, RS, Cp, ci_real, co_real,
            dense_layout, grad, s2d_r);
   return note_launch(), cudaGetLastError();
