@@ -126,6 +126,41 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 template <int NT>
 __device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
+// Reduce-scatter over the 8 lanes sharing lane % 4 (lane bits 4, 3, 2; fixed tree) of two 8-column
+// partial-sum vectors a, b: each step keeps the half of the columns selected by the lane bit and
+// adds the partner's copy, so lane (k4, cg = lane >> 2) ends with column cg's totals in ra / rb --
+// 14 shuffles instead of a 48-shuffle butterfly. with_a = false skips a (rb only, 7 shuffles).
+__device__ __forceinline__ void rs8_pair(const float (&a)[8], const float (&b)[8], int lane, bool with_a, float& ra,
+                                         float& rb) {
+  const int cg = lane >> 2;
+  float v[8];
+  {
+    const bool hb = (cg >> 2) & 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float k1 = hb ? a[4 + i] : a[i], o1 = hb ? a[i] : a[4 + i];
+      const float k2 = hb ? b[4 + i] : b[i], o2 = hb ? b[i] : b[4 + i];
+      v[2 * i] = k1 + (with_a ? __shfl_xor_sync(0xffffffffu, o1, 16) : 0.f);
+      v[2 * i + 1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 16);
+    }
+  }
+  {
+    const bool hb = (cg >> 1) & 1;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float k1 = hb ? v[2 * (2 + i)] : v[2 * i], o1 = hb ? v[2 * i] : v[2 * (2 + i)];
+      const float k2 = hb ? v[2 * (2 + i) + 1] : v[2 * i + 1], o2 = hb ? v[2 * i + 1] : v[2 * (2 + i) + 1];
+      v[2 * i] = k1 + (with_a ? __shfl_xor_sync(0xffffffffu, o1, 8) : 0.f);
+      v[2 * i + 1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 8);
+    }
+  }
+  const bool hb = cg & 1;
+  const float k1 = hb ? v[2] : v[0], o1 = hb ? v[0] : v[2];
+  const float k2 = hb ? v[3] : v[1], o2 = hb ? v[1] : v[3];
+  ra = k1 + (with_a ? __shfl_xor_sync(0xffffffffu, o1, 4) : 0.f);
+  rb = k2 + __shfl_xor_sync(0xffffffffu, o2, 4);
+}
+
 // Column sums of a 32-row x 16-column register tile (one row per lane) with 16
 // shuffles: halve the column set at each butterfly step. Lane l ends holding the
 // full sum of column (l >> 1) & 15.
@@ -1151,39 +1186,11 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                   yr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.bnb[1].y) + o));
                 }
               }
-              // reduce-scatter over the 8 lanes of the chunk (lane bits 4, 3, 2; fixed tree): each
-              // step keeps the half of the columns selected by the lane bit and adds the partner's
-              // copy of it, so lane (k4, cg = lane >> 2) ends with column cg's sums -- 14 shuffles
-              // instead of a 48-shuffle butterfly, and all 32 lanes update red[] at once
+              // 8-lane reduce-scatter: lane (k4, cg) ends with column cl + cg's sums; every lane
+              // updates the CTA partials at once
               const int cg = lane >> 2;
-              float v[8];  // (column, statistic) pairs still held: s1 / s2 of 4, 2, 1 columns
-              {
-                const bool hb = (cg >> 2) & 1;  // off 16: keep columns 4..7 (hb) or 0..3
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const float k1 = hb ? s1[4 + i] : s1[i], o1 = hb ? s1[i] : s1[4 + i];
-                  const float k2 = hb ? s2[4 + i] : s2[i], o2 = hb ? s2[i] : s2[4 + i];
-                  v[2 * i] = k1 + (t == 0 ? __shfl_xor_sync(0xffffffffu, o1, 16) : 0.f);
-                  v[2 * i + 1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 16);
-                }
-              }
-              {
-                const bool hb = (cg >> 1) & 1;  // off 8: keep columns 2,3 (hb) or 0,1 of the four
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                  const float k1 = hb ? v[2 * (2 + i)] : v[2 * i], o1 = hb ? v[2 * i] : v[2 * (2 + i)];
-                  const float k2 = hb ? v[2 * (2 + i) + 1] : v[2 * i + 1], o2 = hb ? v[2 * i + 1] : v[2 * (2 + i) + 1];
-                  v[2 * i] = k1 + (t == 0 ? __shfl_xor_sync(0xffffffffu, o1, 8) : 0.f);
-                  v[2 * i + 1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 8);
-                }
-              }
-              {
-                const bool hb = cg & 1;  // off 4: keep column 1 (hb) or 0 of the two
-                const float k1 = hb ? v[2] : v[0], o1 = hb ? v[0] : v[2];
-                const float k2 = hb ? v[3] : v[1], o2 = hb ? v[1] : v[3];
-                v[0] = k1 + (t == 0 ? __shfl_xor_sync(0xffffffffu, o1, 4) : 0.f);
-                v[1] = k2 + __shfl_xor_sync(0xffffffffu, o2, 4);
-              }
+              float v[2];
+              rs8_pair(s1, s2, lane, t == 0, v[0], v[1]);
               if (t == 0) red[q][cl + cg][0] += v[0];
               red[q][cl + cg][1 + t] += v[1];
             }
@@ -1210,42 +1217,38 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                          : "memory");
           }
           __syncwarp();
+          // lane = (row r = lane / 4 + 8 it, 16-byte chunk k4): each slab read feeds both the store
+          // (8 rows of 64 contiguous bytes per warp store) and the BN statistics of its 8 columns,
+          // reduced over the chunk's 8 lanes by reduce-scatter (the column-pair form re-read the slab
+          // with 16 4-byte loads per lane: L1 84% busy, profiles/r02_fprop_epilogue.md)
+          const int k4 = lane & 3;
+          float s1[8], s2[8];
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {  // 8 rows per pass, 4 lanes (64 contiguous bytes) per row
-            const int r = (lane >> 2) + 8 * it, k = lane & 3;
+          for (int j = 0; j < 8; ++j) s1[j] = s2[j] = 0.f;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int r = (lane >> 2) + 8 * it;
             uint4 raw;
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
-                         : "r"(sDW + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)));
-            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k * 8) = raw;
+                         : "r"(sDW + r * 64 + ((k4 ^ ((r >> 1) & 3)) << 4)));
+            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) = raw;
+            if (want_stats) {
+              const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float y = __uint_as_float((j & 1) ? (w4[j >> 1] & 0xffff0000u) : (w4[j >> 1] << 16));
+                s1[j] += y;
+                s2[j] = fmaf(y, y, s2[j]);
+              }
+            }
           }
           if (want_stats) {
-            // lane: column pair cp (tile columns col0 + 2cp, +1) over rows rh, rh + 2, ... (rh = lane >> 4)
-            const int cp = lane & 15, rh = lane >> 4;
-            float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
-#pragma unroll
-            for (int it = 0; it < 16; ++it) {
-              const int r = rh + 2 * it;
-              uint32_t w;
-              asm volatile("ld.shared.b32 %0, [%1];"
-                           : "=r"(w)
-                           : "r"(sDW + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4));
-              const float ya = __uint_as_float(w << 16), yb = __uint_as_float(w & 0xffff0000u);
-              s1a += ya;
-              s2a = fmaf(ya, ya, s2a);
-              s1b += yb;
-              s2b = fmaf(yb, yb, s2b);
-            }
-            s1a += __shfl_xor_sync(0xffffffffu, s1a, 16);
-            s1b += __shfl_xor_sync(0xffffffffu, s1b, 16);
-            s2a += __shfl_xor_sync(0xffffffffu, s2a, 16);
-            s2b += __shfl_xor_sync(0xffffffffu, s2b, 16);
-            if (lane < 16) {
-              red[q][col0 + 2 * cp][0] += s1a;
-              red[q][col0 + 2 * cp][1] += s2a;
-              red[q][col0 + 2 * cp + 1][0] += s1b;
-              red[q][col0 + 2 * cp + 1][1] += s2b;
-            }
+            float v0, v1;
+            rs8_pair(s1, s2, lane, true, v0, v1);
+            const int c = col0 + k4 * 8 + (lane >> 2);
+            red[q][c][0] += v0;
+            red[q][c][1] += v1;
           }
           __syncwarp();  // the slab is rewritten by the next chunk
         }
