@@ -1047,6 +1047,11 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           // back as lane = row (a lane-per-row global load touched 32 lines per instruction: the L1
           // was the bottleneck, 87% busy, and register-held prefetches spilled;
           // profiles/r02_dgrad_epilogue.md)
+          // the accumulator chunk's TMEM load is issued first and waited for after the residual /
+          // mask requests are out, so its latency overlaps theirs (16% of this epilogue's stall
+          // samples waited on tcgen05.wait::ld right behind the load)
+          uint32_t tr[32];
+          tmem_ld32_issue(tl + col0, tr);
           if (a.residual != nullptr) {
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
@@ -1064,12 +1069,14 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           const uint32_t mw = mword ? __ldg(reinterpret_cast<const uint32_t*>(a.bnb_mask_bits) +
                                             (((size_t)(rbase + lane) * a.ldd + n0 + col0) >> 5))
                                     : 0u;
+          tmem_ld_wait(tr);
+          float vb[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) vb[e] = __uint_as_float(tr[e]);
           if (a.residual != nullptr) {
             cp_async_wait<0>();
             __syncwarp();
           }
-          float vb[32];
-          tmem_ld32(tl + col0, vb);
           if (a.residual != nullptr) {  // row `lane` of the staged residual, one 16-byte chunk at a time
 #pragma unroll
             for (int k = 0; k < 4; ++k) {

@@ -36,13 +36,21 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--r50-block", type=int, default=-1,
                     help="instead of --block: block k of ResNet-50 cut into K=4 FLOP-balanced blocks (B=256)")
+    ap.add_argument("--r56-block", type=int, default=-1,
+                    help="instead of --block: block k of ResNet-56 cut into K=4 FLOP-balanced blocks (B=128)")
     args = ap.parse_args()
     import torch
 
     from paper_1909_02625_b200 import _lib as L
     from paper_1909_02625_b200.runtime import DeviceBlock
 
-    if args.r50_block >= 0:
+    if args.r56_block >= 0:
+        full = P.resnet_cifar_layers(56, 10)
+        cuts = [0] + P.flop_balanced_boundaries(full, 4) + [len(full)]
+        layers, B = full[cuts[args.r56_block]:cuts[args.r56_block + 1]], 128
+        last = args.r56_block == 3
+        args.r50_block = -1
+    elif args.r50_block >= 0:
         full = P.resnet50_layers()
         cuts = [0] + P.flop_balanced_boundaries(full, 4) + [len(full)]
         layers, B = full[cuts[args.r50_block]:cuts[args.r50_block + 1]], 256
@@ -65,7 +73,7 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     labels = torch.zeros(B, dtype=torch.int64, device="cuda")
     loss = torch.zeros(1, device="cuda")
-    first = args.r50_block == 0
+    first = args.r50_block == 0 or args.r56_block == 0
     for r in range(args.reps):
         if r == args.reps - 1:
             ev[0].record(st)
@@ -79,7 +87,8 @@ def main():
         if r == args.reps - 1:
             ev[1].record(st)
     torch.cuda.synchronize()
-    name = f"resnet50 block {args.r50_block}" if args.r50_block >= 0 else args.block
+    name = (f"resnet50 block {args.r50_block}" if args.r50_block >= 0 else
+            f"resnet56 block {args.r56_block}" if args.r56_block >= 0 else args.block)
     print(f"{name}: one fwd + recompute + bwd + update {ev[0].elapsed_time(ev[1]) * 1000:.1f} us "
           f"({model.blocks[0].param_count} params)")
 
