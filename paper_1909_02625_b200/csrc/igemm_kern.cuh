@@ -1069,6 +1069,27 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           const uint32_t mw = mword ? __ldg(reinterpret_cast<const uint32_t*>(a.bnb_mask_bits) +
                                             (((size_t)(rbase + lane) * a.ldd + n0 + col0) >> 5))
                                     : 0u;
+          // y (and mask-byte) row chunks of the statistics, requested before the accumulator wait too
+          const int k4 = lane & 3;
+          const bool mbits = a.bnb_mask_bits != nullptr;  // else the mask is recomputed from y (fastd)
+          uint4 yr[4];
+          uint32_t mb8[4];
+          auto load_y = [&](const void* y) {
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const size_t o = (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8;
+              yr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(y) + o));
+            }
+          };
+          if (want_stats) {
+            load_y(a.bnb[0].y);
+            if (mbits && !mword) {
+#pragma unroll
+              for (int it = 0; it < 4; ++it)
+                mb8[it] = __ldg(a.bnb_mask_bits +
+                                (((size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8) >> 3));
+            }
+          }
           tmem_ld_wait(tr);
           float vb[32];
 #pragma unroll
@@ -1111,26 +1132,6 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           // coalesced 64-byte row segments, 4 (8 for two targets) loads per lane per chunk, all in
           // flight before the slab reads -- and the 8 lanes of a chunk reduced by shuffles in fixed
           // order (the 2-column-per-lane form issued 4-byte loads in two latency-bound batches)
-          const int k4 = lane & 3;
-          const bool mbits = a.bnb_mask_bits != nullptr;  // else the mask is recomputed from y (fastd)
-          uint4 yr[4];
-          uint32_t mb8[4];
-          auto load_y = [&](const void* y) {
-#pragma unroll
-            for (int it = 0; it < 4; ++it) {
-              const size_t o = (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8;
-              yr[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(y) + o));
-            }
-          };
-          if (want_stats) {
-            load_y(a.bnb[0].y);
-            if (mbits && !mword) {
-#pragma unroll
-              for (int it = 0; it < 4; ++it)
-                mb8[it] = __ldg(a.bnb_mask_bits +
-                                (((size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8) >> 3));
-            }
-          }
           // this lane's slab chunk of row r (the stored dX; re-read for the statistics rather than
           // held in registers across the y loads' latency)
           auto slab = [&](int it) {
