@@ -21,6 +21,12 @@ static cudaError_t launch_mode(const dsp_igemm_args_t& a, int splits, cudaStream
   // two CTAs per SM give each SM twice the epilogue warps of one 256-wide CTA
   static const bool wide = getenv("DSP_B200_SHORTK_WIDE") != nullptr;
   if (!wide && MODE != DSP_IGEMM_WGRAD && a.Kd <= 128) return launch_bn<T, MODE, 128>(a, splits, st);
+  // DGRADs with a residual or fused BN-backward statistics are epilogue-bound up to Kd = 512: 128-wide
+  // tiles at two CTAs per SM (ResNet-50 unit-input DGRADs: stage 3 116 -> 105 us, stage 4 75 -> 67 us;
+  // the Kd = 1024 reduce-conv DGRAD gets slower, 58 -> 64 us). DSP_B200_DGRAD_BN128_KD overrides.
+  static const int dg_kd = getenv("DSP_B200_DGRAD_BN128_KD") ? atoi(getenv("DSP_B200_DGRAD_BN128_KD")) : 512;
+  if (MODE == DSP_IGEMM_DGRAD && a.Kd <= dg_kd && (a.residual != nullptr || a.bnb_count > 0))
+    return launch_bn<T, MODE, 128>(a, splits, st);
   return launch_bn<T, MODE, 256>(a, splits, st);
 }
 
