@@ -991,6 +991,16 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                     !(a.out_f32 & 1);
     const uint32_t sDW = sA0 + Cfg::RING + Cfg::OUT_BYTES + (uint32_t)(warp - IG_EPI_WARP0) * 2048;
     int dwc = 0;  // slabs this warp has staged
+    // FPROP fast path with <= 2 column chunks per warp: each lane's BN partial sums (8 columns x
+    // its rows) stay in registers across all of the CTA's tiles (the CTA owns one n-tile, so a
+    // lane's columns never change) and are reduced across lanes once, after the last tile
+    constexpr int FCH = (MODE == DSP_IGEMM_FPROP && sizeof(T) == 2) ? BN / 16 / (NEPI / 4) / 2 : 0;
+    constexpr bool FACC = FCH >= 1 && FCH <= 2;
+    float fa1[FACC ? FCH : 1][8], fa2[FACC ? FCH : 1][8];
+#pragma unroll
+    for (int c = 0; c < (FACC ? FCH : 1); ++c)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fa1[c][j] = fa2[c][j] = 0.f;
     int i = 0;
     int m0, n0, z, kb0, kb1;
     for (; get_unit(i, m0, n0, z, kb0, kb1); ++i) {
@@ -1207,7 +1217,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
         }
       } else if (fast) {
         const int rbase = m0 + q * 32;
-#pragma unroll 1
+#pragma unroll
         for (int c2 = 0; c2 < CPW; c2 += 2) {
           const int col0 = (half * CPW + c2) * 16;  // this chunk: tile columns [col0, col0 + 32)
           float vb[32];
@@ -1232,7 +1242,10 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           const int k4 = lane & 3;
           float s1[8], s2[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) s1[j] = s2[j] = 0.f;
+          for (int j = 0; j < 8; ++j) {
+            s1[j] = FACC ? fa1[FACC ? c2 / 2 : 0][j] : 0.f;
+            s2[j] = FACC ? fa2[FACC ? c2 / 2 : 0][j] : 0.f;
+          }
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
             const int r = (lane >> 2) + 8 * it;
@@ -1252,11 +1265,19 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
             }
           }
           if (want_stats) {
-            float v0, v1;
-            rs8_pair(s1, s2, lane, true, v0, v1);
-            const int c = col0 + k4 * 8 + (lane >> 2);
-            red[q][c][0] += v0;
-            red[q][c][1] += v1;
+            if constexpr (FACC) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                fa1[c2 / 2][j] = s1[j];
+                fa2[c2 / 2][j] = s2[j];
+              }
+            } else {
+              float v0, v1;
+              rs8_pair(s1, s2, lane, true, v0, v1);
+              const int c = col0 + k4 * 8 + (lane >> 2);
+              red[q][c][0] += v0;
+              red[q][c][1] += v1;
+            }
           }
           __syncwarp();  // the slab is rewritten by the next chunk
         }
@@ -1491,6 +1512,18 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
       IG_TRACE(145 + 2 * i, et == 0 && i < 16);
     }
     if (tma_out && et == 0) bulk_wait0();
+    if constexpr (FACC) {
+      if (want_stats && dw) {  // the register-held fast-path partials (zeros if no tile took it)
+#pragma unroll
+        for (int c = 0; c < FCH; ++c) {
+          float v0, v1;
+          rs8_pair(fa1[c], fa2[c], lane, true, v0, v1);
+          const int col = (half * (BN / 16 / (NEPI / 4)) + 2 * c) * 16 + (lane & 3) * 8 + (lane >> 2);
+          red[q][col][0] += v0;
+          red[q][col][1] += v1;
+        }
+      }
+    }
     if (want_stats) {
       epi_barrier<EPI_T>();
       const int n0c = (blockIdx.x % nt) * BN;
