@@ -279,7 +279,8 @@ struct IgTma {
   int i2c;
   int s2;       // stride-2 DGRAD split by output parity (ph, pw) into stride-1 sub-convolutions of dY
   int a2d;      // im2col plan of a 1x1 stride-1 conv: A is a plain [pixels][C] matrix (2-D tiled boxes)
-  int d_warp;   // wide-tile epilogue: per-warp 32 x 16 slabs staged in smem, TMA-stored (box {16, 32})
+  int d_warp;   // wide-tile epilogue: per-warp 32-row x 64-byte slabs staged in smem
+  int d_tma;    // ... and stored by TMA from the slab (tmD: box {32 columns, 32 rows}, SWIZZLE_64B)
   int i2c_pad;  // start coordinate of output pixel (p, q) = (p * st - i2c_pad, q * st - i2c_pad)
   // FastDiv multipliers computed on the host (64-bit divisions are slow on device):
   // [0] output pixels / image, [1] output row width, [2] gathered channels, [3] S, [4] K
@@ -1062,6 +1063,10 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
           // samples waited on tcgen05.wait::ld right behind the load)
           uint32_t tr[32];
           tmem_ld32_issue(tl + col0, tr);
+          if (tm.d_tma) {  // the previous chunk's TMA store has read the slab
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
           if (a.residual != nullptr) {
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
@@ -1136,7 +1141,12 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                          "r"(pk[4 * k + 2]), "r"(pk[4 * k + 3])
                          : "memory");
           }
+          if (tm.d_tma) fence_proxy_async_smem();
           __syncwarp();
+          if (tm.d_tma && lane == 0) {
+            tma_store_2d(&tmD, sDW, n0 + col0, rbase);
+            bulk_commit();
+          }
           // lane = (row r = lane / 4 + 8 it, 16-byte chunk k4): the slab read that feeds the store
           // also feeds the statistics, with y (and mask) read as the same 16-byte row chunks --
           // coalesced 64-byte row segments, 4 (8 for two targets) loads per lane per chunk, all in
@@ -1152,11 +1162,13 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                          : "r"(sDW + r * 64 + ((k4 ^ ((r >> 1) & 3)) << 4)));
             return v;
           };
+          if (!tm.d_tma) {
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            const int r = (lane >> 2) + 8 * it;
-            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) =
-                slab(it);
+            for (int it = 0; it < 4; ++it) {
+              const int r = (lane >> 2) + 8 * it;
+              *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) =
+                  slab(it);
+            }
           }
           if (want_stats) {
             const int cl = col0 + k4 * 8;  // tile columns cl .. cl + 7
@@ -1226,7 +1238,12 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk[j]) : "f"(vb[2 * j + 1]), "f"(vb[2 * j]));
-          // row `lane`: 4 x 16-byte chunks, chunk k at position k ^ ((lane >> 1) & 3)
+          // row `lane`: 4 x 16-byte chunks, chunk k at position k ^ ((lane >> 1) & 3) (= the TMA
+          // SWIZZLE_64B layout of a 32-row x 64-byte box)
+          if (tm.d_tma) {  // the previous chunk's TMA store has read the slab
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t ad = sDW + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4);
@@ -1234,7 +1251,12 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                          "r"(pk[4 * k + 2]), "r"(pk[4 * k + 3])
                          : "memory");
           }
+          if (tm.d_tma) fence_proxy_async_smem();
           __syncwarp();
+          if (tm.d_tma && lane == 0) {
+            tma_store_2d(&tmD, sDW, n0 + col0, rbase);
+            bulk_commit();
+          }
           // lane = (row r = lane / 4 + 8 it, 16-byte chunk k4): each slab read feeds both the store
           // (8 rows of 64 contiguous bytes per warp store) and the BN statistics of its 8 columns,
           // reduced over the chunk's 8 lanes by reduce-scatter (the column-pair form re-read the slab
@@ -1253,7 +1275,8 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
                          : "r"(sDW + r * 64 + ((k4 ^ ((r >> 1) & 3)) << 4)));
-            *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) = raw;
+            if (!tm.d_tma)
+              *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) = raw;
             if (want_stats) {
               const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
@@ -1512,6 +1535,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
       IG_TRACE(145 + 2 * i, et == 0 && i < 16);
     }
     if (tma_out && et == 0) bulk_wait0();
+    if (tm.d_tma && lane == 0) bulk_wait_read0();  // slab reads only: the stores complete after the ticket
     if constexpr (FACC) {
       if (want_stats && dw) {  // the register-held fast-path partials (zeros if no tile took it)
 #pragma unroll
@@ -2142,8 +2166,22 @@ static void dwarp_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
   if (disabled || tm.halo || (tm.i2c ? IgCfg<BN, true>::DW_BYTES : IgCfg<BN>::DW_BYTES) == 0 || MODE == DSP_IGEMM_WGRAD || sizeof(T) != 2 || (a.out_f32 & 1))
     return;
   if ((reinterpret_cast<uintptr_t>(a.D) & 15) || (a.ldd % 8) || a.N % 16 || a.ldd < a.N) return;
-  (void)tmD;
   tm.d_warp = 1;
+  // FPROP / DGRAD slabs leave through TMA stores: the async-proxy stores are not drained by the release
+  // fence of the BN-finalize ticket, so the finalize no longer waits behind the CTA's last output
+  // stores (4-8.5 us per launch, profiles/r01_fin_trace.log)
+  static const bool no_dtma = getenv("DSP_B200_NO_DTMA") != nullptr;
+  if (no_dtma || (a.ldd * 2) % 16) return;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (enc == nullptr) return;
+  cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
+  cuuint64_t strides[1] = {(cuuint64_t)a.ldd * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&tmD, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  tm.d_tma = 1;
 }
 
 // fp32 storage (3xTF32): 2 stages of hi + lo operand tiles (igemm_kernel F32_SPLIT)
