@@ -2172,6 +2172,15 @@ static void dwarp_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
   // stores (4-8.5 us per launch, profiles/r01_fin_trace.log)
   static const bool no_dtma = getenv("DSP_B200_NO_DTMA") != nullptr;
   if (no_dtma || (a.ldd * 2) % 16) return;
+  {  // only into this device's memory (a multi-device engine's DGRAD may write a peer's ring slot)
+    cudaPointerAttributes pa{};
+    int dev = -1;
+    if (cudaPointerGetAttributes(&pa, a.D) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess ||
+        pa.type != cudaMemoryTypeDevice || pa.device != dev) {
+      cudaGetLastError();
+      return;
+    }
+  }
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (enc == nullptr) return;
   cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
