@@ -414,6 +414,47 @@ __global__ void __launch_bounds__(kThreads, 2) bn_bwd_reduce_k(const T* __restri
   if (tid == 0) *fin.sem = 0;
 }
 
+// Column-parallel finalize of the BN-backward partials for wide tensors (Cp >= 512): CTA = 32
+// columns x 32 row lanes (coalesced 128-byte reads of every chunk's partial row), fixed-order double
+// sums. The fused last-CTA finalize read all chunks x Cp partials on ONE SM: 4.8 MB at Cp = 2048,
+// most of a 125 us stage-4 reduction (0.85 TB/s, profiles/r02_r50_block3_launches.csv).
+__global__ void __launch_bounds__(1024) bn_bwd_finalize_cols_k(const float* __restrict__ part, int chunks, int Cp,
+                                                              int c_real, double count,
+                                                              const float* __restrict__ gamma,
+                                                              const float* __restrict__ stat,
+                                                              float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                              float* __restrict__ coef) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  __shared__ double sm[32][2][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double a = 0.0, b = 0.0;
+  if (c < Cp) {
+    for (int t = w; t < chunks; t += 32) {
+      a += (double)part[((size_t)t * 2 + 0) * Cp + c];
+      b += (double)part[((size_t)t * 2 + 1) * Cp + c];
+    }
+  }
+  sm[w][0][lane] = a;
+  sm[w][1][lane] = b;
+  __syncthreads();
+  if (w != 0 || c >= Cp) return;
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    s1 += sm[j][0][lane];
+    s2 += sm[j][1][lane];
+  }
+  const bool real = c < c_real;
+  if (real && dbeta) dbeta[c] = (float)s1;
+  if (real && dgamma && gamma) dgamma[c] = (float)s2;
+  if (coef) {
+    coef[c] = (real && gamma) ? gamma[c] * stat[Cp + c] : 0.f;
+    coef[Cp + c] = real ? (float)(s1 / count) : 0.f;
+    coef[2 * Cp + c] = real ? (float)(s2 / count) : 0.f;
+  }
+}
+
 __global__ void bn_bwd_finalize_k(const float* __restrict__ part, int chunks, int Cp, int c_real, double count,
                                   const float* __restrict__ gamma, const float* __restrict__ stat,
                                   float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ coef) {
@@ -1733,13 +1774,23 @@ cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const vo
                          int* sem, cudaStream_t st, int relu_y, const uint8_t* mbits) {
   const int chunks = bn_bwd_chunks(M, Cp);
   const int rows = (int)bn_rows_per_chunk(M, Cp);
-  const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sem};
+  // wide tensors: a column-parallel finalize launch instead of the last CTA's (DSP_B200_BNR_COLS
+  // sets the width from which it is used; 0 = never)
+  static const int cols_from = getenv("DSP_B200_BNR_COLS") ? atoi(getenv("DSP_B200_BNR_COLS")) : 512;
+  const bool sep = cols_from > 0 && Cp >= cols_from;
+  const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sep ? nullptr : sem};
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
     if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
     launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
              rows, fin, relu_y, mbits);
-    return note_launch(), cudaGetLastError();
+    note_launch();
+    if (sep) {
+      launch_k(bn_bwd_finalize_cols_k, (Cp + 31) / 32, 1024, 0, st, part, chunks, Cp, c_real, (double)M, gamma, stat,
+               dgamma, dbeta, coef);
+      note_launch();
+    }
+    return cudaGetLastError();
   });
 }
 
