@@ -1726,7 +1726,12 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
                (const T*)res, (const T*)y2, stat2, (T*)out, nvec, Cp, relu, mbits);
     };
     if (nvec > kWave && var == 0 && (kThreads % (Cp / V16<T>::N)) == 0) {
-      if (y2 != nullptr) go_rg(bn_apply_rg_k<T, 2, 2, true>);
+      static const int y2v = getenv("DSP_B200_BNA_Y2") ? atoi(getenv("DSP_B200_BNA_Y2")) : 14;  // A/B knob: 14 = UNR 1 at 4 CTAs/SM (ResNet-50 first unit 247 -> 218 us)
+      if (y2 != nullptr) {
+        if (y2v == 14) go_rg(bn_apply_rg_k<T, 1, 4, true>);
+        else if (y2v == 13) go_rg(bn_apply_rg_k<T, 1, 3, true>);
+        else go_rg(bn_apply_rg_k<T, 2, 2, true>);
+      }
       else go_rg(bn_apply_rg_k<T, 2, 4, false>);
     } else if (nvec > kWave) {
       if (var == 23) go(bn_apply_k_lb<T, 2, 3>);
