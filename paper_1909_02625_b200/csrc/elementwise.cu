@@ -1732,7 +1732,13 @@ cudaError_t bn_apply(int dtype, const void* y, const float* stat, const void* re
         else if (y2v == 13) go_rg(bn_apply_rg_k<T, 1, 3, true>);
         else go_rg(bn_apply_rg_k<T, 2, 2, true>);
       }
-      else go_rg(bn_apply_rg_k<T, 2, 4, false>);
+      else {
+        static const int pv = getenv("DSP_B200_BNA_RG") ? atoi(getenv("DSP_B200_BNA_RG")) : 24;  // A/B knob
+        if (pv == 14) go_rg(bn_apply_rg_k<T, 1, 4, false>);
+        else if (pv == 16) go_rg(bn_apply_rg_k<T, 1, 6, false>);
+        else if (pv == 44) go_rg(bn_apply_rg_k<T, 4, 4, false>);
+        else go_rg(bn_apply_rg_k<T, 2, 4, false>);
+      }
     } else if (nvec > kWave) {
       if (var == 23) go(bn_apply_k_lb<T, 2, 3>);
       else if (var == 24) go(bn_apply_k_lb<T, 2, 4>);
@@ -1829,9 +1835,23 @@ cudaError_t bn_bwd_apply(int dtype, const void* gsrc, const void* mask, const vo
                (const T*)y_b, stat_b, coef_b, (T*)dy_b, (T*)g_out, nvec, Cp, relu_y, mbits);
     };
     if (nvec > kWave && rg) {
-      if (y_b != nullptr) go_rg(bn_bwd_apply_rg_k<T, 1, 2, 2>);
-      else if (relu_y) go_rg(bn_bwd_apply_rg_k<T, 2, 2, 1>);
-      else go_rg(bn_bwd_apply_rg_k<T, 2, 2, 0>);
+      // A/B knobs (10*UNR + CTAs/SM) per mask kind
+      static const int k0 = getenv("DSP_B200_BNB_K0") ? atoi(getenv("DSP_B200_BNB_K0")) : 22;
+      static const int k1 = getenv("DSP_B200_BNB_K1") ? atoi(getenv("DSP_B200_BNB_K1")) : 22;
+      static const int k2 = getenv("DSP_B200_BNB_K2") ? atoi(getenv("DSP_B200_BNB_K2")) : 12;
+      if (y_b != nullptr) {
+        if (k2 == 13) go_rg(bn_bwd_apply_rg_k<T, 1, 3, 2>);
+        else go_rg(bn_bwd_apply_rg_k<T, 1, 2, 2>);
+      } else if (relu_y) {
+        if (k1 == 13) go_rg(bn_bwd_apply_rg_k<T, 1, 3, 1>);
+        else if (k1 == 14) go_rg(bn_bwd_apply_rg_k<T, 1, 4, 1>);
+        else go_rg(bn_bwd_apply_rg_k<T, 2, 2, 1>);
+      } else {
+        if (k0 == 13) go_rg(bn_bwd_apply_rg_k<T, 1, 3, 0>);
+        else if (k0 == 14) go_rg(bn_bwd_apply_rg_k<T, 1, 4, 0>);
+        else if (k0 == 23) go_rg(bn_bwd_apply_rg_k<T, 2, 3, 0>);
+        else go_rg(bn_bwd_apply_rg_k<T, 2, 2, 0>);
+      }
     } else if (nvec > kWave) {
       if (var == 23) go(bn_bwd_apply_k_lb<T, 2, 3>);
       else if (var == 24) go(bn_bwd_apply_k_lb<T, 2, 4>);
