@@ -76,6 +76,21 @@ struct MmaTraits<float> {
 #ifndef IG_STAGES_MID
 #define IG_STAGES_MID 2
 #endif
+// WGRAD ring depth for 128 / 64-wide tiles (its grid is ~one CTA per SM, so a deeper ring only costs
+// the SM's co-residency with the other block streams' kernels)
+#ifndef IG_WG_STAGES_128
+#define IG_WG_STAGES_128 3
+#endif
+#ifndef IG_WG_STAGES_64
+#define IG_WG_STAGES_64 4
+#endif
+template <int MODE, int BN, int CFG_STAGES>
+struct IgStages {
+  static constexpr int value = MODE != DSP_IGEMM_WGRAD ? CFG_STAGES
+                               : BN == 128           ? (IG_WG_STAGES_128 > CFG_STAGES ? IG_WG_STAGES_128 : CFG_STAGES)
+                               : BN == 64            ? (IG_WG_STAGES_64 > CFG_STAGES ? IG_WG_STAGES_64 : CFG_STAGES)
+                                                     : CFG_STAGES;
+};
 #ifndef IG_REG_BLOCKS  // register budget as if this many CTAs shared an SM (headroom for other streams)
 #define IG_REG_BLOCKS 3
 #endif
@@ -332,7 +347,7 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
   constexpr int NEPI = IgWarps<NPW, BN, I2C>::NEPI;
   constexpr int EPI_T = NEPI * 32;
   // fp32 storage runs 3xTF32 (see F32_SPLIT below): hi and lo copies of every stage, 2 stages
-  constexpr int STAGES = sizeof(T) == 4 ? 2 : Cfg::STAGES;
+  constexpr int STAGES = sizeof(T) == 4 ? 2 : IgStages<MODE, BN, Cfg::STAGES>::value;
   constexpr int NACC = Cfg::NACC;
   constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
   constexpr int KS = 8 * EPC;               // K extent of one ring stage (128 B per row)
@@ -2209,7 +2224,11 @@ cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
   if (!attr_state[dev]) {
-    const int smax = std::max(std::max(std::max(Cfg::SMEM, IgCfg<BN, true>::SMEM), IG_HALO_SMEM_MAX), f32_smem<T, MODE, BN>());
+    constexpr int wg_extra = (IgStages<MODE, BN, IgCfg<BN, true>::STAGES>::value - IgCfg<BN, true>::STAGES) *
+                             (IG_BM * 128 + BN * 128);
+    const int smax = std::max(std::max(std::max(Cfg::SMEM, IgCfg<BN, true>::SMEM + std::max(wg_extra, 0)),
+                                       IG_HALO_SMEM_MAX),
+                              f32_smem<T, MODE, BN>());
     cudaError_t e = cudaFuncSetAttribute(igemm_kernel<T, MODE, BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smax);
     if (e != cudaSuccess) return e;
@@ -2254,7 +2273,10 @@ cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   tm.fin1 = fin1 ? 1 : 0;
   static const bool force4 = getenv("DSP_B200_NPW4") != nullptr;
   int smem = tm.halo ? tm.h_nst * tm.h_box * a.geom.S + tm.h_nwb * BN * 128
-                     : (tm.i2c ? IgCfg<BN, true>::SMEM : Cfg::SMEM);
+                     : (tm.i2c ? IgCfg<BN, true>::SMEM + (IgStages<MODE, BN, IgCfg<BN, true>::STAGES>::value -
+                                                            IgCfg<BN, true>::STAGES) * (IG_BM * 128 + BN * 128)
+                               : Cfg::SMEM + (IgStages<MODE, BN, Cfg::STAGES>::value - Cfg::STAGES) *
+                                                 (IG_BM * 128 + BN * 128));
   if (sizeof(T) == 4) smem = f32_smem<T, MODE, BN>();
   if (tm.on_a && tm.on_b && (!force4 || tm.i2c))  // nothing to gather: one producer warp
   {
