@@ -73,6 +73,9 @@ struct MmaTraits<float> {
 #ifndef IG_STAGES_SMALL
 #define IG_STAGES_SMALL 3
 #endif
+#ifndef IG_DEEP64_STAGES  // im2col kernels with 64-wide tiles (ResNet-50 stage 1)
+#define IG_DEEP64_STAGES 3
+#endif
 #ifndef IG_STAGES_MID
 #define IG_STAGES_MID 2
 #endif
@@ -114,7 +117,7 @@ constexpr bool kTrace = false;
 // ring at every width <= 64; the CIFAR variants stay shallow so concurrent block streams fit
 template <int BN, bool DEEP = false>
 struct IgCfg {
-  static constexpr int STAGES = (DEEP && BN <= 32) ? 4 : (DEEP && BN == 64) ? 3
+  static constexpr int STAGES = (DEEP && BN <= 32) ? 4 : (DEEP && BN == 64) ? IG_DEEP64_STAGES
                                 : BN <= 32 ? IG_STAGES_SMALL : (BN <= 128 ? IG_STAGES_MID : 4);
   static constexpr int RING = STAGES * (IG_BM * 128 + BN * 128);
 #ifdef IG_TMA_STORE
