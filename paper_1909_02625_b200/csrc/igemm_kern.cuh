@@ -144,6 +144,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 template <int NT>
 __device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
+// bf16 pair (one 32-bit word: element 2j in the low half) -> float2, for the packed FP32x2
+// (FFMA2 / FADD2) statistics arithmetic of the fast epilogues
+__device__ __forceinline__ float2 bf2f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
 // Reduce-scatter over the 8 lanes sharing lane % 4 (lane bits 4, 3, 2; fixed tree) of two 8-column
 // partial-sum vectors a, b: each step keeps the half of the columns selected by the lane bit and
 // adds the partner's copy, so lane (k4, cg = lane >> 2) ends with column cg's totals in ra / rb --
@@ -1206,8 +1212,11 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                 const uint32_t yw[4] = {yr[it].x, yr[it].y, yr[it].z, yr[it].w};
                 uint32_t b8 = 0u;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  b8 |= (fmaf(bf(yw[j >> 1], j), bst[1][0][cl + j], bst[1][1][cl + j]) > 0.f ? 1u : 0u) << j;
+                for (int jp = 0; jp < 4; ++jp) {
+                  const float2 z = __ffma2_rn(bf2f2(yw[jp]), make_float2(bst[1][0][cl + 2 * jp], bst[1][0][cl + 2 * jp + 1]),
+                                              make_float2(bst[1][1][cl + 2 * jp], bst[1][1][cl + 2 * jp + 1]));
+                  b8 |= ((z.x > 0.f ? 1u : 0u) | (z.y > 0.f ? 2u : 0u)) << (2 * jp);
+                }
                 on[it] = b8;
               }
             }
@@ -1224,10 +1233,19 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                 const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
                 const uint32_t yw[4] = {yr[it].x, yr[it].y, yr[it].z, yr[it].w};
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const float g = ((on[it] >> j) & 1u) ? bf(gw[j >> 1], j) : 0.f;
-                  s1[j] += g;
-                  s2[j] += g * ((bf(yw[j >> 1], j) - bst[t][0][cl + j]) * bst[t][1][cl + j]);
+                for (int jp = 0; jp < 4; ++jp) {  // packed FP32x2: columns 2jp, 2jp + 1
+                  const float2 gv2 = bf2f2(gw[jp]);
+                  const float2 g = make_float2(((on[it] >> (2 * jp)) & 1u) ? gv2.x : 0.f,
+                                               ((on[it] >> (2 * jp + 1)) & 1u) ? gv2.y : 0.f);
+                  const float2 xh = __fmul2_rn(
+                      __fadd2_rn(bf2f2(yw[jp]), make_float2(-bst[t][0][cl + 2 * jp], -bst[t][0][cl + 2 * jp + 1])),
+                      make_float2(bst[t][1][cl + 2 * jp], bst[t][1][cl + 2 * jp + 1]));
+                  const float2 a1 = __fadd2_rn(make_float2(s1[2 * jp], s1[2 * jp + 1]), g);
+                  const float2 a2 = __ffma2_rn(g, xh, make_float2(s2[2 * jp], s2[2 * jp + 1]));
+                  s1[2 * jp] = a1.x;
+                  s1[2 * jp + 1] = a1.y;
+                  s2[2 * jp] = a2.x;
+                  s2[2 * jp + 1] = a2.y;
                 }
                 if (t + 1 < nbt) {
                   const size_t o = (size_t)(rbase + (lane >> 2) + 8 * it) * a.ldd + n0 + col0 + k4 * 8;
@@ -1295,13 +1313,17 @@ __global__ void __launch_bounds__(IgWarps<NPW, BN, I2C>::THREADS, IgWarps<NPW, B
                          : "r"(sDW + r * 64 + ((k4 ^ ((r >> 1) & 3)) << 4)));
             if (!tm.d_tma)
               *reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.D) + (size_t)(rbase + r) * a.ldd + n0 + col0 + k4 * 8) = raw;
-            if (want_stats) {
+            if (want_stats) {  // packed FP32x2: columns 2jp, 2jp + 1 per instruction
               const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float y = __uint_as_float((j & 1) ? (w4[j >> 1] & 0xffff0000u) : (w4[j >> 1] << 16));
-                s1[j] += y;
-                s2[j] = fmaf(y, y, s2[j]);
+              for (int jp = 0; jp < 4; ++jp) {
+                const float2 y = bf2f2(w4[jp]);
+                const float2 a1 = __fadd2_rn(make_float2(s1[2 * jp], s1[2 * jp + 1]), y);
+                const float2 a2 = __ffma2_rn(y, y, make_float2(s2[2 * jp], s2[2 * jp + 1]));
+                s1[2 * jp] = a1.x;
+                s1[2 * jp + 1] = a1.y;
+                s2[2 * jp] = a2.x;
+                s2[2 * jp + 1] = a2.y;
               }
             }
           }
