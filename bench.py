@@ -42,7 +42,7 @@ DEPTH = 56
 CLASSES = 10
 IN_SHAPE = (3, 32, 32)
 
-# --model: BASELINE.json configs this bench can run (configs[1] is the default bench line).
+# --model: BASELINE.json configs this bench can run (configs[4], ResNet-50, is the default bench line).
 # configs[2] asks for Adam, which the reference rejects (optim.py:70-71): it runs this package's
 # rule="adam" extension, checked against the oracle restatement only (tests/test_optim_gpu.py).
 MODELS = {
@@ -59,7 +59,7 @@ MODELS = {
 
 
 def select_model(args):
-    """Point the module-level workload constants at --model (default: configs[1], ResNet-56)."""
+    """Point the module-level workload constants at --model (default: configs[4], ResNet-50)."""
     global DEPTH, CLASSES, IN_SHAPE
     m = MODELS[args.model]
     DEPTH, CLASSES, IN_SHAPE = m["depth"], m["classes"], m["in_shape"]
