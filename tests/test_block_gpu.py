@@ -147,6 +147,12 @@ def test_pools_odd_maxpool_input():
     _check(*_run_block(layers, 8, last=True))
 
 
+def test_wide_dense_bias_head():
+    """A 600-way biased head (>= 512 columns: the bias gradient's BN-style column reduction takes the
+    column-parallel finalize launch) and a 1000-way one like ResNet-50's classifier."""
+    _check(*_run_block([P.dense(64, 600), P.relu(), P.dense(600, 1000)], 16, last=True))
+
+
 def test_mlp_kinds():
     layers = [P.dense(12, 16), P.relu(), P.dense(16, 12), P.tanh(), P.dense(12, 4)]
     _check(*_run_block(layers, 16, last=True))
