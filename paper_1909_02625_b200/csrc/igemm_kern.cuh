@@ -2282,6 +2282,12 @@ cudaError_t launch_bn(const dsp_igemm_args_t& a, int splits, cudaStream_t st) {
   static const int small_cap = getenv("DSP_B200_SMALL_CAP") ? atoi(getenv("DSP_B200_SMALL_CAP")) : 1;
   static const int small_m = getenv("DSP_B200_SMALL_M") ? atoi(getenv("DSP_B200_SMALL_M")) : 131072;
   if (small_cap && MODE != DSP_IGEMM_WGRAD && BN <= 64 && a.M <= small_m) grid = std::min(grid, num_sms);
+  {  // per-mode caps (A/B knobs): DSP_B200_FPROP_CAP / DSP_B200_DGRAD_CAP
+    static const int fcap = getenv("DSP_B200_FPROP_CAP") ? atoi(getenv("DSP_B200_FPROP_CAP")) : 0;
+    static const int dcap = getenv("DSP_B200_DGRAD_CAP") ? atoi(getenv("DSP_B200_DGRAD_CAP")) : 0;
+    const int mc = MODE == DSP_IGEMM_FPROP ? fcap : MODE == DSP_IGEMM_DGRAD ? dcap : 0;
+    if (mc > 0) grid = std::min(grid, mc);
+  }
   if (MODE != DSP_IGEMM_WGRAD) {  // each CTA owns one n-tile: grid must be a multiple of nt
     const int nt = (a.N + BN - 1) / BN;
     grid = std::max(nt, grid / nt * nt);
