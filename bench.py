@@ -79,7 +79,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cuts", default="", help="block boundaries (layer indices), default FLOP-balanced")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip k1_bp / conv_tensor_pipe / the resnet56 line")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip k1_bp / k_sweep_1gpu / conv_tensor_pipe / the resnet56 line")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     return ap.parse_args()
 
@@ -725,6 +726,21 @@ def run_b200(args):
                                "dsp_over_bp": main_run["value"] / bp["value"],
                                "config": "same model / batch / optimizer, K=1 (one block, plain BP)"}
             extras["conv_tensor_pipe"] = conv_tensor_pipe(torch, peaks, MODELS["resnet50"]["batch"])
+            # the metric's K = 2 / 8 with all K blocks on this ONE GPU (the K-GPU figures come from the
+            # driver's --gpus N runs): what the schedule costs per sample as K grows, same model and batch
+            sweep = {}
+            for kk in (2, 8):
+                if kk == K:
+                    continue
+                try:
+                    r = measure(args.model, kk, args.batch, args.steps, args.warmup, dev, 1, e2e=False,
+                                precision=args.precision, opt=opt_of(args))
+                    sweep[str(kk)] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"]}
+                except Exception as exc:  # an extra must never sink the bench line
+                    sweep[str(kk)] = {"value": None, "error": repr(exc)[:200]}
+            sweep["note"] = ("DSP with K blocks, all on one GPU (p_k=1, m_k=2(K-1-k), FLOP-balanced cuts); "
+                             "K=1 is k1_bp, K=%d the main value" % K)
+            extras["k_sweep_1gpu"] = sweep
         if args.model != "resnet56":
             r56 = measure("resnet56", 8 if world >= 8 else 4, MODELS["resnet56"]["batch"], args.steps, args.warmup, dev,
                           world, e2e=not args.no_e2e, precision=args.precision)
