@@ -2211,7 +2211,8 @@ static void dwarp_plan(const dsp_igemm_args_t& a, IgTma& tm, CUtensorMap& tmD) {
   // fence of the BN-finalize ticket, so the finalize no longer waits behind the CTA's last output
   // stores (4-8.5 us per launch, profiles/r01_fin_trace.log)
   static const bool no_dtma = getenv("DSP_B200_NO_DTMA") != nullptr;
-  if (no_dtma || (a.ldd * 2) % 16) return;
+  static const int dtma_min_bn = getenv("DSP_B200_DTMA_MIN_BN") ? atoi(getenv("DSP_B200_DTMA_MIN_BN")) : 64;
+  if (no_dtma || (a.ldd * 2) % 16 || BN < dtma_min_bn) return;
   {  // only into this device's memory (a multi-device engine's DGRAD may write a peer's ring slot)
     cudaPointerAttributes pa{};
     int dev = -1;
