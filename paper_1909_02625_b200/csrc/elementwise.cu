@@ -308,7 +308,11 @@ __global__ void __launch_bounds__(kThreads, 2) bn_bwd_reduce_k(const T* __restri
   pdl_wait();  // predecessor complete before any global access (successors launch at exit)
   constexpr int VE = V16<T>::N;
   __shared__ float red[kThreads][2 * VE];
-  const int G = Cp / VE;
+  // column window of this CTA (blockIdx.y): kThreads channel vectors at most (fp32 storage of
+  // 2048-channel tensors needs two windows)
+  const int cw0 = (int)blockIdx.y * kThreads * VE;
+  const int Cw = min(Cp - cw0, kThreads * VE);
+  const int G = Cw / VE;
   const int TR = kThreads / G;
   const int tid = threadIdx.x;
   const int cg = tid % G;
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 2) bn_bwd_reduce_k(const T* __restri
 #pragma unroll
   for (int i = 0; i < VE; ++i) s1[i] = s2[i] = 0.f;
   if (tr < TR) {
-    const int c0 = cg * VE;
+    const int c0 = cw0 + cg * VE;
     float mean[VE], inv[VE], msc[VE], msh[VE];
 #pragma unroll
     for (int i = 0; i < VE; ++i) {
@@ -384,17 +388,17 @@ __global__ void __launch_bounds__(kThreads, 2) bn_bwd_reduce_k(const T* __restri
     red[tid][VE + i] = s2[i];
   }
   __syncthreads();
-  for (int c = tid; c < Cp; c += kThreads) {
+  for (int c = tid; c < Cw; c += kThreads) {
     const int g = c / VE, e = c % VE;
     float a = 0.f, b = 0.f;
     for (int t = 0; t < TR; ++t) {
       a += red[t * G + g][e];
       b += red[t * G + g][VE + e];
     }
-    part[((size_t)blockIdx.x * 2 + 0) * Cp + c] = a;
-    part[((size_t)blockIdx.x * 2 + 1) * Cp + c] = b;
+    part[((size_t)blockIdx.x * 2 + 0) * Cp + cw0 + c] = a;
+    part[((size_t)blockIdx.x * 2 + 1) * Cp + cw0 + c] = b;
   }
-  if (fin.sem == nullptr) return;
+  if (fin.sem == nullptr) return;  // (the launcher never fuses the finalize into a windowed grid)
   // ---- last CTA to finish reduces the per-chunk partials in fixed order ----
   __shared__ int last;
   if (!last_cta_ticket(fin.sem, (int)gridDim.x, &last)) return;
@@ -1796,12 +1800,12 @@ cudaError_t bn_bwd_stats(int dtype, const void* gsrc, const void* mask, const vo
   // wide tensors: a column-parallel finalize launch instead of the last CTA's (DSP_B200_BNR_COLS
   // sets the width from which it is used; 0 = never)
   static const int cols_from = getenv("DSP_B200_BNR_COLS") ? atoi(getenv("DSP_B200_BNR_COLS")) : 512;
-  const bool sep = cols_from > 0 && Cp >= cols_from;
-  const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sep ? nullptr : sem};
   return dispatch_dtype(dtype, [&](auto t) {
     using T = decltype(t);
-    if (Cp / V16<T>::N > kThreads) return cudaErrorInvalidValue;
-    launch_k(bn_bwd_reduce_k<T>, chunks, kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
+    const int nwin = (Cp / V16<T>::N + kThreads - 1) / kThreads;  // column windows (grid y)
+    const bool sep = (cols_from > 0 && Cp >= cols_from) || nwin > 1;
+    const BnBwdFin fin{c_real, (double)M, gamma, stat, dgamma, dbeta, coef, sep ? nullptr : sem};
+    launch_k(bn_bwd_reduce_k<T>, dim3(chunks, nwin), kThreads, 0, st, (const T*)gsrc, (const T*)mask, (const T*)y, stat, part, M, Cp,
              rows, fin, relu_y, mbits);
     note_launch();
     if (sep) {
