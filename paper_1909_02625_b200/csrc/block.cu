@@ -403,7 +403,17 @@ int bn_backward_pair(dsp_block* b, const void* gsrc, const void* mask, const Con
 }
 
 // ------------------------------------------------------------------ layer forward / backward
-int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_t st) {
+// The stem's BN-apply + ReLU can ride on the max pool right after it (bf16, mask from y): the
+// stem's activation is then never materialised (DSP_B200_NO_POOL_FUSE=1 keeps both launches).
+bool stem_pool_fused(const dsp_block* b, const LayerP& l, const LayerP* next) {
+  static const bool off = getenv("DSP_B200_NO_POOL_FUSE") != nullptr;
+  return !off && next != nullptr && b->dtype == DSP_DTYPE_BF16 && l.d.kind == DSP_LAYER_CONV_BN_RELU &&
+         next->d.kind == DSP_LAYER_MAXPOOL && mask_of(b->ws + l.out) == nullptr && (l.convs[0].g.K % 8) == 0 &&
+         256 % (l.convs[0].g.K / 8) == 0;
+}
+
+int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_t st, bool skip_apply = false,
+                  const LayerP* fused_stem = nullptr) {
   const int dt = b->dtype;
   switch (l.d.kind) {
     case DSP_LAYER_DENSE: {
@@ -430,6 +440,12 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
       DSP_CUDA(avgpool_forward(dt, x, out, b->B, l.in_h * l.in_w, l.in_cp, st));
       return DSP_OK;
     case DSP_LAYER_MAXPOOL:
+      if (fused_stem != nullptr) {
+        const ConvP& c = fused_stem->convs[0];
+        DSP_CUDA(maxpool_bnrelu_forward(dt, b->ws + c.y, at<float>(b, c.stat), out, at<uint8_t>(b, l.arg), b->B,
+                                        l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
+        return DSP_OK;
+      }
       DSP_CUDA(maxpool_forward(dt, x, out, at<uint8_t>(b, l.arg), b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
       return DSP_OK;
     case DSP_LAYER_CONV_BN_RELU: {
@@ -440,7 +456,8 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
         x = b->ws + c.s2d_buf;
       }
       DSP_TRY(conv_fprop(b, c, x, st));
-      DSP_CUDA(bn_apply(dt, b->ws + c.y, at<float>(b, c.stat), nullptr, nullptr, nullptr, out, c.M(), c.g.K, 1, st));
+      if (!skip_apply)
+        DSP_CUDA(bn_apply(dt, b->ws + c.y, at<float>(b, c.stat), nullptr, nullptr, nullptr, out, c.M(), c.g.K, 1, st));
       return DSP_OK;
     }
     case DSP_LAYER_BASIC_UNIT:
@@ -876,7 +893,9 @@ extern "C" int dsp_block_forward(dsp_block_t* b, const void* x, void* y, int rec
       if (!y) return set_error(DSP_E_INVALID, "dsp_block_forward: fresh forward needs an output buffer");
       out = y;
     }
-    DSP_TRY(layer_forward(b, l, cur, out, st));
+    const bool fuse_next = stem_pool_fused(b, l, i + 1 < n ? &b->L[i + 1] : nullptr);
+    const bool fused_here = i > 0 && stem_pool_fused(b, b->L[i - 1], &l);
+    DSP_TRY(layer_forward(b, l, cur, out, st, fuse_next, fused_here ? &b->L[i - 1] : nullptr));
     cur = out;
   }
   if (b->is_last && y) {

@@ -1032,6 +1032,63 @@ __global__ void maxpool_fwd_bf16x2_k(const uint4* __restrict__ x, uint4* __restr
   }
 }
 
+// Stem BN-apply + ReLU fused into the max pool (bf16): each tap's y is normalised, rectified and
+// rounded to bf16 exactly as bn_apply would store it, then pooled as above -- the stem's full-
+// resolution activation is never written (nor re-read by the pool); its backward recomputes the
+// ReLU mask from y. The grid is a multiple of the channel-vector count, so a thread's 8 channels
+// (and their scale / shift) never change.
+__global__ void maxpool_bnrelu_fwd_bf16x2_k(const uint4* __restrict__ y, const float* __restrict__ stat,
+                                            uint4* __restrict__ out, uint2* __restrict__ arg, int B, int H, int W,
+                                            int P, int Q, int CV) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  const int Cp = CV * 8;
+  const int c0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) % CV) * 8;
+  float2 sc[4], sh[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    sc[j] = make_float2(stat[2 * Cp + c0 + 2 * j], stat[2 * Cp + c0 + 2 * j + 1]);
+    sh[j] = make_float2(stat[3 * Cp + c0 + 2 * j], stat[3 * Cp + c0 + 2 * j + 1]);
+  }
+  const int n = B * P * Q * CV;  // < 2^31 (checked by the launcher)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int cv = i % CV;
+    int t = i / CV;
+    const int q = t % Q;
+    t /= Q;
+    const int p = t % P;
+    const int b = t / P;
+    uint4 raw[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) raw[k] = __ldg(y + ((b * H + h) * W + w) * CV + cv);
+    }
+    uint32_t best[4] = {0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u}, ba[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if ((unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) {
+        const uint32_t yw[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 z = __ffma2_rn(make_float2(__uint_as_float(yw[j] << 16), __uint_as_float(yw[j] & 0xffff0000u)), sc[j],
+                                sh[j]);
+          z.x = fmaxf(z.x, 0.f);
+          z.y = fmaxf(z.y, 0.f);
+          uint32_t v;
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(v) : "f"(z.y), "f"(z.x));
+          const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&v),
+                                         *reinterpret_cast<const __nv_bfloat162*>(&best[j]));
+          best[j] = (v & m) | (best[j] & ~m);
+          ba[j] = ((uint32_t)k * 0x00010001u & m) | (ba[j] & ~m);
+        }
+      }
+    }
+    out[i] = make_uint4(best[0], best[1], best[2], best[3]);
+    arg[i] = make_uint2(__byte_perm(ba[0], ba[1], 0x6420), __byte_perm(ba[2], ba[3], 0x6420));
+  }
+}
+
 // Backward by output quads: thread (b, i, j, channel vector) writes input pixels (2i + di, 2j + dj)
 // from the (up to) four windows (i + di', j + dj') that contain them -- four 16-byte window loads,
 // no divergent tap search, every store a full 16 bytes. Each input pixel sums its windows in the
@@ -1927,6 +1984,16 @@ cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, i
                                                                             Cp);
     return note_launch(), cudaGetLastError();
   });
+}
+
+cudaError_t maxpool_bnrelu_forward(int dtype, const void* y, const float* stat, void* out, uint8_t* arg, int B, int H,
+                                   int W, int P, int Q, int Cp, cudaStream_t st) {
+  const int CV = Cp / 8;
+  if (dtype != DSP_DTYPE_BF16 || Cp % 8 || kThreads % CV || (int64_t)B * H * W * Cp >= (1ll << 31))
+    return cudaErrorInvalidValue;
+  launch_k(maxpool_bnrelu_fwd_bf16x2_k, grid_for((int64_t)B * P * Q * CV), kThreads, 0, st, (const uint4*)y, stat,
+           (uint4*)out, (uint2*)arg, B, H, W, P, Q, CV);
+  return note_launch(), cudaGetLastError();
 }
 
 cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void* dx, int B, int H, int W, int P, int Q,

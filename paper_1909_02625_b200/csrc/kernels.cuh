@@ -66,6 +66,9 @@ cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, 
 
 // 3x3 stride-2 pad-1 max pool and backward (argmax of the first max in (r,s) order).
 // arg: the argmax tap (0..8) of every output element, one byte each.
+// the stem's BN-apply + ReLU fused into the pool (bf16; y / stat = the stem conv's output and BN stats)
+cudaError_t maxpool_bnrelu_forward(int dtype, const void* y, const float* stat, void* out, uint8_t* arg, int B, int H,
+                                   int W, int P, int Q, int Cp, cudaStream_t st);
 cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, int B, int H, int W, int P, int Q,
                             int Cp, cudaStream_t st);
 cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void* dx, int B, int H, int W, int P,
