@@ -493,8 +493,11 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
 // below: the top BatchNorm(s) of the layer under this one, whose backward statistics the
 // final DGRAD (producing dx = that layer's upstream) accumulates; top_done: this layer's top
 // BN statistics were produced that way by the layer above (only the apply pass is left).
+// pool_u / pool (the fused stem + max pool, stem_pool_fused): the stem's BN backward re-gathers its
+// upstream from the pool's upstream pool_u and argmax taps instead of reading a stored gradient
 int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* dx, cudaStream_t st,
-                   const BnbFuse* below = nullptr, bool top_done = false) {
+                   const BnbFuse* below = nullptr, bool top_done = false, const void* pool_u = nullptr,
+                   const LayerP* pool = nullptr) {
   const int dt = b->dtype;
   switch (l.d.kind) {
     case DSP_LAYER_DENSE: {
@@ -535,7 +538,12 @@ int layer_backward(dsp_block* b, LayerP& l, const void* x, const void* u, void* 
     case DSP_LAYER_CONV_BN_RELU: {
       const ConvP& c = l.convs[0];
       void* dy = b->ws + b->S[0];
-      if (top_done)
+      if (pool != nullptr) {
+        DSP_CUDA(pool_bn_backward(dt, pool_u, at<uint8_t>(b, pool->arg), b->ws + c.y, at<float>(b, c.stat),
+                                  at<float>(b, b->bpart), c.co_real, b->params + c.gamma_off, b->grads + c.gamma_off,
+                                  b->grads + c.beta_off, at<float>(b, c.coef), dy, b->B, pool->in_h, pool->in_w,
+                                  pool->out_h, pool->out_w, c.g.K, st));
+      } else if (top_done)
         DSP_TRY(bn_backward_apply(b, u, mask_of(b->ws + l.out), c, dy, nullptr, nullptr, nullptr, st));
       else
         DSP_TRY(bn_backward_pair(b, u, mask_of(b->ws + l.out), c, dy, nullptr, nullptr, nullptr, st));
@@ -934,8 +942,24 @@ extern "C" int dsp_block_backward(dsp_block_t* b, const void* upstream, void* gr
            l.d.kind == DSP_LAYER_BOTTLENECK;
   };
   bool top_done = false;
+  const void* pool_u = nullptr;  // upstream of a max pool whose stem below is fused with it
   for (int i = n - 1; i >= 0; --i) {
     LayerP& l = b->L[i];
+    // fused stem + max pool: the pool's backward is folded into the stem's BN backward
+    if (l.d.kind == DSP_LAYER_MAXPOOL && i > 0 && stem_pool_fused(b, b->L[i - 1], &l)) {
+      pool_u = u;
+      top_done = false;
+      continue;
+    }
+    if (pool_u != nullptr) {
+      const void* x0 = i == 0 ? b->rec_x : (const void*)(b->ws + b->L[i - 1].out);
+      void* dx0 = i == 0 ? grad_in : (void*)(b->ws + b->G[i & 1]);
+      DSP_TRY(layer_backward(b, l, x0, nullptr, dx0, st, nullptr, false, pool_u, &b->L[i + 1]));
+      pool_u = nullptr;
+      top_done = false;
+      u = dx0;
+      continue;
+    }
     const void* x = i == 0 ? b->rec_x : (const void*)(b->ws + b->L[i - 1].out);
     void* dx = i == 0 ? grad_in : (void*)(b->ws + b->G[i & 1]);
     // the layer below's top BN statistics ride on this layer's final DGRAD (g = dx * (x > 0))

@@ -1166,6 +1166,189 @@ __global__ void maxpool_bwd_quad_k(const T* __restrict__ u, const uint8_t* __res
   }
 }
 
+// ---- the stem's BN backward fused with the max-pool backward (bf16, stem mask from y) ----
+// The pool's input gradient dx (the stem activation's gradient, 411 MB at ResNet-50 B=256) is never
+// stored: both passes of the stem's BN backward re-gather it per output quad (2x2 stem pixels from
+// their <= 4 pooling windows: u + argmax taps, 154 MB, L2-resident) exactly as maxpool_bwd_quad_k
+// sums it, then g = dx * (relu(y*scale + shift) > 0).
+struct PoolQuad {
+  uint4 u[2][2];
+  uint2 a[2][2];
+};
+
+__device__ __forceinline__ void pool_quad_load(const uint4* __restrict__ u, const uint2* __restrict__ arg, int b,
+                                               int i, int j, int P, int Q, int CV, int cv, PoolQuad& pq) {
+#pragma unroll
+  for (int di = 0; di < 2; ++di)
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj) {
+      const bool ok = i + di < P && j + dj < Q;
+      const int64_t o = (((int64_t)b * P + i + di) * Q + j + dj) * CV + cv;
+      pq.u[di][dj] = ok ? __ldg(u + o) : make_uint4(0u, 0u, 0u, 0u);
+      pq.a[di][dj] = ok ? __ldg(arg + o) : make_uint2(0xffffffffu, 0xffffffffu);
+    }
+}
+
+// dx of stem pixel (2i + dh, 2j + dw), 8 channels, in the generic pool backward's summation order
+__device__ __forceinline__ void pool_quad_dx(const PoolQuad& pq, int dh, int dw, float (&acc)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  auto term = [&](int di, int dj, uint32_t k) {
+    const uint32_t uw[4] = {pq.u[di][dj].x, pq.u[di][dj].y, pq.u[di][dj].z, pq.u[di][dj].w};
+    const uint32_t aw[2] = {pq.a[di][dj].x, pq.a[di][dj].y};
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (((aw[e >> 2] >> (8 * (e & 3))) & 0xffu) == k)
+        acc[e] += __uint_as_float((e & 1) ? (uw[e >> 1] & 0xffff0000u) : (uw[e >> 1] << 16));
+  };
+  if (dh == 0 && dw == 0) {
+    term(0, 0, 4);
+  } else if (dh == 0) {
+    term(0, 1, 3);
+    term(0, 0, 5);
+  } else if (dw == 0) {
+    term(1, 0, 1);
+    term(0, 0, 7);
+  } else {
+    term(1, 1, 0);
+    term(1, 0, 2);
+    term(0, 1, 6);
+    term(0, 0, 8);
+  }
+}
+
+// pass 1: per-chunk partial sums of g and g * xhat (chunk = a contiguous quad range; thread =
+// (quad lane, channel vector); fixed-order CTA reduction) -> part[chunk][2][Cp]
+__global__ void __launch_bounds__(256) pool_bn_bwd_reduce_k(const uint4* __restrict__ u, const uint2* __restrict__ arg,
+                                                          const uint4* __restrict__ y, const float* __restrict__ stat,
+                                                          float* __restrict__ part, int B, int H, int W, int P, int Q,
+                                                          int CV, int quads_per_chunk) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  __shared__ float red[256][16];
+  const int Cp = CV * 8;
+  const int tid = threadIdx.x, cv = tid % CV, ql = tid / CV, QL = 256 / CV;
+  const int c0 = cv * 8;
+  float mean[8], inv[8], sc[8], sh[8], s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    mean[e] = stat[c0 + e];
+    inv[e] = stat[Cp + c0 + e];
+    sc[e] = stat[2 * Cp + c0 + e];
+    sh[e] = stat[3 * Cp + c0 + e];
+    s1[e] = s2[e] = 0.f;
+  }
+  const int64_t nq = (int64_t)B * P * Q;
+  const int64_t q0 = (int64_t)blockIdx.x * quads_per_chunk, q1 = min(nq, q0 + quads_per_chunk);
+  for (int64_t qd = q0 + ql; qd < q1; qd += QL) {
+    const int j = (int)(qd % Q);
+    const int64_t t = qd / Q;
+    const int i = (int)(t % P), b = (int)(t / P);
+    PoolQuad pq;
+    pool_quad_load(u, arg, b, i, j, P, Q, CV, cv, pq);
+    uint4 yr[2][2];
+#pragma unroll
+    for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+      for (int dw = 0; dw < 2; ++dw) {
+        const int h = 2 * i + dh, w = 2 * j + dw;
+        yr[dh][dw] = (h < H && w < W) ? __ldg(y + (((int64_t)b * H + h) * W + w) * CV + cv) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+    for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+      for (int dw = 0; dw < 2; ++dw) {
+        if (2 * i + dh >= H || 2 * j + dw >= W) continue;
+        float g[8];
+        pool_quad_dx(pq, dh, dw, g);
+        // the stored dx is bf16: round exactly as the unfused pool backward's store does
+#pragma unroll
+        for (int e = 0; e < 8; ++e) g[e] = __bfloat162float(__float2bfloat16(g[e]));
+        const uint32_t yw[4] = {yr[dh][dw].x, yr[dh][dw].y, yr[dh][dw].z, yr[dh][dw].w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float yy = __uint_as_float((e & 1) ? (yw[e >> 1] & 0xffff0000u) : (yw[e >> 1] << 16));
+          const float ge = fmaf(yy, sc[e], sh[e]) > 0.f ? g[e] : 0.f;
+          s1[e] += ge;
+          s2[e] += ge * ((yy - mean[e]) * inv[e]);
+        }
+      }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[tid][e] = s1[e];
+    red[tid][8 + e] = s2[e];
+  }
+  __syncthreads();
+  for (int c = tid; c < Cp; c += 256) {
+    const int g = c / 8, e = c % 8;
+    float a = 0.f, bsum = 0.f;
+    for (int l = 0; l < QL; ++l) {
+      a += red[l * CV + g][e];
+      bsum += red[l * CV + g][8 + e];
+    }
+    part[((size_t)blockIdx.x * 2 + 0) * Cp + c] = a;
+    part[((size_t)blockIdx.x * 2 + 1) * Cp + c] = bsum;
+  }
+}
+
+// pass 2: dy = coef0 * (g - coef1 - xhat * coef2), written per stem pixel (grid a multiple of CV:
+// a thread's channels, and their coefficients, never change)
+__global__ void pool_bn_bwd_apply_k(const uint4* __restrict__ u, const uint2* __restrict__ arg,
+                                    const uint4* __restrict__ y, const float* __restrict__ stat,
+                                    const float* __restrict__ coef, uint4* __restrict__ dy, int B, int H, int W, int P,
+                                    int Q, int CV) {
+  pdl_wait();  // predecessor complete before any global access (successors launch at exit)
+  const int Cp = CV * 8;
+  const int c0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) % CV) * 8;
+  float k0[8], k1[8], km[8], kq[8], sc[8], sh[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int c = c0 + e;
+    k0[e] = coef[c];
+    k1[e] = coef[Cp + c];
+    km[e] = stat[c];
+    kq[e] = stat[Cp + c] * coef[2 * Cp + c];
+    sc[e] = stat[2 * Cp + c];
+    sh[e] = stat[3 * Cp + c];
+  }
+  const int n = B * P * Q * CV;  // < 2^31 (checked by the launcher)
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const int cv = idx % CV;
+    int t = idx / CV;
+    const int j = t % Q;
+    t /= Q;
+    const int i = t % P, b = t / P;
+    PoolQuad pq;
+    pool_quad_load(u, arg, b, i, j, P, Q, CV, cv, pq);
+#pragma unroll
+    for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+      for (int dw = 0; dw < 2; ++dw) {
+        const int h = 2 * i + dh, w = 2 * j + dw;
+        if (h >= H || w >= W) continue;
+        const int64_t o = (((int64_t)b * H + h) * W + w) * CV + cv;
+        const uint4 yv = __ldg(y + o);
+        float g[8];
+        pool_quad_dx(pq, dh, dw, g);
+        const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+        float out[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float ge0 = __bfloat162float(__float2bfloat16(g[e]));
+          const float yy = __uint_as_float((e & 1) ? (yw[e >> 1] & 0xffff0000u) : (yw[e >> 1] << 16));
+          const float ge = fmaf(yy, sc[e], sh[e]) > 0.f ? ge0 : 0.f;
+          out[e] = k0[e] * (ge - k1[e] - (yy - km[e]) * kq[e]);
+        }
+        uint4 r;
+        uint32_t* rw = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2)
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(rw[e2]) : "f"(out[2 * e2 + 1]), "f"(out[2 * e2]));
+        dy[o] = r;
+      }
+  }
+}
+
 // ------------------------------------------------------------------ space-to-depth stem
 // One thread per s2d pixel: its cps channels = 4 sub-positions (i, j) x c input channels.
 // the ResNet-50 stem case: bf16, 8-channel input pixels (one 16-byte load each), 16 s2d channels
@@ -1993,6 +2176,25 @@ cudaError_t maxpool_bnrelu_forward(int dtype, const void* y, const float* stat, 
     return cudaErrorInvalidValue;
   launch_k(maxpool_bnrelu_fwd_bf16x2_k, grid_for((int64_t)B * P * Q * CV), kThreads, 0, st, (const uint4*)y, stat,
            (uint4*)out, (uint2*)arg, B, H, W, P, Q, CV);
+  return note_launch(), cudaGetLastError();
+}
+
+cudaError_t pool_bn_backward(int dtype, const void* u, const uint8_t* arg, const void* y, const float* stat, float* part,
+                             int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef, void* dy, int B,
+                             int H, int W, int P, int Q, int Cp, cudaStream_t st) {
+  const int CV = Cp / 8;
+  if (dtype != DSP_DTYPE_BF16 || Cp % 8 || 256 % CV || (int64_t)B * H * W * Cp >= (1ll << 31)) return cudaErrorInvalidValue;
+  const int64_t nq = (int64_t)B * P * Q;
+  const int chunks = (int)std::min<int64_t>(296, nq);
+  const int qpc = (int)((nq + chunks - 1) / chunks);
+  launch_k(pool_bn_bwd_reduce_k, chunks, 256, 0, st, (const uint4*)u, (const uint2*)arg, (const uint4*)y, stat, part, B, H,
+           W, P, Q, CV, qpc);
+  note_launch();
+  launch_k(bn_bwd_finalize_cols_k, (Cp + 31) / 32, 1024, 0, st, (const float*)part, chunks, Cp, c_real,
+           (double)B * H * W, gamma, stat, dgamma, dbeta, coef);
+  note_launch();
+  launch_k(pool_bn_bwd_apply_k, grid_for(nq * CV), kThreads, 0, st, (const uint4*)u, (const uint2*)arg, (const uint4*)y,
+           stat, (const float*)coef, (uint4*)dy, B, H, W, P, Q, CV);
   return note_launch(), cudaGetLastError();
 }
 

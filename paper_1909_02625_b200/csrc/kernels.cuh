@@ -69,6 +69,11 @@ cudaError_t avgpool_backward(int dtype, const void* u, void* dx, int B, int HW, 
 // the stem's BN-apply + ReLU fused into the pool (bf16; y / stat = the stem conv's output and BN stats)
 cudaError_t maxpool_bnrelu_forward(int dtype, const void* y, const float* stat, void* out, uint8_t* arg, int B, int H,
                                    int W, int P, int Q, int Cp, cudaStream_t st);
+// the stem's BN backward fused with the max-pool backward (bf16, stem mask from y): reduce + finalize
+// + apply, the pool's input gradient re-gathered from u / arg instead of stored
+cudaError_t pool_bn_backward(int dtype, const void* u, const uint8_t* arg, const void* y, const float* stat, float* part,
+                             int c_real, const float* gamma, float* dgamma, float* dbeta, float* coef, void* dy, int B,
+                             int H, int W, int P, int Q, int Cp, cudaStream_t st);
 cudaError_t maxpool_forward(int dtype, const void* x, void* out, uint8_t* arg, int B, int H, int W, int P, int Q,
                             int Cp, cudaStream_t st);
 cudaError_t maxpool_backward(int dtype, const void* u, const uint8_t* arg, void* dx, int B, int H, int W, int P,
