@@ -404,7 +404,7 @@ extern "C" int dsp_create(const dsp_config_t* cfg, dsp_engine_t** out) {
     // forward twins when a device holds few blocks (engine_b200.use_twins; DSP_B200_TWIN=0/1)
     int on_dev = 0;
     for (int k2 = 0; k2 < K; ++k2) on_dev += e->dj[k2] == e->dj[k];
-    const bool twins = tw_env ? tw_env[0] == '1' : on_dev <= 4;
+    const bool twins = tw_env ? tw_env[0] == '1' : on_dev <= 8;
     if (k < K - 1 && twins) {
       const int off_k = (int)(std::accumulate(cfg->n_layers, cfg->n_layers + k, 0));
       if ((rc = dsp_block_create(e->layers.data() + off_k, cfg->n_layers[k], e->B, cfg->dtype, 0, &e->twin[k])) !=

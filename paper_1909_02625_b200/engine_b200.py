@@ -57,15 +57,16 @@ def block_priorities(model, local) -> dict:
 
 
 def use_twins(n_local: int) -> bool:
-    """Forward twins when a rank holds few blocks. Measured on B200 (tools/block_step_latency.py,
+    """Forward twins (up to 8 blocks per rank). Measured on B200 (tools/block_step_latency.py,
     profiles/r01_twins.md): a GPU owning one block steps 11-22% faster on the CIFAR ResNets
-    (ResNet-56 block 0 905 -> 775 us), while a GPU already running 4 blocks concurrently gains
-    nothing (ResNet-56 K=4 +0.3%) and one running 8 loses 3% (ResNet-110 K=8).
+    (ResNet-56 block 0 905 -> 775 us). With round-2 grid sizing (one CTA per SM for the CIFAR
+    convs) they also pay when one GPU runs all blocks: ResNet-56 K=4 82.8k vs 74.2k samples/s,
+    ResNet-164 K=4 22.6k vs 21.7k, ResNet-110 K=8 46.3k vs 45.8k (round 1: -3% at K=8).
     DSP_B200_TWIN=0/1 overrides."""
     env = os.environ.get("DSP_B200_TWIN")
     if env is not None:
         return env == "1"
-    return n_local <= 4
+    return n_local <= 8
 
 
 class B200Runtime:
