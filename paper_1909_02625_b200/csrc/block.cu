@@ -412,8 +412,10 @@ bool stem_pool_fused(const dsp_block* b, const LayerP& l, const LayerP* next) {
          256 % (l.convs[0].g.K / 8) == 0;
 }
 
+// tape = false (a fresh forward): what only the recorded pass's backward reads -- max-pool argmax
+// taps, residual units' ReLU mask bits -- is not written
 int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_t st, bool skip_apply = false,
-                  const LayerP* fused_stem = nullptr) {
+                  const LayerP* fused_stem = nullptr, bool tape = true) {
   const int dt = b->dtype;
   switch (l.d.kind) {
     case DSP_LAYER_DENSE: {
@@ -442,11 +444,13 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
     case DSP_LAYER_MAXPOOL:
       if (fused_stem != nullptr) {
         const ConvP& c = fused_stem->convs[0];
-        DSP_CUDA(maxpool_bnrelu_forward(dt, b->ws + c.y, at<float>(b, c.stat), out, at<uint8_t>(b, l.arg), b->B,
-                                        l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
+        DSP_CUDA(maxpool_bnrelu_forward(dt, b->ws + c.y, at<float>(b, c.stat), out,
+                                        tape ? at<uint8_t>(b, l.arg) : nullptr, b->B, l.in_h, l.in_w, l.out_h,
+                                        l.out_w, l.in_cp, st));
         return DSP_OK;
       }
-      DSP_CUDA(maxpool_forward(dt, x, out, at<uint8_t>(b, l.arg), b->B, l.in_h, l.in_w, l.out_h, l.out_w, l.in_cp, st));
+      DSP_CUDA(maxpool_forward(dt, x, out, tape ? at<uint8_t>(b, l.arg) : nullptr, b->B, l.in_h, l.in_w, l.out_h,
+                               l.out_w, l.in_cp, st));
       return DSP_OK;
     case DSP_LAYER_CONV_BN_RELU: {
       const ConvP& c = l.convs[0];
@@ -474,7 +478,7 @@ int layer_forward(dsp_block* b, LayerP& l, const void* x, void* out, cudaStream_
       }
       const ConvP& cl = l.convs[nmain - 1];
       DSP_TRY(conv_fprop(b, cl, cur, st));
-      uint8_t* mb = l.mbits ? at<uint8_t>(b, l.mbits) : nullptr;
+      uint8_t* mb = (l.mbits && tape) ? at<uint8_t>(b, l.mbits) : nullptr;
       if (l.proj) {
         const ConvP& cs = l.convs[nmain];
         DSP_TRY(conv_fprop(b, cs, x, st));
@@ -903,7 +907,7 @@ extern "C" int dsp_block_forward(dsp_block_t* b, const void* x, void* y, int rec
     }
     const bool fuse_next = stem_pool_fused(b, l, i + 1 < n ? &b->L[i + 1] : nullptr);
     const bool fused_here = i > 0 && stem_pool_fused(b, b->L[i - 1], &l);
-    DSP_TRY(layer_forward(b, l, cur, out, st, fuse_next, fused_here ? &b->L[i - 1] : nullptr));
+    DSP_TRY(layer_forward(b, l, cur, out, st, fuse_next, fused_here ? &b->L[i - 1] : nullptr, record != 0));
     cur = out;
   }
   if (b->is_last && y) {

@@ -937,6 +937,7 @@ __global__ void maxpool_fwd_k(const T* __restrict__ x, T* __restrict__ out, uint
 #pragma unroll
     for (int e = 0; e < VE; e += 4)
       packed[e / 4] = (uint32_t)ba[e] | ((uint32_t)ba[e + 1] << 8) | ((uint32_t)ba[e + 2] << 16) | ((uint32_t)ba[e + 3] << 24);
+    if (arg == nullptr) continue;
     if constexpr (VE == 8) {
       *reinterpret_cast<uint2*>(arg + i * VE) = make_uint2(packed[0], packed[1]);
     } else {
@@ -1028,7 +1029,8 @@ __global__ void maxpool_fwd_bf16x2_k(const uint4* __restrict__ x, uint4* __restr
       }
     }
     out[i] = make_uint4(best[0], best[1], best[2], best[3]);
-    arg[i] = make_uint2(__byte_perm(ba[0], ba[1], 0x6420), __byte_perm(ba[2], ba[3], 0x6420));
+    if (arg != nullptr)  // (a fresh forward keeps no argmax: only the recorded pass's backward reads it)
+      arg[i] = make_uint2(__byte_perm(ba[0], ba[1], 0x6420), __byte_perm(ba[2], ba[3], 0x6420));
   }
 }
 
@@ -1085,7 +1087,8 @@ __global__ void maxpool_bnrelu_fwd_bf16x2_k(const uint4* __restrict__ y, const f
       }
     }
     out[i] = make_uint4(best[0], best[1], best[2], best[3]);
-    arg[i] = make_uint2(__byte_perm(ba[0], ba[1], 0x6420), __byte_perm(ba[2], ba[3], 0x6420));
+    if (arg != nullptr)  // (a fresh forward keeps no argmax: only the recorded pass's backward reads it)
+      arg[i] = make_uint2(__byte_perm(ba[0], ba[1], 0x6420), __byte_perm(ba[2], ba[3], 0x6420));
   }
 }
 
