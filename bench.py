@@ -135,7 +135,10 @@ def config_dict_for(model: str, K: int, batch: int, world: int, opt: str = "") -
 
 
 def config_dict(args, K, world):
-    return config_dict_for(args.model, K, args.batch, world, opt_desc(args))
+    d = config_dict_for(args.model, K, args.batch, world, opt_desc(args))
+    d["cuts"] = ([int(c) for c in args.cuts.split(",")] if args.cuts
+                 else "FLOP-balanced residual-unit cuts (SURVEY 8)")
+    return d
 
 
 # ------------------------------------------------------------------ clocks
