@@ -156,3 +156,15 @@ def test_device_of_block_config_matches_single_device():
         with pytest.raises(P.DspError, match="device"):
             nm, _ = twin_models(layers, [1, 2, 3], seed=3)
             NativeEngine(nm, cfg, 8, sched, devices=[0, 1, 1, 1])
+
+
+def test_resnet50_shapes_native_matches_python_engine():
+    """configs[4]'s network (ResNet-50, FLOP-balanced K=4 cuts, default queues) at a small batch,
+    past the graph-capture horizon: the engine C-ABI reproduces the Python engine bitwise with every
+    ResNet-50 kernel path in play (space-to-depth stem fused with the max pool, im2col / 2-D TMA
+    operands, TMA-stored epilogue slabs, stride-2 parity DGRAD, projection units)."""
+    layers = P.resnet50_layers()
+    bounds = P.flop_balanced_boundaries(layers, 4)
+    cfg = P.default_queue_config(4)
+    py, pm, ne, *_ = _pair(layers, bounds, cfg.p, cfg.m, 4, 14, (3, 224, 224), 1000, decay=False)
+    _same(py, pm, ne)
