@@ -153,10 +153,11 @@ def test_bp_gradient_at_trained_state(name, precision):
     assert lerr <= OP_LOSS[precision], lerr
 
 
-def test_resnet50_config4_early_steps_vs_oracle():
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_resnet50_config4_early_steps_vs_oracle(precision):
     """configs[4]'s network (ResNet-50, K=4 FLOP-balanced cuts, default queues, SUM momentum) on a
-    2-sample batch for 5 steps, device bf16 vs the float64 oracle engine: the FIFO / staleness
-    schedule exact, the first steps' loss and gradient norms within the bf16 EARLY bounds (every
+    2-sample batch for 5 steps, device (bf16 / fp32) vs the float64 oracle engine: the FIFO /
+    staleness schedule exact, the loss and gradient norms within 3x the emulated floor + EARLY (every
     ResNet-50 kernel path in play: space-to-depth stem fused with the max pool, im2col / 2-D TMA
     operands, TMA-stored slabs, parity-split stride-2 DGRAD, projection units, 1000-way head)."""
     from tests.gpu_util import twin_models
@@ -167,7 +168,8 @@ def test_resnet50_config4_early_steps_vs_oracle():
     B, steps = 2, 5
     pool = R.synthetic_batches(3, B, (3, 224, 224), 1000, seed=5)
     pm, _ = twin_models(layers, bounds, seed=0)
-    eng = P.TrainEngine(pm, cfg, cycle(pool), P.LrSchedule(0.05), rule="sum", beta=0.9, weight_decay=5e-4)
+    eng = P.TrainEngine(pm, cfg, cycle(pool), P.LrSchedule(0.05), rule="sum", beta=0.9, weight_decay=5e-4,
+                        precision=precision)
     eng.run(steps)
     def oracle_run(mode):
         _, om2 = twin_models(layers, bounds, seed=0)
@@ -178,17 +180,17 @@ def test_resnet50_config4_early_steps_vs_oracle():
         return sorted(ref.records, key=lambda r: (r.step, r.block))
 
     got = eng.log.sorted()
-    want, emu = oracle_run("f64"), oracle_run("bf16")
+    want, emu = oracle_run("f64"), oracle_run("bf16" if precision == "bf16" else "f32")
     assert [(r.step, r.block, r.batch_index) for r in got] == [(r.step, r.block, r.batch_index) for r in want]
     # K=4, p_k=1: the head first sees a real activation at step cum_p[3] = 3 and every block's first
     # real (non-zero-packet) gradient arrives at step cum_p[k] + m_k = 6, so through step 4 the
     # parameters move only by the zero-packet weight decay -- no trajectory chaos yet. Every record
     # is held to FLOOR_X x the same record's error of the oracle with bf16 storage emulated (+ the
     # EARLY bounds as the absolute slack); steps 3-4 check the full 4-block forward's loss.
-    le, ge = EARLY["bf16"]
+    le, ge = EARLY[precision]
     assert any(r.loss is not None and r.step >= 3 for r in got)
     last = [(rg, rw, re) for rg, rw, re in zip(got, want, emu) if rw.loss is not None][-1]
-    print(f"\nresnet50 step {last[0].step}: loss dev {last[0].loss:.4f} f64 {last[1].loss:.4f} emu {last[2].loss:.4f}; "
+    print(f"\nresnet50 {precision} step {last[0].step}: loss dev {last[0].loss:.4f} f64 {last[1].loss:.4f} emu {last[2].loss:.4f}; "
           f"head grad norm dev {last[0].grad_norm:.3f} f64 {last[1].grad_norm:.3f} emu {last[2].grad_norm:.3f}")
     for rg, rw, re in zip(got, want, emu):
         if rw.loss is not None:
