@@ -199,3 +199,146 @@ def test_resnet50_config4_early_steps_vs_oracle(precision):
         fg = abs(re.grad_norm - rw.grad_norm)
         assert abs(rg.grad_norm - rw.grad_norm) <= FLOOR_X * fg + ge * max(rw.grad_norm, 1e-3), (
             rg.step, rg.block, rg.grad_norm, rw.grad_norm, re.grad_norm)
+
+
+# configs[2] / configs[3] at their full depth on a 4-sample batch. Learning rates are below the
+# bench's so the comparison stays out of the chaotic regime long enough to be discriminating: at
+# B=4 ResNet-164's gradient norm grows ~260x from the head to block 0 (15k at block 0's first real
+# gradient), and the oracle's own float32 run leaves its float64 one by 5-16 % within a few updates
+# (tools: the emulated floor printed by the test).
+DEEP_CONFIGS = {
+    # ResNet-110, K=8 blocks, Adam (the bench's rule / beta / s): block 0's first real gradient
+    # arrives at step cum_p[0] + m_0 = 14, so 17 steps update every block with real gradients
+    "resnet110_k8_adam": dict(depth=110, classes=10, K=8, bottleneck=False, steps=17,
+                              opt=dict(rule="adam", beta=0.0, s=1.0, lr=1e-4)),
+    # ResNet-164 (bottleneck units), K=4, CIFAR-100 head, SUM momentum: steps 0-6 (block 0's
+    # first real gradient at step 6)
+    "resnet164_k4": dict(depth=164, classes=100, K=4, bottleneck=True, steps=7,
+                         opt=dict(rule="sum", beta=0.9, s=1.0, lr=5e-4)),
+}
+_DEEP_ORACLE = {}
+
+
+def _deep_oracle(name, mode):
+    """(sorted records, final params) of the float64 oracle engine, or with the storage of the device
+    precision emulated (the arithmetic floor the device run is held against)."""
+    key = (name, mode)
+    if key not in _DEEP_ORACLE:
+        from tests.gpu_util import twin_models
+
+        c = DEEP_CONFIGS[name]
+        layers, bounds, cfg, pool = _deep_setup(c)
+        _, om = twin_models(layers, bounds, seed=0)
+        o = c["opt"]
+        with R.storage(mode):
+            ref = R.Engine(om, R.validate_config(cfg.p, cfg.m), R.cycle(pool), R.LrSchedule(o["lr"]), rule=o["rule"],
+                           beta=o["beta"], s=o["s"], weight_decay=5e-4)
+            ref.run(c["steps"])
+        _DEEP_ORACLE[key] = (sorted(ref.records, key=lambda r: (r.step, r.block)),
+                             [np.asarray(b.params, dtype=np.float64) for b in om.blocks])
+    return _DEEP_ORACLE[key]
+
+
+def _deep_setup(c):
+    layers = (P.resnet_cifar_bottleneck_layers(c["depth"], c["classes"]) if c["bottleneck"]
+              else P.resnet_cifar_layers(c["depth"], c["classes"]))
+    bounds = P.flop_balanced_boundaries(layers, c["K"])
+    cfg = P.default_queue_config(c["K"])
+    pool = R.synthetic_batches(3, 4, (3, 32, 32), c["classes"], seed=7)
+    return layers, bounds, cfg, pool
+
+
+def _as_golden(records, params):
+    g = {"loss": np.array([np.nan if r.loss is None else r.loss for r in records]),
+         "grad_norm": np.array([r.grad_norm for r in records]), "stride": 1}
+    for k, p in enumerate(params):
+        g[f"final_{k}"] = p
+    return g
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("name", sorted(DEEP_CONFIGS))
+def test_deep_configs_vs_oracle(name, precision):
+    """configs[2] (ResNet-110, K=8, Adam) and configs[3] (ResNet-164 bottleneck, K=4) at full depth
+    through TrainEngine(backend="b200") vs the float64 oracle engine, past every block's first real
+    gradient: the FIFO / staleness schedule exact; steps 0-2 within the EARLY bounds; the whole run's
+    (loss, grad norm, final params) divergence within FLOOR_X x the divergence of the oracle run with
+    the device's storage emulated (+ FLOOR_ABS), as the configs[0] / [1] trajectory tests."""
+    from tests.gpu_util import twin_models
+
+    c = DEEP_CONFIGS[name]
+    layers, bounds, cfg, pool = _deep_setup(c)
+    pm, _ = twin_models(layers, bounds, seed=0)
+    o = c["opt"]
+    eng = P.TrainEngine(pm, cfg, cycle(pool), P.LrSchedule(o["lr"]), rule=o["rule"], beta=o["beta"], s=o["s"],
+                        weight_decay=5e-4, precision=precision)
+    eng.run(c["steps"])
+    got = eng.log.sorted()
+    want, want_p = _deep_oracle(name, "f64")
+    emu, emu_p = _deep_oracle(name, "bf16" if precision == "bf16" else "f32")
+    assert [(r.step, r.block, r.batch_index) for r in got] == [(r.step, r.block, r.batch_index) for r in want]
+    first_real = max(k + m for k, m in enumerate(cfg.m))  # cum_p[k] + m_k with p_k = 1
+    assert c["steps"] > first_real
+    g = _as_golden(want, want_p)
+    le, ge = EARLY[precision]
+    for r, w in zip(got, want):
+        if r.step < EARLY_STEPS:
+            if w.loss is not None:
+                assert abs(r.loss - w.loss) <= le * max(1.0, abs(w.loss)), (r.step, r.loss, w.loss)
+            assert abs(r.grad_norm - w.grad_norm) <= ge * max(w.grad_norm, 1e-3), (r.step, r.block, r.grad_norm,
+                                                                                  w.grad_norm)
+    div = divergence(got, [b.params for b in pm.blocks], g)
+    floor = divergence(emu, emu_p, g)
+    print(f"\n{name} {precision}: {c['steps']} steps (loss, gn, params) {np.array2string(div, precision=2)}"
+          f" floor {np.array2string(floor, precision=2)}")
+    assert np.all(np.isfinite(div))
+    assert np.all(div <= FLOOR_X * floor + FLOOR_ABS), (div, floor)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("name", sorted(DEEP_CONFIGS))
+def test_deep_bp_gradient_vs_oracle(name, precision):
+    """Teacher-forced at full depth (no trajectory involved): the device's chained BP gradient of every
+    block of configs[2] / configs[3] at the initial parameters vs the float64 oracle's on the same
+    batch, within OP_X x the oracle's own error with the device's arithmetic emulated (+ OP_ABS)."""
+    import torch
+
+    from paper_1909_02625_b200.deviation import DeviceOperators
+    from paper_1909_02625_b200.runtime import pack_input
+    from tests.gpu_util import to_oracle_layers, twin_models
+
+    c = DEEP_CONFIGS[name]
+    layers, bounds, cfg, pool = _deep_setup(c)
+    pm, _ = twin_models(layers, bounds, seed=0)
+    eng = P.TrainEngine(pm, cfg, cycle(pool), P.LrSchedule(c["opt"]["lr"]), rule=c["opt"]["rule"],
+                        beta=c["opt"]["beta"], s=c["opt"]["s"], weight_decay=5e-4, precision=precision)
+    params = [b.params.copy() for b in pm.blocks]
+    x, lab = pool[0]
+    B = len(lab)
+    ops = DeviceOperators(pm, B, device=eng.rt.device, stream=eng.rt.stream, dtype=eng.rt.dtype_code)
+    dev = eng.rt.device
+    xd = pack_input(np.asarray(x), (3, 32, 32), dev, eng.rt.stream, dtype=eng.rt.dtype_code)
+    ld = torch.from_numpy(np.asarray(lab, dtype=np.int64)).to(dev)
+    got = ops.bp_gradient([torch.from_numpy(p.astype(np.float32)).to(dev) for p in params], xd, ld)
+    eng.rt.stream.synchronize()
+    loss_dev = float(ops.loss.item())
+
+    def oracle(mode, acc):
+        with R.storage(mode, acc=acc):
+            om = R.build_model(to_oracle_layers(layers), bounds)
+            for b, p in zip(om.blocks, params):
+                b.params = np.asarray(p, dtype=np.float32).astype(np.float64)
+            return R.bp_gradient(om, x, lab)
+
+    want, loss_ref = oracle("f64", "f64")
+    emu, loss_emu = oracle(*(("f32", "f32") if precision == "fp32" else ("bf16", "f64")))
+    errs = np.array([rel_err(gd.double().cpu().numpy(), w) for gd, w in zip(got, want)])
+    floor = np.array([rel_err(e, w) for e, w in zip(emu, want)])
+    lerr = abs(loss_dev - loss_ref) / max(1.0, abs(loss_ref))
+    lfloor = abs(loss_emu - loss_ref) / max(1.0, abs(loss_ref))
+    print(f"\n{name} BP operator {precision}: per-block grad rel err {np.array2string(errs, precision=2)}"
+          f" floor {np.array2string(floor, precision=2)} loss {lerr:.1e} floor {lfloor:.1e}")
+    # bf16 storage at init on a 4-sample batch: the oracle's own emulated run is ~1.2 away in
+    # relative L2 (ReLU masks flip through 50+ BatchNorms); the device must track that floor
+    assert np.all(errs <= OP_X * floor + OP_ABS[precision]), (errs, floor)
+    assert lerr <= OP_X * lfloor + OP_LOSS[precision], (lerr, lfloor)
