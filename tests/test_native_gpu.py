@@ -168,3 +168,21 @@ def test_resnet50_shapes_native_matches_python_engine():
     cfg = P.default_queue_config(4)
     py, pm, ne, *_ = _pair(layers, bounds, cfg.p, cfg.m, 4, 14, (3, 224, 224), 1000, decay=False)
     _same(py, pm, ne)
+
+
+@pytest.mark.parametrize("name", ["resnet110_k8_adam", "resnet164_k4"])
+def test_deep_configs_native_matches_python_engine(name):
+    """configs[2] (ResNet-110, K=8, Adam, weight decay) and configs[3] (ResNet-164 bottleneck, K=4)
+    at full depth, past the graph-capture horizon and every block's first real gradient: the engine
+    C-ABI reproduces the Python engine bitwise (params, loss / grad-norm checksums, staleness)."""
+    if name == "resnet110_k8_adam":
+        layers, K, classes, rule, beta, lr = P.resnet_cifar_layers(110, 10), 8, 10, "adam", 0.0, 1e-3
+    else:
+        layers, K, classes, rule, beta, lr = P.resnet_cifar_bottleneck_layers(164, 100), 4, 100, "sum", 0.9, 0.01
+    bounds = P.flop_balanced_boundaries(layers, K)
+    cfg = P.default_queue_config(K)
+    steps = max(k + m for k, m in enumerate(cfg.m)) + 6
+    py, pm, ne, *_ = _pair(layers, bounds, cfg.p, cfg.m, 8, steps, (3, 32, 32), classes, rule=rule, beta=beta,
+                           lr=lr, wd=5e-4)
+    _same(py, pm, ne)
+    assert ne.realized_staleness() == list(cfg.m)
